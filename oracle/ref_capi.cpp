@@ -1,0 +1,381 @@
+// TEST INFRASTRUCTURE (oracle) — not product code.
+//
+// A flat extern "C" driver around the *unmodified* reference library compiled
+// from /root/reference/proj/src (see oracle/Makefile). It exists so that
+// Python tests, the golden-vector generator and bench.py's CPU baseline can
+// call the reference through ctypes. Every function composes the reference's
+// own public API; nothing here re-implements reference arithmetic.
+//
+// Array conventions (shared with include/flowfem_b200.h):
+//   * images and vertex fields: row-major W*H doubles, vertex id = y*W + x
+//     (proj/include/flowfem/mesh.hpp:35);
+//   * "terms10": the ten DataTerms planes a11,a12,a13,a22,a23,a33,f1,f2,f3,c
+//     (proj/include/flowfem/imaging.hpp:61-67), each W*H;
+//   * per-triangle fields: 2*(W-1)*(H-1) doubles, lower/upper triangle of
+//     cell (x,y) at 2*(y*(W-1)+x) and +1 (proj/src/mesh.cpp:29);
+//   * "planes3": u1, u2, mt planes back to back, each W*H.
+//   * the flat partition format is documented in include/flowfem_b200.h.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include <omp.h>
+
+#include "flowfem/adapt.hpp"
+#include "flowfem/assembly.hpp"
+#include "flowfem/imaging.hpp"
+#include "flowfem/linsolve.hpp"
+#include "flowfem/mesh.hpp"
+#include "flowfem/pipeline.hpp"
+#include "flowfem/schwarz.hpp"
+
+using namespace flowfem;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  } catch (...) {
+    g_err = "unknown exception";
+    return 1;
+  }
+}
+
+Image to_image(int W, int H, const double* p) {
+  Image img(W, H);
+  std::memcpy(img.data.data(), p, sizeof(double) * W * H);
+  return img;
+}
+
+DataTerms to_terms(int W, int H, const double* t10) {
+  DataTerms dt;
+  dt.width = W;
+  dt.height = H;
+  const size_t n = static_cast<size_t>(W) * H;
+  std::vector<double>* f[10] = {&dt.a11, &dt.a12, &dt.a13, &dt.a22, &dt.a23,
+                                &dt.a33, &dt.f1,  &dt.f2,  &dt.f3,  &dt.c};
+  for (int k = 0; k < 10; ++k) f[k]->assign(t10 + k * n, t10 + (k + 1) * n);
+  return dt;
+}
+
+void from_terms(const DataTerms& dt, double* t10) {
+  const size_t n = static_cast<size_t>(dt.width) * dt.height;
+  const std::vector<double>* f[10] = {&dt.a11, &dt.a12, &dt.a13, &dt.a22, &dt.a23,
+                                      &dt.a33, &dt.f1,  &dt.f2,  &dt.f3,  &dt.c};
+  for (int k = 0; k < 10; ++k) std::memcpy(t10 + k * n, f[k]->data(), sizeof(double) * n);
+}
+
+RegField to_reg(int ntri, const double* alpha, const double* lambda) {
+  RegField r;
+  r.alpha.assign(alpha, alpha + ntri);
+  r.lambda.assign(lambda, lambda + ntri);
+  return r;
+}
+
+FlowState to_state(int W, int H, const double* p3) {
+  FlowState s(W, H);
+  const size_t n = static_cast<size_t>(W) * H;
+  std::memcpy(s.u1.data(), p3, sizeof(double) * n);
+  std::memcpy(s.u2.data(), p3 + n, sizeof(double) * n);
+  std::memcpy(s.mt.data(), p3 + 2 * n, sizeof(double) * n);
+  return s;
+}
+
+void from_state(const FlowState& s, double* p3) {
+  const size_t n = s.u1.size();
+  std::memcpy(p3, s.u1.data(), sizeof(double) * n);
+  std::memcpy(p3 + n, s.u2.data(), sizeof(double) * n);
+  std::memcpy(p3 + 2 * n, s.mt.data(), sizeof(double) * n);
+}
+
+std::vector<int> flatten_partition(const Partition& p) {
+  std::vector<int> out = {p.width, p.height, p.parts_x, p.parts_y, p.overlap,
+                          static_cast<int>(p.parts.size())};
+  for (const auto& s : p.parts) {
+    const int r[8] = {s.core.x0, s.core.y0, s.core.x1, s.core.y1,
+                      s.ext.x0,  s.ext.y0,  s.ext.x1,  s.ext.y1};
+    out.insert(out.end(), r, r + 8);
+    out.push_back(static_cast<int>(s.boundary.size()));
+    out.push_back(static_cast<int>(s.neighbors.size()));
+  }
+  for (const auto& s : p.parts) {
+    out.insert(out.end(), s.boundary.begin(), s.boundary.end());
+    for (const auto& nb : s.neighbors) {
+      out.push_back(nb.part);
+      out.push_back(nb.band.x0);
+      out.push_back(nb.band.y0);
+      out.push_back(nb.band.x1);
+      out.push_back(nb.band.y1);
+      out.push_back(static_cast<int>(nb.gamma.size()));
+      out.insert(out.end(), nb.gamma.begin(), nb.gamma.end());
+    }
+  }
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_set_threads(int n) {
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+}
+
+int ref_gaussian_smooth(int W, int H, const double* in, double sigma, double* out) {
+  return guard([&] {
+    const Image r = gaussian_smooth(to_image(W, H, in), sigma);
+    std::memcpy(out, r.data.data(), sizeof(double) * W * H);
+  });
+}
+
+int ref_compute_derivatives(int W, int H, const double* f0, const double* f1, double* fx,
+                            double* fy, double* ft, double* f) {
+  return guard([&] {
+    const DerivativeField d = compute_derivatives(to_image(W, H, f0), to_image(W, H, f1));
+    const size_t n = static_cast<size_t>(W) * H;
+    std::memcpy(fx, d.fx.data(), n * sizeof(double));
+    std::memcpy(fy, d.fy.data(), n * sizeof(double));
+    std::memcpy(ft, d.ft.data(), n * sizeof(double));
+    std::memcpy(f, d.f.data(), n * sizeof(double));
+  });
+}
+
+int ref_build_data_terms(int W, int H, const double* fx, const double* fy, const double* ft,
+                         const double* f, double rho, double* out10) {
+  return guard([&] {
+    DerivativeField d;
+    d.width = W;
+    d.height = H;
+    const size_t n = static_cast<size_t>(W) * H;
+    d.fx.assign(fx, fx + n);
+    d.fy.assign(fy, fy + n);
+    d.ft.assign(ft, ft + n);
+    d.f.assign(f, f + n);
+    from_terms(build_data_terms(d, rho), out10);
+  });
+}
+
+// run_on_frames' imaging prefix (proj/src/pipeline.cpp:49-52)
+int ref_frames_to_terms(int W, int H, const double* f0, const double* f1, double sigma,
+                        double rho, double* out10) {
+  return guard([&] {
+    const Image s0 = gaussian_smooth(to_image(W, H, f0), sigma);
+    const Image s1 = gaussian_smooth(to_image(W, H, f1), sigma);
+    from_terms(build_data_terms(compute_derivatives(s0, s1), rho), out10);
+  });
+}
+
+int ref_choose_split(int W, int H, int n_parts, int* px, int* py, double* ratio) {
+  return guard([&] {
+    const SplitChoice s = choose_split(W, H, n_parts);
+    *px = s.parts_x;
+    *py = s.parts_y;
+    *ratio = s.ratio;
+  });
+}
+
+// returns the number of splits written (<= cap) or -1
+int ref_enumerate_splits(int W, int H, int n_parts, int* px, int* py, double* ratio, int cap) {
+  int count = -1;
+  if (guard([&] {
+        const auto all = enumerate_splits(W, H, n_parts);
+        count = 0;
+        for (const auto& s : all) {
+          if (count >= cap) break;
+          px[count] = s.parts_x;
+          py[count] = s.parts_y;
+          ratio[count] = s.ratio;
+          ++count;
+        }
+      }))
+    return -1;
+  return count;
+}
+
+// flat partition; returns the required length (write happens if cap suffices), -1 on error
+long ref_build_partition(int W, int H, int px, int py, int ov, int* buf, long cap) {
+  long need = -1;
+  if (guard([&] {
+        const std::vector<int> flat = flatten_partition(build_partition(W, H, px, py, ov));
+        need = static_cast<long>(flat.size());
+        if (buf && cap >= need) std::memcpy(buf, flat.data(), flat.size() * sizeof(int));
+      }))
+    return -1;
+  return need;
+}
+
+// y = A x and b for the unconstrained global system (assembly.cpp:32-166, 240-249)
+int ref_assemble_apply(int W, int H, const double* t10, const double* alpha,
+                       const double* lambda, int nc, const double* x3, double* y3, double* b3) {
+  return guard([&] {
+    const TriMesh m = build_pixel_mesh(W, H);
+    const DataTerms dt = to_terms(W, H, t10);
+    const RegField reg = to_reg(m.n_triangles, alpha, lambda);
+    const SparseSystem s = assemble(m, dt, reg, nc);
+    const FlowState st = to_state(W, H, x3);
+    std::vector<double> x = flatten_state(s, st), y;
+    spmv(s, x, y);
+    const FlowState ys = expand_solution(m, s, y);
+    const FlowState bs = expand_solution(m, s, s.rhs);
+    from_state(ys, y3);
+    from_state(bs, b3);
+  });
+}
+
+// monolithic solve of the global system with the reference solver
+// method 0: cg_solve (Jacobi PCG, true residual), 1: direct (SparseCholesky + refinement)
+int ref_solve_monolithic(int W, int H, const double* t10, const double* alpha,
+                         const double* lambda, int nc, int method, double tol,
+                         const double* warm3, double* out3, int* iters, double* res) {
+  return guard([&] {
+    const TriMesh m = build_pixel_mesh(W, H);
+    const DataTerms dt = to_terms(W, H, t10);
+    const RegField reg = to_reg(m.n_triangles, alpha, lambda);
+    const SparseSystem s = assemble(m, dt, reg, nc);
+    SolverConfig cfg;
+    cfg.method = method == 1 ? SolveMethod::DirectCholesky : SolveMethod::ConjugateGradient;
+    cfg.cg_tolerance = tol;
+    std::vector<double> warm;
+    if (warm3) warm = flatten_state(s, to_state(W, H, warm3));
+    SolveReport rep;
+    const std::vector<double> x = solve(s, cfg, &rep, warm3 ? &warm : nullptr);
+    from_state(expand_solution(m, s, x), out3);
+    if (iters) *iters = rep.iterations;
+    if (res) *res = rep.residual;
+  });
+}
+
+int ref_error_indicator(int W, int H, const double* t10, const double* alpha,
+                        const double* lambda, const double* u3, int nc, double* eta,
+                        double* eta_max) {
+  return guard([&] {
+    const TriMesh m = build_pixel_mesh(W, H);
+    const IndicatorField ind = error_indicator(m, to_terms(W, H, t10),
+                                               to_reg(m.n_triangles, alpha, lambda),
+                                               to_state(W, H, u3), nc);
+    if (eta) std::memcpy(eta, ind.eta.data(), ind.eta.size() * sizeof(double));
+    *eta_max = ind.eta_max;
+  });
+}
+
+int ref_update_alpha(int ntri, const double* alpha, const double* lambda, const double* eta,
+                     double eta_max, double kappa, double eta_thr, double alpha_th,
+                     double* alpha_out) {
+  return guard([&] {
+    IndicatorField ind;
+    ind.eta.assign(eta, eta + ntri);
+    ind.eta_max = eta_max;
+    AdaptConfig cfg;
+    cfg.kappa = kappa;
+    cfg.eta_threshold = eta_thr;
+    cfg.alpha_th = alpha_th;
+    const RegField out = update_alpha(to_reg(ntri, alpha, lambda), ind, cfg);
+    std::memcpy(alpha_out, out.alpha.data(), ntri * sizeof(double));
+  });
+}
+
+// The converged-pass protocol composed from the
+// reference's public functions: n_passes x {monolithic solve to tol, error_indicator,
+// update_alpha}, then one final solve. CG passes are warm-started from the previous
+// pass. Outputs the final state, the final alpha, eta_max per update and the
+// solver iterations per solve (n_passes + 1 entries).
+int ref_converged_chain(int W, int H, const double* f0, const double* f1, double sigma,
+                        double rho, double alpha0, double lambda0, int nc, int n_passes,
+                        double kappa, double eta_thr, double alpha_th, double tol, int method,
+                        double* out3, double* alpha_out, double* eta_max_out, int* iters_out,
+                        double* seconds_out) {
+  return guard([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    const Image s0 = gaussian_smooth(to_image(W, H, f0), sigma);
+    const Image s1 = gaussian_smooth(to_image(W, H, f1), sigma);
+    const DataTerms dt = build_data_terms(compute_derivatives(s0, s1), rho);
+    const TriMesh m = build_pixel_mesh(W, H);
+    RegField reg = uniform_reg(m, alpha0, lambda0);
+    AdaptConfig acfg;
+    acfg.kappa = kappa;
+    acfg.eta_threshold = eta_thr;
+    acfg.alpha_th = alpha_th;
+    SolverConfig cfg;
+    cfg.method = method == 1 ? SolveMethod::DirectCholesky : SolveMethod::ConjugateGradient;
+    cfg.cg_tolerance = tol;
+    std::vector<double> x;
+    FlowState state(W, H);
+    for (int pass = 0; pass <= n_passes; ++pass) {
+      const SparseSystem s = assemble(m, dt, reg, nc);
+      SolveReport rep;
+      x = solve(s, cfg, &rep, x.empty() ? nullptr : &x);
+      if (iters_out) iters_out[pass] = rep.iterations;
+      state = expand_solution(m, s, x);
+      if (pass == n_passes) break;
+      const IndicatorField ind = error_indicator(m, dt, reg, state, nc);
+      if (eta_max_out) eta_max_out[pass] = ind.eta_max;
+      reg = update_alpha(reg, ind, acfg);
+    }
+    from_state(state, out3);
+    if (alpha_out) std::memcpy(alpha_out, reg.alpha.data(), reg.alpha.size() * sizeof(double));
+    if (seconds_out)
+      *seconds_out =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+// The reference's own Schwarz loop (proj/src/schwarz.cpp:162-319), literal semantics.
+// alpha/lambda are in-out. method 0: CG subdomain solves, 1: Cholesky.
+int ref_schwarz_solve(int W, int H, const double* t10, double* alpha, double* lambda, int px,
+                      int py, int ov, int n_iters, int workers, int nc, int adapt, int n_adapt,
+                      double kappa, double eta_thr, double alpha_th, int method, double cg_tol,
+                      double* out3, double* increments, double* eta_max_out) {
+  return guard([&] {
+    const TriMesh m = build_pixel_mesh(W, H);
+    const DataTerms dt = to_terms(W, H, t10);
+    RegField reg = to_reg(m.n_triangles, alpha, lambda);
+    const Partition part = build_partition(W, H, px, py, ov);
+    SchwarzOptions opt;
+    opt.n_iters = n_iters;
+    opt.workers = workers;
+    opt.components = nc;
+    opt.adapt.enabled = adapt != 0;
+    opt.adapt.n_adapt = n_adapt;
+    opt.adapt.kappa = kappa;
+    opt.adapt.eta_threshold = eta_thr;
+    opt.adapt.alpha_th = alpha_th;
+    opt.solver.method =
+        method == 1 ? SolveMethod::DirectCholesky : SolveMethod::ConjugateGradient;
+    opt.solver.cg_tolerance = cg_tol;
+    SchwarzStats stats;
+    const FlowState g = schwarz_solve(m, dt, reg, part, opt, &stats);
+    from_state(g, out3);
+    std::memcpy(alpha, reg.alpha.data(), reg.alpha.size() * sizeof(double));
+    std::memcpy(lambda, reg.lambda.data(), reg.lambda.size() * sizeof(double));
+    if (increments)
+      std::memcpy(increments, stats.increments.data(), stats.increments.size() * sizeof(double));
+    if (eta_max_out)
+      std::memcpy(eta_max_out, stats.eta_max.data(), stats.eta_max.size() * sizeof(double));
+  });
+}
+
+// Discrete energy (assembly.cpp:201-238), test-only optimality check.
+int ref_energy(int W, int H, const double* t10, const double* alpha, const double* lambda,
+               const double* u3, int nc, double* e) {
+  return guard([&] {
+    const TriMesh m = build_pixel_mesh(W, H);
+    *e = energy(m, to_terms(W, H, t10), to_reg(m.n_triangles, alpha, lambda),
+                to_state(W, H, u3), nc);
+  });
+}
+
+}  // extern "C"
