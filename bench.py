@@ -1,0 +1,305 @@
+#!/usr/bin/env python
+"""Benchmark: full adaptive flow solve (frames -> u1, u2, mt with all alpha passes) in
+Mpixel/s, fp64, on the B200 path; plus the HBM roofline of the dominant kernel (the
+band forward/backward solve of the Schwarz preconditioner) and the CPU reference.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
+
+One step = one run_on_frames over one synthetic frame pair of the configuration (all
+n_passes alpha updates and n_passes+1 converged Schwarz-PCG solves). ``value`` is timed
+with CUDA events on the launching stream with frames already in HBM; ``e2e`` goes through
+the host API (host frames in, u3 + alpha out). For N > 1 (torchrun) every rank solves its
+own frame pair (replicas; weak scaling) and the time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "full flow solve Mpixel/s (fp64)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("FFB_BENCH_CONFIG", "c2"))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def profiled_traffic(config):
+    """dram bytes per launch of the band-solve kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "asm_traffic.json")) as fh:
+            d = json.load(fh)
+        return d.get(config)
+    except Exception:
+        return None
+
+
+def run_config_for(cfg, ff):
+    return ff.RunConfig(sigma=cfg.sigma, rho=cfg.rho, alpha0=cfg.alpha0, lambda0=cfg.lambda0,
+                        parts=cfg.parts, overlap=cfg.overlap, adapt_iters=cfg.n_passes,
+                        kappa=cfg.kappa, eta_threshold=cfg.eta_threshold,
+                        cg_tolerance=cfg.tol)
+
+
+def cpu_reference_step(f0, f1, cfg):
+    """The reference's own CPU path (oracle/_ref; else the C port), converged-pass protocol."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    o = pyoracle.REF or pyoracle.PORT
+    cores = os.cpu_count() or 1
+    o.set_threads(cores)
+    t = time.perf_counter()
+    r = o.converged_chain(f0, f1, cfg.sigma, rho=cfg.rho, alpha0=cfg.alpha0,
+                          lambda0=cfg.lambda0, n_passes=cfg.n_passes, kappa=cfg.kappa,
+                          thr=cfg.eta_threshold, tol=cfg.tol)
+    return time.perf_counter() - t, o.kind, cores, r
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def bench_reference(args, cfg, f0, f1):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    npx = cfg.H * cfg.W
+    for _ in range(min(args.warmup, 1)):
+        cpu_reference_step(f0, f1, cfg)
+    times = []
+    kind = cores = None
+    for _ in range(args.steps):
+        dt, kind, cores, _r = cpu_reference_step(f0, f1, cfg)
+        times.append(dt)
+    tot = sum(times)
+    v = npx * len(times) / tot / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "Mpixel/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1),
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "H": cfg.H, "W": cfg.W, "parts": cfg.parts,
+                   "overlap": cfg.overlap, "n_passes": cfg.n_passes, "tol": cfg.tol},
+        "cpu_baseline": {"value": v, "unit": "Mpixel/s", "cores": cores, "kind": kind,
+                         "sample": f"{args.steps} full converged-pass solves of {cfg.name} "
+                                   f"(reference Jacobi-CG, monolithic), {cpu_model()}"},
+        "e2e": {"value": v, "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    from paper_1508_02977_b200 import synth
+    f0, f1, _, cfg = synth.make(args.config, seed=rank)
+    if args.impl == "reference":
+        bench_reference(args, cfg, f0, f1)
+        return
+
+    import numpy as np
+    import torch
+    from paper_1508_02977_b200 import flowfem as ff
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    ctx = ff.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    rc = run_config_for(cfg, ff)
+    H, W = cfg.H, cfg.W
+    npx = H * W
+    d_f0 = torch.from_numpy(f0).to(dev)
+    d_f1 = torch.from_numpy(f1).to(dev)
+    d_u3 = torch.empty((3, H, W), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > L2
+
+    def step():
+        return ff.run_on_frames_device(d_f0.data_ptr(), d_f1.data_ptr(), W, H, d_u3.data_ptr(),
+                                       rc, ctx)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = ff.kernel_launches()
+    stats = []
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))  # evict L2 between steps
+            ev0[k].record(stream)
+            stats.append(step())
+            ev1[k].record(stream)
+        torch.cuda.synchronize()
+    launches = ff.kernel_launches() - launches0
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    tot_ms = sum(step_ms)
+    if pg:
+        t = torch.tensor([tot_ms], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = world * npx * args.steps / (tot_ms / 1e3) / 1e6
+
+    # end to end through the host API (pinned host frames in, u3 + alpha out)
+    ctx.set_stream(None)
+    pin0 = torch.from_numpy(f0).pin_memory().numpy()
+    pin1 = torch.from_numpy(f1).pin_memory().numpy()
+    ff.run_on_frames(pin0, pin1, rc, ctx)  # warm
+    e2e_times = []
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = ff.run_on_frames(pin0, pin1, rc, ctx)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_times) / len(e2e_times)
+    if pg:
+        t = torch.tensor([e2e_s], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": world * npx / e2e_s / 1e6, "unit": "Mpixel/s",
+           "h2d_bytes_per_step": 2 * npx * 8,
+           "d2h_bytes_per_step": 3 * npx * 8 + 2 * (W - 1) * (H - 1) * 8,
+           "timing": "host wall clock around the blocking run_on_frames call"}
+
+    if rank != 0:
+        if pg:
+            pg.destroy_process_group()
+        return
+    s = stats[-1]
+    peak, peak_kind = measured_peak()
+    asm_bytes = 16.0 * s.factor_doubles  # band factor read forward + backward
+    achieved = asm_bytes / (s.ms_asm_per_iter * 1e-3) / 1e9 if s.ms_asm_per_iter > 0 else None
+    iters_total = s.pcg_iterations
+    line = {
+        "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "H": H, "W": W, "parts": f"{s.parts_x}x{s.parts_y}",
+                   "overlap": cfg.overlap, "n_passes": cfg.n_passes, "tol": cfg.tol,
+                   "parallelism": "replicas" if world > 1 else "1gpu",
+                   "l2": "flushed (256 MB write) between steps; band factors > L2"},
+        "gpu_launches": int(launches),
+        "e2e": e2e,
+        "roofline": {"bound": "hbm", "kernel": "k_asm (band fwd/bwd solve)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": profiled_traffic(cfg.name), "peak_kind": peak_kind,
+                     "bytes_per_launch": asm_bytes, "ms_per_launch": s.ms_asm_per_iter},
+        "solver": {"pcg_iterations_per_step": iters_total, "iters": s.iters,
+                   "ms_terms": s.ms_terms, "ms_factor": s.ms_factor, "ms_pcg": s.ms_pcg,
+                   "ms_adapt": s.ms_adapt, "ms_total": s.ms_total,
+                   "iter_bytes": s.iter_bytes,
+                   "pcg_iter_gbs": (s.iter_bytes * iters_total / (s.ms_pcg * 1e-3) / 1e9)
+                   if s.ms_pcg > 0 else None},
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        dt, kind, cores, _ = cpu_reference_step(f0, f1, cfg)
+        line["cpu_baseline"] = {"value": npx / dt / 1e6, "unit": "Mpixel/s", "cores": cores,
+                                "kind": kind,
+                                "sample": f"1 full converged-pass solve of {cfg.name} "
+                                          f"({dt:.1f} s; reference Jacobi-CG), {cpu_model()}"}
+    print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,162 @@
+/* flowfem_b200 — C-ABI of the B200-native adaptive-alpha Horn–Schunck + illumination
+ * solver (arXiv 1508.02977 hot path). Plain C: pointers, sizes, status codes; no torch
+ * or C++ types cross this boundary.
+ *
+ * Every entry point replaces a function of the reference library `flowfem`
+ * (/root/reference/proj/include/flowfem/*.hpp); the citation is given per function.
+ * Reference paths below are relative to /root/reference/proj.
+ *
+ * Conventions (identical to the test oracle, oracle/flowfem_port.h):
+ *   - images / vertex fields: row-major H x W doubles, vertex id = y*W + x
+ *     (include/flowfem/mesh.hpp:35);
+ *   - "terms10": the ten DataTerms planes a11,a12,a13,a22,a23,a33,f1,f2,f3,c
+ *     (include/flowfem/imaging.hpp:61-67), each W*H, back to back;
+ *   - per-triangle fields: 2*(W-1)*(H-1) doubles, lower/upper triangle of cell (x,y)
+ *     at 2*(y*(W-1)+x) and +1 (src/mesh.cpp:29-35);
+ *   - "planes3": u1, u2, mt planes back to back, each W*H (FlowState,
+ *     include/flowfem/assembly.hpp:11-22); with 2 components mt is written as 0;
+ *   - flat partition format (Partition, include/flowfem/schwarz.hpp:23-48):
+ *       [W, H, px, py, ov, np,
+ *        per part p: core.x0 y0 x1 y1, ext.x0 y0 x1 y1, n_boundary, n_neighbors   (10 ints),
+ *        then per part p: boundary[n_boundary],
+ *                         per neighbor: part, band.x0 y0 x1 y1, n_gamma, gamma[n_gamma]]
+ *
+ * Errors: every call returns 0 on success and non-zero on failure; ffb_last_error()
+ * returns the message of the calling thread's last failure, prefixed with the
+ * reference module the way the reference's std::runtime_error messages are
+ * ("linsolve.cg: …", "schwarz.build_partition: …", "imaging.compute_derivatives: …").
+ * Host buffers are owned by the caller; device state is owned by the context.
+ * One host thread per context; one context per GPU (one process per GPU).
+ */
+#ifndef FLOWFEM_B200_H
+#define FLOWFEM_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FFB_ABI_VERSION 1
+
+typedef struct ffb_ctx ffb_ctx;
+
+/* flowfem::RunConfig (include/flowfem/pipeline.hpp:15-33), solver-relevant fields. */
+typedef struct ffb_run_config {
+  double sigma;          /* pre-smoothing of both frames (imaging.cpp:33) */
+  double rho;            /* data-term smoothing (imaging.cpp:108) */
+  double alpha0;         /* uniform_reg (assembly.cpp:9-14) */
+  double lambda0;
+  int illumination;      /* 1 -> 3 components (u1,u2,mt), 0 -> 2 */
+  int parts;             /* choose_split(W,H,parts) (schwarz.cpp:32-44) */
+  int overlap;           /* build_partition overlap (schwarz.cpp:54) */
+  int adapt;             /* AdaptConfig::enabled */
+  int n_passes;          /* AdaptConfig::n_adapt: alpha updates; n_passes+1 solves */
+  double kappa;          /* update_alpha (adapt.cpp:101-112) */
+  double eta_threshold;
+  double alpha_th;       /* <= 0 -> alpha0/100 (pipeline.cpp:71) */
+  double tol;            /* SolverConfig::cg_tolerance, true relative residual */
+  int max_iters;         /* 0 -> 10 * unknowns (linsolve.cpp:333) */
+} ffb_run_config;
+
+#define FFB_MAX_SOLVES 64
+
+typedef struct ffb_run_stats {
+  int parts_x, parts_y;
+  int n_solves;                         /* n_passes + 1 */
+  int iters[FFB_MAX_SOLVES];            /* PCG iterations per solve */
+  double residual[FFB_MAX_SOLVES];      /* final ||b-Ax||/||b|| per solve */
+  double eta_max[FFB_MAX_SOLVES];       /* per alpha update */
+  long long pcg_iterations;             /* sum of iters */
+  double ms_terms, ms_factor, ms_pcg, ms_adapt, ms_total; /* CUDA-event phase times */
+  double factor_doubles;                /* sum_i npad_i (kd_i + 1): band factor storage */
+  double iter_bytes;                    /* algorithmic HBM bytes per PCG iteration */
+  double ms_asm_per_iter;               /* mean duration of the band fwd/bwd kernel */
+} ffb_run_stats;
+
+/* ---- library ---------------------------------------------------------------------- */
+const char* ffb_last_error(void);
+int ffb_abi_version(void);
+/* number of device kernels this library launched since load (evidence counter) */
+long long ffb_kernel_launches(void);
+
+/* ---- context (one GPU) ------------------------------------------------------------ */
+int ffb_create(ffb_ctx** ctx, int device);
+int ffb_destroy(ffb_ctx* ctx);
+/* Launch on the caller's CUDA stream (cudaStream_t passed as void*); NULL restores the
+ * context's own stream. Lets a host framework bracket the solve with its own events. */
+int ffb_set_stream(ffb_ctx* ctx, void* stream);
+
+/* ---- imaging: include/flowfem/imaging.hpp ----------------------------------------- */
+/* gaussian_smooth (imaging.hpp:42-44, imaging.cpp:33-63) */
+int ffb_gaussian_smooth(ffb_ctx* ctx, int W, int H, const double* in, double sigma,
+                        double* out);
+/* compute_derivatives (imaging.hpp:54-56, imaging.cpp:65-106) */
+int ffb_compute_derivatives(ffb_ctx* ctx, int W, int H, const double* f0, const double* f1,
+                            double* fx, double* fy, double* ft, double* f);
+/* build_data_terms (imaging.hpp:69, imaging.cpp:108-138) */
+int ffb_build_data_terms(ffb_ctx* ctx, int W, int H, const double* fx, const double* fy,
+                         const double* ft, const double* f, double rho, double* out10);
+/* run_on_frames' imaging prefix: smooth x2 -> derivatives -> data terms (pipeline.cpp:49-52) */
+int ffb_frames_to_terms(ffb_ctx* ctx, int W, int H, const double* f0, const double* f1,
+                        double sigma, double rho, double* out10);
+
+/* ---- decomposition: include/flowfem/schwarz.hpp (host-only, bit-exact) ------------- */
+/* enumerate_splits (schwarz.hpp:16, schwarz.cpp:16-30); returns count written or -1 */
+int ffb_enumerate_splits(int W, int H, int n_parts, int* px, int* py, double* ratio, int cap);
+/* choose_split (schwarz.hpp:19, schwarz.cpp:32-44) */
+int ffb_choose_split(int W, int H, int n_parts, int* px, int* py, double* ratio);
+/* build_partition (schwarz.hpp:52, schwarz.cpp:54-128): returns the flat length
+ * (writes when cap suffices) or -1 */
+long ffb_build_partition(int W, int H, int px, int py, int ov, int* buf, long cap);
+/* assign_workers (schwarz.hpp:56, schwarz.cpp:46-52) */
+int ffb_assign_workers(int n_workers, int n_parts, int* out);
+
+/* ---- operator: include/flowfem/assembly.hpp --------------------------------------- */
+/* y = A x and b of the unconstrained global system: assemble (assembly.hpp:59-61,
+ * assembly.cpp:32-166) followed by spmv (assembly.hpp:76, assembly.cpp:240-249), computed
+ * matrix-free on the device. x3/y3/b3 are planes3. */
+int ffb_assemble_apply(ffb_ctx* ctx, int W, int H, const double* t10, const double* alpha,
+                       const double* lambda, int nc, const double* x3, double* y3, double* b3);
+
+/* ---- adaptation: include/flowfem/adapt.hpp ----------------------------------------- */
+/* error_indicator (adapt.hpp:20-23, adapt.cpp:9-99); eta may be NULL */
+int ffb_error_indicator(ffb_ctx* ctx, int W, int H, const double* t10, const double* alpha,
+                        const double* lambda, const double* u3, int nc, double* eta,
+                        double* eta_max);
+/* update_alpha (adapt.hpp:34-35, adapt.cpp:101-112) */
+int ffb_update_alpha(ffb_ctx* ctx, int ntri, const double* alpha, const double* eta,
+                     double eta_max, double kappa, double eta_thr, double alpha_th,
+                     double* alpha_out);
+
+/* ---- stateful solver: the Schwarz-preconditioned solve of the global system -------- */
+/* Replaces the linear solve inside the adaptive loop (linsolve.hpp:53-62 on the global
+ * system; schwarz_solve's subdomain factorizations, schwarz.cpp:228-252). The system
+ * stays on the device between calls. */
+int ffb_set_terms(ffb_ctx* ctx, int W, int H, const double* t10);
+int ffb_set_frames(ffb_ctx* ctx, int W, int H, const double* f0, const double* f1,
+                   double sigma, double rho);
+int ffb_set_reg(ffb_ctx* ctx, const double* alpha, const double* lambda);
+int ffb_get_reg(ffb_ctx* ctx, double* alpha, double* lambda);
+int ffb_set_partition(ffb_ctx* ctx, int px, int py, int overlap);
+/* Additive-Schwarz-preconditioned CG to ||b-Au||/||b|| <= tol (true residual,
+ * linsolve.cpp:314-356). u3 (planes3): warm start on input if warm != 0, solution on
+ * output. Refactors the subdomain band factors iff alpha changed since the last factor. */
+int ffb_pcg_solve(ffb_ctx* ctx, int nc, double tol, int max_iters, int warm, double* u3,
+                  int* iters, double* residual);
+/* error_indicator + update_alpha on the resident state (adapt.cpp:9-112) */
+int ffb_adapt(ffb_ctx* ctx, int nc, double kappa, double eta_thr, double alpha_th,
+              double* eta_max);
+
+/* run_on_frames (pipeline.hpp:53, pipeline.cpp:38-78) under the converged-pass protocol:
+ * n_passes x {solve to tol, error_indicator, update_alpha} + one final solve.
+ * u3: planes3 out; alpha: per-triangle out (may be NULL); stats may be NULL. */
+int ffb_run_on_frames(ffb_ctx* ctx, int W, int H, const double* f0, const double* f1,
+                      const ffb_run_config* cfg, double* u3, double* alpha,
+                      ffb_run_stats* stats);
+/* Same with DEVICE pointers (frames and u3 resident in HBM), on the context's stream. */
+int ffb_run_on_frames_dev(ffb_ctx* ctx, int W, int H, const double* d_f0, const double* d_f1,
+                          const ffb_run_config* cfg, double* d_u3, ffb_run_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

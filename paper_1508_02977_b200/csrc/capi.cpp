@@ -1,0 +1,877 @@
+// C-ABI of flowfem_b200 (include/flowfem_b200.h) and the host orchestration of the hot
+// path: run_on_frames (src/pipeline.cpp:38-78) under the converged-pass protocol, with the
+// Schwarz-preconditioned CG of pcg.cu/band.cu as the linear solve.
+//
+// There is no CPU fallback: every numerical step runs in this library's CUDA kernels, and a
+// missing or unusable device is an error.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/flowfem_b200.h"
+#include "ffb_internal.cuh"
+#include "partition.hpp"
+
+namespace ffb {
+
+namespace {
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+}  // namespace
+
+void fail(const std::string& msg) { throw Error(msg); }
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  (void)file;
+  (void)line;
+  fail(std::string("cuda: ") + cudaGetErrorString(e) + " (" + what + ")");
+}
+
+void note_launch(long long n) { g_launches += n; }
+
+// fill kernels live in operator.cu's translation unit family; declared here
+void fill(double* p, double v, long long n, cudaStream_t st);
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  T* ensure(size_t m) {
+    if (m > n || !p) {
+      release();
+      const cudaError_t e = cudaMalloc(&p, std::max<size_t>(m, 1) * sizeof(T));
+      if (e != cudaSuccess) {
+        p = nullptr;
+        cudaGetLastError();
+        fail("cuda: out of device memory allocating " + std::to_string(m * sizeof(T)) +
+             " bytes");
+      }
+      n = m;
+    }
+    return p;
+  }
+};
+
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+
+}  // namespace ffb
+
+using namespace ffb;
+
+struct ffb_ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  cudaStream_t own_st = nullptr;
+  // problem on the device
+  int W = 0, H = 0;
+  size_t N = 0;
+  long long ntri = 0;
+  DBuf<double> t10, alpha, lambda, coef, b, x, r, z, p0, p1, q, eta, part, tmp, work, frames;
+  DBuf<double> eta_hist;
+  DBuf<int> bad_diag;
+  DBuf<unsigned> counter;
+  DBuf<PcgCtl> ctl;
+  PcgCtl* h_ctl = nullptr;
+  long long terms_version = 0, alpha_version = 0;
+  long long coef_key_a = -1, coef_key_t = -1;
+  int coef_nc = 0;
+  long long rhs_key_t = -1;
+  int rhs_nc = 0;
+  long long factor_key_a = -1, factor_key_t = -1;
+  // partition
+  bool have_part = false;
+  int part_px = 0, part_py = 0, part_ov = -1, part_nc = 0;
+  Partition decomp;
+  int nb = 32, kd_max = 0;
+  AsmLaunch plan{};
+  std::vector<SubInfo> subs;
+  DBuf<SubInfo> d_subs;
+  DBuf<AxisMap> d_col, d_row;
+  DBuf<double> band, ylocal, zlocal;
+  DBuf<int> d_bad;
+  double factor_doubles = 0, sum_n = 0;
+  // asm kernel timing
+  std::vector<EventPair> asm_events;
+  double asm_ms_total = 0;
+  long long asm_launches_timed = 0;
+  bool time_asm = false;
+
+  ~ffb_ctx() {
+    for (auto& e : asm_events) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    if (h_ctl) cudaFreeHost(h_ctl);
+    if (own_st) cudaStreamDestroy(own_st);
+  }
+};
+
+namespace {
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  } catch (...) {
+    g_err = "unknown error";
+    return 1;
+  }
+}
+
+void check_ctx(ffb_ctx* c) {
+  if (!c) fail("ffb: null context");
+  FFB_CUDA(cudaSetDevice(c->device));
+}
+
+void check_dims(int W, int H, const char* who) {
+  if (W < 2 || H < 2) fail(std::string(who) + ": frames must be at least 2x2");
+}
+
+void set_problem(ffb_ctx* c, int W, int H) {
+  if (c->W == W && c->H == H) return;
+  c->W = W;
+  c->H = H;
+  c->N = static_cast<size_t>(W) * H;
+  c->ntri = 2LL * (W - 1) * (H - 1);
+  c->have_part = false;
+  c->coef_key_a = c->coef_key_t = c->rhs_key_t = c->factor_key_a = c->factor_key_t = -1;
+}
+
+void upload(double* d, const double* h, size_t n, cudaStream_t st) {
+  FFB_CUDA(cudaMemcpyAsync(d, h, n * sizeof(double), cudaMemcpyHostToDevice, st));
+}
+void download(double* h, const double* d, size_t n, cudaStream_t st) {
+  FFB_CUDA(cudaMemcpyAsync(h, d, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+}
+void sync(ffb_ctx* c) { FFB_CUDA(cudaStreamSynchronize(c->st)); }
+
+// s0,s1 (2N) <- smooth(f0), smooth(f1); t10 <- data terms (imaging.cpp:33-138)
+void frames_to_terms_dev(ffb_ctx* c, const double* f0, const double* f1, double sigma,
+                         double rho) {
+  const int W = c->W, H = c->H;
+  const size_t N = c->N;
+  double* s = c->work.ensure(2 * N);
+  double* tmp = c->tmp.ensure(10 * N);
+  smooth_planes(f0, s, tmp, W, H, 1, sigma, c->st);
+  smooth_planes(f1, s + N, tmp, W, H, 1, sigma, c->st);
+  double* prod = c->tmp.p;  // 10 N
+  double* t10 = c->t10.ensure(10 * N);
+  deriv_products(s, s + N, prod, W, H, c->st);
+  double* tmp2 = c->coef.ensure(10 * N);  // scratch; the coefficients are rebuilt afterwards
+  c->coef_key_a = c->coef_key_t = -1;
+  smooth_planes(prod, t10, tmp2, W, H, 10, rho, c->st);
+  c->terms_version++;
+}
+
+void ensure_coef(ffb_ctx* c, int nc) {
+  if (c->coef_key_a == c->alpha_version && c->coef_key_t == c->terms_version && c->coef_nc == nc)
+    return;
+  c->coef.ensure(kCoefPlanes * c->N);
+  int* bad = c->bad_diag.ensure(1);
+  FFB_CUDA(cudaMemsetAsync(bad, 0x7f, sizeof(int), c->st));
+  build_coef(c->t10.p, c->alpha.p, c->lambda.p, c->W, c->H, nc, c->coef.p, bad, c->st);
+  int hbad = 0;
+  FFB_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  if (hbad != 0x7f7f7f7f) fail("linsolve.cg: non-positive diagonal at row " + std::to_string(hbad));
+  c->coef_key_a = c->alpha_version;
+  c->coef_key_t = c->terms_version;
+  c->coef_nc = nc;
+}
+
+void ensure_rhs(ffb_ctx* c, int nc) {
+  if (c->rhs_key_t == c->terms_version && c->rhs_nc == nc) return;
+  build_rhs(c->t10.p, c->W, c->H, nc, c->b.ensure(3 * c->N), c->st);
+  c->rhs_key_t = c->terms_version;
+  c->rhs_nc = nc;
+}
+
+int choose_nb(int kd_max) {
+  if (const char* e = std::getenv("FFB_NB")) {
+    const int v = std::atoi(e);
+    if (v == 16 || v == 32) return v;
+  }
+  // 32-row blocks when two ring stages of the widest band (plus the ring window) fit the
+  // shared memory (same arithmetic as asm_plan) and the factor's panel fits too.
+  int win = 1;
+  while (win < std::max(2 * kd_max, kd_max + 32) + 32) win <<= 1;
+  const size_t stage32 = (32ull * (kd_max + 1) + 15) / 16 * 16 * 8;
+  const size_t fixed = 128 + (win + 64) * 8;
+  const size_t panel32 = 32ull * ((kd_max + 63) / 64 * 64) * 8 + 2 * 32 * 33 * 8;
+  if (2 * stage32 + fixed <= 227 * 1024 && panel32 <= 227 * 1024) return 32;
+  return 16;
+}
+
+void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
+  if (c->have_part && c->part_px == px && c->part_py == py && c->part_ov == ov &&
+      c->part_nc == nc)
+    return;
+  c->have_part = false;
+  c->factor_key_a = c->factor_key_t = -1;
+  const int W = c->W, H = c->H;
+  c->decomp = build_partition(W, H, px, py, ov);
+  const int np = px * py;
+  std::vector<Rect> fr(np);
+  int kd_max = 0;
+  for (int p = 0; p < np; ++p) {
+    fr[p] = free_rect(c->decomp, p);
+    const int fw = fr[p].w(), fh = fr[p].h();
+    kd_max = std::max(kd_max, nc * std::min(fw, fh));
+  }
+  c->nb = choose_nb(kd_max);
+  c->kd_max = kd_max;
+  c->plan = asm_plan(c->nb, kd_max);
+  c->subs.assign(np, SubInfo{});
+  long long band_off = 0, vec_off = 0;
+  double fd = 0, sn = 0;
+  for (int p = 0; p < np; ++p) {
+    SubInfo& s = c->subs[p];
+    s.fx0 = fr[p].x0, s.fy0 = fr[p].y0, s.fw = fr[p].w(), s.fh = fr[p].h();
+    if (s.fw < 1 || s.fh < 1) fail("schwarz.build_partition: empty subdomain");
+    s.xfast = s.fw <= s.fh ? 1 : 0;
+    s.S = s.xfast ? s.fw : s.fh;
+    const long long n = static_cast<long long>(nc) * s.fw * s.fh;
+    if (n > (1LL << 30)) fail("schwarz: subdomain too large");
+    s.n = static_cast<int>(n);
+    s.npad = (s.n + c->nb - 1) / c->nb * c->nb;
+    s.kd = nc * s.S;
+    s.nblk = s.npad / c->nb;
+    s.band_off = band_off;
+    s.vec_off = vec_off;
+    band_off += (static_cast<long long>(s.npad) * (s.kd + 1) + 31) / 32 * 32;
+    vec_off += (s.npad + 31) / 32 * 32;
+    fd += static_cast<double>(s.npad) * (s.kd + 1);
+    sn += s.n;
+  }
+  c->factor_doubles = fd;
+  c->sum_n = sn;
+  // free-rectangle membership along each axis (free rect of part (i,j) = X_i x Y_j)
+  std::vector<AxisMap> col(W, AxisMap{-1, 0, -1, 0}), row(H, AxisMap{-1, 0, -1, 0});
+  for (int i = 0; i < px; ++i) {
+    const Rect& f = fr[i];
+    for (int x = f.x0; x < f.x1; ++x) {
+      AxisMap& m = col[x];
+      if (m.p0 < 0) m.p0 = i, m.l0 = x - f.x0;
+      else if (m.p1 < 0) m.p1 = i, m.l1 = x - f.x0;
+      else fail("schwarz: more than two overlapping parts along x");
+    }
+  }
+  for (int j = 0; j < py; ++j) {
+    const Rect& f = fr[j * px];
+    for (int y = f.y0; y < f.y1; ++y) {
+      AxisMap& m = row[y];
+      if (m.p0 < 0) m.p0 = j, m.l0 = y - f.y0;
+      else if (m.p1 < 0) m.p1 = j, m.l1 = y - f.y0;
+      else fail("schwarz: more than two overlapping parts along y");
+    }
+  }
+  for (int x = 0; x < W; ++x)
+    if (col[x].p0 < 0) fail("schwarz: column not covered by any subdomain");
+  for (int y = 0; y < H; ++y)
+    if (row[y].p0 < 0) fail("schwarz: row not covered by any subdomain");
+  c->d_subs.ensure(np);
+  c->d_col.ensure(W);
+  c->d_row.ensure(H);
+  FFB_CUDA(cudaMemcpyAsync(c->d_subs.p, c->subs.data(), np * sizeof(SubInfo),
+                           cudaMemcpyHostToDevice, c->st));
+  FFB_CUDA(cudaMemcpyAsync(c->d_col.p, col.data(), W * sizeof(AxisMap), cudaMemcpyHostToDevice,
+                           c->st));
+  FFB_CUDA(cudaMemcpyAsync(c->d_row.p, row.data(), H * sizeof(AxisMap), cudaMemcpyHostToDevice,
+                           c->st));
+  c->band.ensure(band_off);
+  c->ylocal.ensure(vec_off);
+  c->zlocal.ensure(vec_off);
+  c->d_bad.ensure(np);
+  sync(c);
+  c->have_part = true;
+  c->part_px = px, c->part_py = py, c->part_ov = ov, c->part_nc = nc;
+}
+
+void ensure_factor(ffb_ctx* c, int nc) {
+  if (!c->have_part) fail("schwarz: no partition set");
+  if (c->part_nc != nc) ensure_partition(c, c->part_px, c->part_py, c->part_ov, nc);
+  if (c->factor_key_a == c->alpha_version && c->factor_key_t == c->terms_version) return;
+  ensure_coef(c, nc);
+  const int np = static_cast<int>(c->subs.size());
+  band_assemble(c->d_subs.p, np, c->coef.p, c->W, c->N, nc, c->band.p, c->st);
+  FFB_CUDA(cudaMemsetAsync(c->d_bad.p, 0x7f, np * sizeof(int), c->st));
+  band_factor(c->d_subs.p, np, c->nb, c->kd_max, c->band.p, c->d_bad.p, c->st);
+  std::vector<int> bad(np);
+  FFB_CUDA(cudaMemcpyAsync(bad.data(), c->d_bad.p, np * sizeof(int), cudaMemcpyDeviceToHost,
+                           c->st));
+  sync(c);
+  for (int p = 0; p < np; ++p)
+    if (bad[p] != 0x7f7f7f7f)
+      fail("linsolve.cholesky: breakdown at pivot " + std::to_string(bad[p]) + " of subdomain " +
+           std::to_string(p) + ": matrix is not positive definite");
+  c->factor_key_a = c->alpha_version;
+  c->factor_key_t = c->terms_version;
+}
+
+void launch_asm(ffb_ctx* c, int nc, const double* rvec, const int* flags) {
+  EventPair* ev = nullptr;
+  if (c->time_asm) {
+    c->asm_events.emplace_back();
+    ev = &c->asm_events.back();
+    FFB_CUDA(cudaEventCreate(&ev->a));
+    FFB_CUDA(cudaEventCreate(&ev->b));
+    FFB_CUDA(cudaEventRecord(ev->a, c->st));
+  }
+  asm_solve(c->d_subs.p, static_cast<int>(c->subs.size()), c->kd_max, c->plan, c->band.p, rvec,
+            c->ylocal.p, c->zlocal.p, c->W, nc, flags, c->st);
+  if (ev) FFB_CUDA(cudaEventRecord(ev->b, c->st));
+}
+
+void harvest_asm_events(ffb_ctx* c) {
+  for (auto& e : c->asm_events) {
+    float ms = 0;
+    FFB_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
+    // kernels that returned at entry (converged) take ~2 us; count real applications only
+    if (ms > 0.02f) {
+      c->asm_ms_total += ms;
+      c->asm_launches_timed++;
+    }
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  c->asm_events.clear();
+}
+
+struct PcgResult {
+  int iters;
+  double res;
+};
+
+// Schwarz-preconditioned CG on the resident system, x warm or zero.
+PcgResult pcg(ffb_ctx* c, int nc, double tol, int max_iters, bool warm) {
+  ensure_coef(c, nc);
+  ensure_rhs(c, nc);
+  ensure_factor(c, nc);
+  const size_t N = c->N;
+  const long long nvec = static_cast<long long>(N) * nc;
+  double* x = c->x.ensure(3 * N);
+  double* r = c->r.ensure(3 * N);
+  double* z = c->z.ensure(3 * N);
+  double* P0 = c->p0.ensure(3 * N);
+  double* P1 = c->p1.ensure(3 * N);
+  double* q = c->q.ensure(3 * N);
+  double* part = c->part.ensure(4 * kRedBlocks);
+  PcgCtl* ctl = c->ctl.ensure(1);
+  if (!c->h_ctl) FFB_CUDA(cudaMallocHost(&c->h_ctl, sizeof(PcgCtl)));
+  if (!warm) FFB_CUDA(cudaMemsetAsync(x, 0, nvec * sizeof(double), c->st));
+  if (max_iters <= 0) max_iters = static_cast<int>(std::min<long long>(10 * nvec, 1 << 30));
+  std::memset(c->h_ctl, 0, sizeof(PcgCtl));
+  c->h_ctl->tol = tol;
+  FFB_CUDA(cudaMemcpyAsync(ctl, c->h_ctl, sizeof(PcgCtl), cudaMemcpyHostToDevice, c->st));
+  const int* flags = &ctl->done;
+  const int px = c->part_px;
+  pcg_init(nc, c->coef.p, c->b.p, x, r, c->W, c->H, ctl, part, c->st);
+  launch_asm(c, nc, r, flags);
+  pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, px, c->zlocal.p, r, z, c->W, c->H, ctl,
+              part, c->st);
+  const int chunk = 8;
+  for (;;) {
+    for (int it = 0; it < chunk; ++it) {
+      pcg_spmv_p(nc, c->coef.p, z, P0, P1, q, c->W, c->H, ctl, part, c->st);
+      pcg_update(nc, x, r, P0, P1, q, nvec, max_iters, ctl, part, c->st);
+      launch_asm(c, nc, r, flags);
+      pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, px, c->zlocal.p, r, z, c->W, c->H,
+                  ctl, part, c->st);
+    }
+    FFB_CUDA(cudaMemcpyAsync(c->h_ctl, ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    if (c->time_asm) harvest_asm_events(c);
+    if (c->h_ctl->done || c->h_ctl->err) break;
+  }
+  const PcgCtl& h = *c->h_ctl;
+  if (h.err)
+    fail("linsolve.cg: indefinite matrix detected at iteration " + std::to_string(h.err_it));
+  if (h.zero_rhs) {
+    FFB_CUDA(cudaMemsetAsync(x, 0, nvec * sizeof(double), c->st));
+    return {0, 0.0};
+  }
+  if (!(h.res <= tol)) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf,
+                  "linsolve.cg: no convergence after %d iterations, relative residual %f",
+                  h.iters, h.res);
+    fail(buf);
+  }
+  return {h.iters, h.res};
+}
+
+void ensure_reg(ffb_ctx* c) {
+  c->alpha.ensure(c->ntri);
+  c->lambda.ensure(c->ntri);
+}
+
+// run_on_frames, converged-pass protocol: n_passes x {solve, indicator,
+// update} + final solve; frames and u3 on the device.
+void run_dev(ffb_ctx* c, int W, int H, const double* f0, const double* f1,
+             const ffb_run_config* cfg, double* d_u3, ffb_run_stats* stats) {
+  if (!cfg) fail("cli.run: null config");
+  check_dims(W, H, "cli.run");
+  set_problem(c, W, H);
+  const int nc = cfg->illumination ? 3 : 2;
+  const int n_passes = cfg->adapt ? std::max(0, cfg->n_passes) : 0;
+  if (n_passes + 1 > FFB_MAX_SOLVES) fail("cli.run: too many adaptive passes");
+  cudaEvent_t ev[6];
+  for (auto& e : ev) FFB_CUDA(cudaEventCreate(&e));
+  FFB_CUDA(cudaEventRecord(ev[0], c->st));
+  frames_to_terms_dev(c, f0, f1, cfg->sigma, cfg->rho);
+  ensure_reg(c);
+  fill(c->alpha.p, cfg->alpha0, c->ntri, c->st);
+  fill(c->lambda.p, cfg->lambda0, c->ntri, c->st);
+  c->alpha_version++;
+  const Split sp = choose_split(W, H, cfg->parts);
+  ensure_partition(c, sp.px, sp.py, cfg->overlap, nc);
+  FFB_CUDA(cudaEventRecord(ev[1], c->st));
+  const double alpha_th = cfg->alpha_th > 0 ? cfg->alpha_th : cfg->alpha0 / 100.0;
+  double* eh = c->eta_hist.ensure(FFB_MAX_SOLVES);
+  double* eta = c->eta.ensure(c->ntri);
+  double* blockmax = c->part.ensure(4 * kRedBlocks);
+  unsigned* counter = c->counter.ensure(1);
+  FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
+  double ms_factor = 0, ms_pcg = 0, ms_adapt = 0;
+  long long total_it = 0;
+  c->asm_ms_total = 0;
+  c->asm_launches_timed = 0;
+  c->time_asm = stats != nullptr;
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->parts_x = sp.px;
+    stats->parts_y = sp.py;
+    stats->n_solves = n_passes + 1;
+  }
+  for (int pass = 0; pass <= n_passes; ++pass) {
+    FFB_CUDA(cudaEventRecord(ev[2], c->st));
+    ensure_factor(c, nc);
+    FFB_CUDA(cudaEventRecord(ev[3], c->st));
+    const PcgResult pr = pcg(c, nc, cfg->tol, cfg->max_iters, pass > 0);
+    FFB_CUDA(cudaEventRecord(ev[4], c->st));
+    total_it += pr.iters;
+    if (stats) {
+      stats->iters[pass] = pr.iters;
+      stats->residual[pass] = pr.res;
+    }
+    if (pass < n_passes) {
+      double* u3 = c->work.ensure(3 * c->N);
+      inter_to_planes(c->x.p, u3, static_cast<long long>(c->N), nc, c->st);
+      error_indicator(c->t10.p, c->alpha.p, c->lambda.p, u3, W, H, nc, eta, eh + pass,
+                      blockmax, counter, c->st);
+      update_alpha(c->alpha.p, c->alpha.p, eta, eh + pass, c->ntri, cfg->kappa,
+                   cfg->eta_threshold, alpha_th, c->st);
+      c->alpha_version++;
+    }
+    FFB_CUDA(cudaEventRecord(ev[5], c->st));
+    sync(c);
+    float a = 0, b = 0, d = 0;
+    FFB_CUDA(cudaEventElapsedTime(&a, ev[2], ev[3]));
+    FFB_CUDA(cudaEventElapsedTime(&b, ev[3], ev[4]));
+    FFB_CUDA(cudaEventElapsedTime(&d, ev[4], ev[5]));
+    ms_factor += a, ms_pcg += b, ms_adapt += d;
+  }
+  inter_to_planes(c->x.p, d_u3, static_cast<long long>(c->N), nc, c->st);
+  FFB_CUDA(cudaEventRecord(ev[5], c->st));
+  sync(c);
+  c->time_asm = false;
+  if (stats) {
+    float t_terms = 0, t_total = 0;
+    FFB_CUDA(cudaEventElapsedTime(&t_terms, ev[0], ev[1]));
+    FFB_CUDA(cudaEventElapsedTime(&t_total, ev[0], ev[5]));
+    if (n_passes > 0)
+      FFB_CUDA(cudaMemcpy(stats->eta_max, eh, n_passes * sizeof(double), cudaMemcpyDeviceToHost));
+    stats->pcg_iterations = total_it;
+    stats->ms_terms = t_terms;
+    stats->ms_factor = ms_factor;
+    stats->ms_pcg = ms_pcg;
+    stats->ms_adapt = ms_adapt;
+    stats->ms_total = t_total;
+    stats->factor_doubles = c->factor_doubles;
+    // algorithmic bytes of one PCG iteration: the factor read twice (16 B per stored band
+    // entry) + the vector kernels (coefficients 80 B/px, ~14 vector passes of nc doubles)
+    stats->iter_bytes = 16.0 * c->factor_doubles + (80.0 + 14.0 * 8.0 * nc) * c->N;
+    stats->ms_asm_per_iter =
+        c->asm_launches_timed ? c->asm_ms_total / c->asm_launches_timed : 0.0;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+}
+
+}  // namespace
+
+// ===================================================================== C-ABI
+extern "C" {
+
+const char* ffb_last_error(void) { return g_err.c_str(); }
+int ffb_abi_version(void) { return FFB_ABI_VERSION; }
+long long ffb_kernel_launches(void) { return g_launches.load(); }
+
+int ffb_create(ffb_ctx** out, int device) {
+  return guard([&] {
+    if (!out) fail("ffb: null output pointer");
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      fail("ffb: no CUDA device available (this library has no CPU fallback)");
+    }
+    if (device < 0 || device >= n) fail("ffb: device index out of range");
+    cudaDeviceProp prop{};
+    FFB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) fail("ffb: requires an sm_100 (Blackwell) device");
+    auto c = std::make_unique<ffb_ctx>();
+    c->device = device;
+    FFB_CUDA(cudaSetDevice(device));
+    FFB_CUDA(cudaStreamCreateWithFlags(&c->own_st, cudaStreamNonBlocking));
+    c->st = c->own_st;
+    *out = c.release();
+  });
+}
+
+int ffb_destroy(ffb_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->st);
+    delete ctx;
+  });
+}
+
+int ffb_set_stream(ffb_ctx* c, void* stream) {
+  return guard([&] {
+    check_ctx(c);
+    FFB_CUDA(cudaStreamSynchronize(c->st));
+    c->st = stream ? static_cast<cudaStream_t>(stream) : c->own_st;
+  });
+}
+
+int ffb_gaussian_smooth(ffb_ctx* c, int W, int H, const double* in, double sigma, double* out) {
+  return guard([&] {
+    check_ctx(c);
+    if (W < 1 || H < 1) fail("imaging.gaussian_smooth: empty image");
+    const size_t N = static_cast<size_t>(W) * H;
+    double* d = c->work.ensure(2 * N);
+    double* tmp = c->tmp.ensure(N);
+    upload(d, in, N, c->st);
+    smooth_planes(d, d + N, tmp, W, H, 1, sigma, c->st);
+    download(out, d + N, N, c->st);
+    sync(c);
+  });
+}
+
+int ffb_compute_derivatives(ffb_ctx* c, int W, int H, const double* f0, const double* f1,
+                            double* fx, double* fy, double* ft, double* f) {
+  return guard([&] {
+    check_ctx(c);
+    check_dims(W, H, "imaging.compute_derivatives");
+    const size_t N = static_cast<size_t>(W) * H;
+    double* d = c->tmp.ensure(6 * N);
+    upload(d, f0, N, c->st);
+    upload(d + N, f1, N, c->st);
+    derivatives4(d, d + N, d + 2 * N, d + 3 * N, d + 4 * N, d + 5 * N, W, H, c->st);
+    download(fx, d + 2 * N, N, c->st);
+    download(fy, d + 3 * N, N, c->st);
+    download(ft, d + 4 * N, N, c->st);
+    download(f, d + 5 * N, N, c->st);
+    sync(c);
+  });
+}
+
+int ffb_build_data_terms(ffb_ctx* c, int W, int H, const double* fx, const double* fy,
+                         const double* ft, const double* f, double rho, double* out10) {
+  return guard([&] {
+    check_ctx(c);
+    const size_t N = static_cast<size_t>(W) * H;
+    double* in4 = c->work.ensure(4 * N);
+    double* prod = c->tmp.ensure(10 * N);
+    double* tmp = c->frames.ensure(20 * N);
+    upload(in4, fx, N, c->st);
+    upload(in4 + N, fy, N, c->st);
+    upload(in4 + 2 * N, ft, N, c->st);
+    upload(in4 + 3 * N, f, N, c->st);
+    products_from4(in4, in4 + N, in4 + 2 * N, in4 + 3 * N, prod, W, H, c->st);
+    smooth_planes(prod, tmp, tmp + 10 * N, W, H, 10, rho, c->st);
+    download(out10, tmp, 10 * N, c->st);
+    sync(c);
+  });
+}
+
+int ffb_frames_to_terms(ffb_ctx* c, int W, int H, const double* f0, const double* f1,
+                        double sigma, double rho, double* out10) {
+  return guard([&] {
+    check_ctx(c);
+    check_dims(W, H, "imaging.compute_derivatives");
+    set_problem(c, W, H);
+    double* fr = c->frames.ensure(2 * c->N);
+    upload(fr, f0, c->N, c->st);
+    upload(fr + c->N, f1, c->N, c->st);
+    frames_to_terms_dev(c, fr, fr + c->N, sigma, rho);
+    download(out10, c->t10.p, 10 * c->N, c->st);
+    sync(c);
+  });
+}
+
+int ffb_enumerate_splits(int W, int H, int n_parts, int* px, int* py, double* ratio, int cap) {
+  int count = -1;
+  if (guard([&] {
+        const auto all = enumerate_splits(W, H, n_parts);
+        count = 0;
+        for (const auto& s : all) {
+          if (count >= cap) break;
+          px[count] = s.px, py[count] = s.py, ratio[count] = s.ratio;
+          ++count;
+        }
+      }))
+    return -1;
+  return count;
+}
+
+int ffb_choose_split(int W, int H, int n_parts, int* px, int* py, double* ratio) {
+  return guard([&] {
+    const Split s = choose_split(W, H, n_parts);
+    *px = s.px, *py = s.py, *ratio = s.ratio;
+  });
+}
+
+long ffb_build_partition(int W, int H, int px, int py, int ov, int* buf, long cap) {
+  long need = -1;
+  if (guard([&] {
+        const std::vector<int> flat = flatten(build_partition(W, H, px, py, ov));
+        need = static_cast<long>(flat.size());
+        if (buf && cap >= need) std::memcpy(buf, flat.data(), flat.size() * sizeof(int));
+      }))
+    return -1;
+  return need;
+}
+
+int ffb_assign_workers(int n_workers, int n_parts, int* out) {
+  return guard([&] {
+    const auto a = assign_workers(n_workers, n_parts);
+    std::memcpy(out, a.data(), a.size() * sizeof(int));
+  });
+}
+
+int ffb_assemble_apply(ffb_ctx* c, int W, int H, const double* t10, const double* alpha,
+                       const double* lambda, int nc, const double* x3, double* y3, double* b3) {
+  return guard([&] {
+    check_ctx(c);
+    if (nc != 2 && nc != 3) fail("assembly.assemble: components must be 2 or 3");
+    check_dims(W, H, "mesh.build_pixel_mesh");
+    set_problem(c, W, H);
+    const size_t N = c->N;
+    upload(c->t10.ensure(10 * N), t10, 10 * N, c->st);
+    c->terms_version++;
+    ensure_reg(c);
+    upload(c->alpha.p, alpha, c->ntri, c->st);
+    upload(c->lambda.p, lambda, c->ntri, c->st);
+    c->alpha_version++;
+    c->coef.ensure(kCoefPlanes * N);
+    build_coef(c->t10.p, c->alpha.p, c->lambda.p, W, H, nc, c->coef.p, nullptr, c->st);
+    c->coef_key_a = c->alpha_version, c->coef_key_t = c->terms_version, c->coef_nc = nc;
+    double* w = c->work.ensure(3 * N);
+    double* xi = c->x.ensure(3 * N);
+    double* yi = c->q.ensure(3 * N);
+    upload(w, x3, 3 * N, c->st);
+    planes_to_inter(w, xi, static_cast<long long>(N), nc, c->st);
+    apply_op(c->coef.p, W, H, nc, xi, yi, c->st);
+    inter_to_planes(yi, w, static_cast<long long>(N), nc, c->st);
+    download(y3, w, 3 * N, c->st);
+    sync(c);
+    build_rhs(c->t10.p, W, H, nc, yi, c->st);
+    inter_to_planes(yi, w, static_cast<long long>(N), nc, c->st);
+    download(b3, w, 3 * N, c->st);
+    sync(c);
+  });
+}
+
+int ffb_error_indicator(ffb_ctx* c, int W, int H, const double* t10, const double* alpha,
+                        const double* lambda, const double* u3, int nc, double* eta,
+                        double* eta_max) {
+  return guard([&] {
+    check_ctx(c);
+    check_dims(W, H, "adapt.error_indicator");
+    set_problem(c, W, H);
+    const size_t N = c->N;
+    upload(c->t10.ensure(10 * N), t10, 10 * N, c->st);
+    c->terms_version++;
+    ensure_reg(c);
+    upload(c->alpha.p, alpha, c->ntri, c->st);
+    upload(c->lambda.p, lambda, c->ntri, c->st);
+    c->alpha_version++;
+    double* u = c->work.ensure(3 * N);
+    upload(u, u3, 3 * N, c->st);
+    double* e = c->eta.ensure(c->ntri);
+    double* em = c->eta_hist.ensure(FFB_MAX_SOLVES);
+    unsigned* counter = c->counter.ensure(1);
+    FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
+    error_indicator(c->t10.p, c->alpha.p, c->lambda.p, u, W, H, nc, e, em,
+                    c->part.ensure(4 * kRedBlocks), counter, c->st);
+    if (eta) download(eta, e, c->ntri, c->st);
+    download(eta_max, em, 1, c->st);
+    sync(c);
+  });
+}
+
+int ffb_update_alpha(ffb_ctx* c, int ntri, const double* alpha, const double* eta,
+                     double eta_max, double kappa, double eta_thr, double alpha_th,
+                     double* alpha_out) {
+  return guard([&] {
+    check_ctx(c);
+    double* d = c->tmp.ensure(3 * static_cast<size_t>(ntri) + 1);
+    upload(d, alpha, ntri, c->st);
+    upload(d + ntri, eta, ntri, c->st);
+    upload(d + 3 * static_cast<size_t>(ntri), &eta_max, 1, c->st);
+    update_alpha(d + 2 * static_cast<size_t>(ntri), d, d + ntri, d + 3 * static_cast<size_t>(ntri),
+                 ntri, kappa, eta_thr, alpha_th, c->st);
+    download(alpha_out, d + 2 * static_cast<size_t>(ntri), ntri, c->st);
+    sync(c);
+  });
+}
+
+int ffb_set_terms(ffb_ctx* c, int W, int H, const double* t10) {
+  return guard([&] {
+    check_ctx(c);
+    check_dims(W, H, "mesh.build_pixel_mesh");
+    set_problem(c, W, H);
+    upload(c->t10.ensure(10 * c->N), t10, 10 * c->N, c->st);
+    c->terms_version++;
+    sync(c);
+  });
+}
+
+int ffb_set_frames(ffb_ctx* c, int W, int H, const double* f0, const double* f1, double sigma,
+                   double rho) {
+  return guard([&] {
+    check_ctx(c);
+    check_dims(W, H, "imaging.compute_derivatives");
+    set_problem(c, W, H);
+    double* fr = c->frames.ensure(2 * c->N);
+    upload(fr, f0, c->N, c->st);
+    upload(fr + c->N, f1, c->N, c->st);
+    frames_to_terms_dev(c, fr, fr + c->N, sigma, rho);
+    sync(c);
+  });
+}
+
+int ffb_set_reg(ffb_ctx* c, const double* alpha, const double* lambda) {
+  return guard([&] {
+    check_ctx(c);
+    if (!c->W) fail("assembly.assemble: no problem set");
+    ensure_reg(c);
+    upload(c->alpha.p, alpha, c->ntri, c->st);
+    upload(c->lambda.p, lambda, c->ntri, c->st);
+    c->alpha_version++;
+    sync(c);
+  });
+}
+
+int ffb_get_reg(ffb_ctx* c, double* alpha, double* lambda) {
+  return guard([&] {
+    check_ctx(c);
+    if (!c->alpha.p) fail("assembly.assemble: no regularization set");
+    if (alpha) download(alpha, c->alpha.p, c->ntri, c->st);
+    if (lambda) download(lambda, c->lambda.p, c->ntri, c->st);
+    sync(c);
+  });
+}
+
+int ffb_set_partition(ffb_ctx* c, int px, int py, int overlap) {
+  return guard([&] {
+    check_ctx(c);
+    if (!c->W) fail("schwarz.schwarz_solve: no problem set");
+    ensure_partition(c, px, py, overlap, 3);
+  });
+}
+
+int ffb_pcg_solve(ffb_ctx* c, int nc, double tol, int max_iters, int warm, double* u3,
+                  int* iters, double* residual) {
+  return guard([&] {
+    check_ctx(c);
+    if (nc != 2 && nc != 3) fail("assembly.assemble: components must be 2 or 3");
+    if (!c->alpha.p) fail("assembly.assemble: no regularization set");
+    if (!c->have_part) fail("schwarz.schwarz_solve: no partition set");
+    if (warm) {
+      double* w = c->work.ensure(3 * c->N);
+      upload(w, u3, 3 * c->N, c->st);
+      planes_to_inter(w, c->x.ensure(3 * c->N), static_cast<long long>(c->N), nc, c->st);
+    }
+    const PcgResult r = pcg(c, nc, tol, max_iters, warm != 0);
+    double* w = c->work.ensure(3 * c->N);
+    inter_to_planes(c->x.p, w, static_cast<long long>(c->N), nc, c->st);
+    download(u3, w, 3 * c->N, c->st);
+    sync(c);
+    if (iters) *iters = r.iters;
+    if (residual) *residual = r.res;
+  });
+}
+
+int ffb_adapt(ffb_ctx* c, int nc, double kappa, double eta_thr, double alpha_th,
+              double* eta_max) {
+  return guard([&] {
+    check_ctx(c);
+    if (!c->x.p) fail("adapt.error_indicator: no solution on the device");
+    double* u3 = c->work.ensure(3 * c->N);
+    inter_to_planes(c->x.p, u3, static_cast<long long>(c->N), nc, c->st);
+    double* em = c->eta_hist.ensure(FFB_MAX_SOLVES);
+    unsigned* counter = c->counter.ensure(1);
+    FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
+    double* eta = c->eta.ensure(c->ntri);
+    error_indicator(c->t10.p, c->alpha.p, c->lambda.p, u3, c->W, c->H, nc, eta, em,
+                    c->part.ensure(4 * kRedBlocks), counter, c->st);
+    update_alpha(c->alpha.p, c->alpha.p, eta, em, c->ntri, kappa, eta_thr, alpha_th, c->st);
+    c->alpha_version++;
+    if (eta_max) download(eta_max, em, 1, c->st);
+    sync(c);
+  });
+}
+
+int ffb_run_on_frames(ffb_ctx* c, int W, int H, const double* f0, const double* f1,
+                      const ffb_run_config* cfg, double* u3, double* alpha,
+                      ffb_run_stats* stats) {
+  return guard([&] {
+    check_ctx(c);
+    check_dims(W, H, "cli.run");
+    const size_t N = static_cast<size_t>(W) * H;
+    double* fr = c->frames.ensure(5 * N);
+    upload(fr, f0, N, c->st);
+    upload(fr + N, f1, N, c->st);
+    run_dev(c, W, H, fr, fr + N, cfg, fr + 2 * N, stats);
+    download(u3, fr + 2 * N, 3 * N, c->st);
+    if (alpha) download(alpha, c->alpha.p, c->ntri, c->st);
+    sync(c);
+  });
+}
+
+int ffb_run_on_frames_dev(ffb_ctx* c, int W, int H, const double* d_f0, const double* d_f1,
+                          const ffb_run_config* cfg, double* d_u3, ffb_run_stats* stats) {
+  return guard([&] {
+    check_ctx(c);
+    run_dev(c, W, H, d_f0, d_f1, cfg, d_u3, stats);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,133 @@
+// Internal declarations shared by the flowfem_b200 translation units.
+// Reference paths are relative to /root/reference/proj.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace ffb {
+
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+[[noreturn]] void fail(const std::string& msg);
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+void note_launch(long long n = 1);
+
+#define FFB_CUDA(x) ::ffb::cuda_check((x), #x, __FILE__, __LINE__)
+#define FFB_LAUNCHED() \
+  do {                 \
+    ::ffb::note_launch(); \
+    FFB_CUDA(cudaPeekAtLastError()); \
+  } while (0)
+
+constexpr int kMaxTaps = 129;  // radius <= 64
+
+struct Taps {
+  int r;
+  double w[kMaxTaps];
+};
+// gauss_kernel (src/imaging.cpp:19-29), computed on the host with std::exp
+Taps make_taps(double sigma);
+
+// ---- imaging kernels (imaging.cu) ---------------------------------------------------
+// separable smoothing of `planes` planes (stride W*H) in -> out, tmp is scratch of the
+// same size; sigma <= 0 copies.
+void smooth_planes(const double* in, double* out, double* tmp, int W, int H, int planes,
+                   double sigma, cudaStream_t st);
+void deriv_products(const double* s0, const double* s1, double* prod10, int W, int H,
+                    cudaStream_t st);
+void derivatives4(const double* s0, const double* s1, double* fx, double* fy, double* ft,
+                  double* f, int W, int H, cudaStream_t st);
+void products_from4(const double* fx, const double* fy, const double* ft, const double* f,
+                    double* prod10, int W, int H, cudaStream_t st);
+
+// ---- operator (operator.cu) -----------------------------------------------------------
+// Per-vertex coefficient planes (SoA, each N = W*H):
+//   0..5  m11 m12 m13 m22 m23 m33  (lumped data block + stiffness diagonal)
+//   6..7  eh_a eh_l : coupling (x,y)-(x+1,y) for alpha / lambda weights
+//   8..9  ev_a ev_l : coupling (x,y)-(x,y+1)
+constexpr int kCoefPlanes = 10;
+void build_coef(const double* t10, const double* alpha, const double* lambda, int W, int H,
+                int nc, double* coef, int* bad_diag, cudaStream_t st);
+void build_rhs(const double* t10, int W, int H, int nc, double* b, cudaStream_t st);
+void apply_op(const double* coef, int W, int H, int nc, const double* x, double* y,
+              cudaStream_t st);
+void planes_to_inter(const double* p3, double* x, long long N, int nc, cudaStream_t st);
+void inter_to_planes(const double* x, double* p3, long long N, int nc, cudaStream_t st);
+
+// ---- subdomain band factor / solve (band.cu) ------------------------------------------
+// Subdomain i of the partition: the free vertices of its extended rectangle (ext minus
+// the artificial Dirichlet ring, schwarz.cpp:93-112), ordered lexicographically with the
+// short side fast and components interleaved, giving a band of half-width kd = nc*S.
+struct SubInfo {
+  int fx0, fy0, fw, fh;  // free rectangle (global pixel coordinates)
+  int xfast;             // 1: local vertex = ly*fw + lx ; 0: lx*fh + ly
+  int S;                 // fast extent
+  int n;                 // nc*fw*fh scalar unknowns
+  int npad;              // n rounded up to the block size
+  int kd;                // half bandwidth nc*S
+  int nblk;              // npad / NB
+  long long band_off;    // offset (doubles) of the row-major band, rows of kd+1
+  long long vec_off;     // offset (doubles) into the per-subdomain vectors
+};
+
+struct AxisMap {  // free-rectangle membership along one axis (<= 2 parts)
+  int p0, l0, p1, l1;  // part index along the axis and local coordinate; p1 = -1 if none
+};
+
+void band_assemble(const SubInfo* d_subs, int nsub, const double* coef, int W, size_t N,
+                   int nc, double* band, cudaStream_t st);
+void band_factor(const SubInfo* d_subs, int nsub, int nb, int kd_max, double* band,
+                 int* d_bad, cudaStream_t st);
+struct AsmLaunch {
+  int nb, stages, threads;
+  size_t smem;
+};
+AsmLaunch asm_plan(int nb, int kd_max);
+void asm_solve(const SubInfo* d_subs, int nsub, int kd_max, const AsmLaunch& pl,
+               const double* band, const double* r, double* ylocal, double* zlocal, int W,
+               int nc, const int* d_ctl_flags, cudaStream_t st);
+
+// ---- PCG control block (solver.cu) ----------------------------------------------------
+struct PcgCtl {
+  double rz, rz_old, pAp, rr, bb, normb, res, tol;
+  int k;       // combines completed
+  int iters;   // CG iterations completed
+  int done;    // converged (or zero rhs)
+  int err;     // 1: indefinite (pAp <= 0)
+  int err_it;
+  int zero_rhs;
+  int pad[2];
+  unsigned counter[4];
+};
+
+void pcg_init(int nc, const double* coef, const double* b, const double* x, double* r, int W,
+              int H, PcgCtl* ctl, double* part, cudaStream_t st);
+void pcg_combine(int nc, const SubInfo* subs, const AxisMap* colmap, const AxisMap* rowmap,
+                 int px, const double* zlocal, const double* r, double* z, int W, int H,
+                 PcgCtl* ctl, double* part, cudaStream_t st);
+void pcg_spmv_p(int nc, const double* coef, const double* z, double* P0, double* P1, double* q,
+                int W, int H, PcgCtl* ctl, double* part, cudaStream_t st);
+void pcg_update(int nc, double* x, double* r, const double* P0, const double* P1,
+                const double* q, long long nvec, int max_iters, PcgCtl* ctl, double* part,
+                cudaStream_t st);
+
+// ---- adaptation (adapt.cu) ------------------------------------------------------------
+void error_indicator(const double* t10, const double* alpha, const double* lambda,
+                     const double* u3, int W, int H, int nc, double* eta, double* eta_max_dev,
+                     double* scratch, unsigned* counter, cudaStream_t st);
+void update_alpha(double* alpha_out, const double* alpha, const double* eta,
+                  const double* eta_max_dev, long long ntri, double kappa, double thr,
+                  double alpha_th, cudaStream_t st);
+
+// reductions
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs
+constexpr int kRedThreads = 256;
+
+}  // namespace ffb

@@ -1,0 +1,44 @@
+"""The C-ABI library loads and exports every entry point include/flowfem_b200.h declares;
+device entry points fail loudly (no CPU fallback) when no GPU is present."""
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "flowfem_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ffb_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_matches_binding():
+    from paper_1508_02977_b200 import _lib
+    assert header_symbols() == sorted(_lib.SIGNATURES)
+
+
+def test_library_exports_all_symbols():
+    from paper_1508_02977_b200 import _lib
+    lib = _lib.load()
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+    assert lib.ffb_abi_version() == 1
+
+
+def test_library_is_sm100a_cuda():
+    import subprocess
+    from paper_1508_02977_b200 import _lib
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-lelf", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1508_02977_b200 import flowfem
+    with pytest.raises(flowfem.FlowfemError, match="no CUDA device"):
+        flowfem.Context(0)
