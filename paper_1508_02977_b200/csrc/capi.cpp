@@ -243,6 +243,9 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
     kd_max = std::max(kd_max, nc * std::min(fw, fh));
   }
   c->nb = choose_nb(kd_max);
+  // the band stores each NB x NB diagonal block (inv(L_BB) is dense lower triangular), so
+  // the stored half-bandwidth is at least NB-1 even for subdomains narrower than a block
+  kd_max = std::max(kd_max, c->nb - 1);
   c->kd_max = kd_max;
   c->plan = asm_plan(c->nb, kd_max);
   c->subs.assign(np, SubInfo{});
@@ -258,7 +261,7 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
     if (n > (1LL << 30)) fail("schwarz: subdomain too large");
     s.n = static_cast<int>(n);
     s.npad = (s.n + c->nb - 1) / c->nb * c->nb;
-    s.kd = nc * s.S;
+    s.kd = std::max(nc * s.S, c->nb - 1);
     s.nblk = s.npad / c->nb;
     s.band_off = band_off;
     s.vec_off = vec_off;

@@ -71,7 +71,7 @@ struct SubInfo {
   int S;                 // fast extent
   int n;                 // nc*fw*fh scalar unknowns
   int npad;              // n rounded up to the block size
-  int kd;                // half bandwidth nc*S
+  int kd;                // stored half bandwidth max(nc*S, NB-1); the operator's is nc*S
   int nblk;              // npad / NB
   long long band_off;    // offset (doubles) of the row-major band, rows of kd+1
   long long vec_off;     // offset (doubles) into the per-subdomain vectors
