@@ -263,7 +263,7 @@ def main():
         return
     s = stats[-1]
     peak, peak_kind = measured_peak()
-    asm_bytes = 16.0 * s.factor_doubles  # band factor read forward + backward
+    asm_bytes = 8.0 * s.factor_doubles  # packed line inverses, forward + backward sweep
     achieved = asm_bytes / (s.ms_asm_per_iter * 1e-3) / 1e9 if s.ms_asm_per_iter > 0 else None
     iters_total = s.pcg_iterations
     line = {
@@ -277,7 +277,7 @@ def main():
                    "l2": "flushed (256 MB write) between steps; band factors > L2"},
         "gpu_launches": int(launches),
         "e2e": e2e,
-        "roofline": {"bound": "hbm", "kernel": "k_asm (band fwd/bwd solve)",
+        "roofline": {"bound": "hbm", "kernel": "k_line_solve (subdomain fwd/bwd sweeps)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
                      "traffic": profiled_traffic(cfg.name), "peak_kind": peak_kind,

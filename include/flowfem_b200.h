@@ -67,9 +67,10 @@ typedef struct ffb_run_stats {
   double eta_max[FFB_MAX_SOLVES];       /* per alpha update */
   long long pcg_iterations;             /* sum of iters */
   double ms_terms, ms_factor, ms_pcg, ms_adapt, ms_total; /* CUDA-event phase times */
-  double factor_doubles;                /* sum_i npad_i (kd_i + 1): band factor storage */
+  double factor_doubles;                /* doubles of the packed line inverses one
+                                           preconditioner application streams */
   double iter_bytes;                    /* algorithmic HBM bytes per PCG iteration */
-  double ms_asm_per_iter;               /* mean duration of the band fwd/bwd kernel */
+  double ms_asm_per_iter;               /* mean duration of the subdomain-solve kernel */
 } ffb_run_stats;
 
 /* ---- library ---------------------------------------------------------------------- */

@@ -102,14 +102,14 @@ struct ffb_ctx {
   bool have_part = false;
   int part_px = 0, part_py = 0, part_ov = -1, part_nc = 0;
   Partition decomp;
-  int nb = 32, kd_max = 0;
-  AsmLaunch plan{};
+  int nbf = 32, kd_max = 0;
+  SolvePlan plan{};
   std::vector<SubInfo> subs;
   DBuf<SubInfo> d_subs;
   DBuf<AxisMap> d_col, d_row;
-  DBuf<double> band, ylocal, zlocal;
+  DBuf<double> fac, dscratch, ylocal, zlocal;
   DBuf<int> d_bad;
-  double factor_doubles = 0, sum_n = 0;
+  double factor_doubles = 0, apply_doubles = 0, sum_n = 0;
   // asm kernel timing
   std::vector<EventPair> asm_events;
   double asm_ms_total = 0;
@@ -210,22 +210,6 @@ void ensure_rhs(ffb_ctx* c, int nc) {
   c->rhs_nc = nc;
 }
 
-int choose_nb(int kd_max) {
-  if (const char* e = std::getenv("FFB_NB")) {
-    const int v = std::atoi(e);
-    if (v == 16 || v == 32) return v;
-  }
-  // 32-row blocks when two ring stages of the widest band (plus the ring window) fit the
-  // shared memory (same arithmetic as asm_plan) and the factor's panel fits too.
-  int win = 1;
-  while (win < std::max(2 * kd_max, kd_max + 32) + 32) win <<= 1;
-  const size_t stage32 = (32ull * (kd_max + 1) + 15) / 16 * 16 * 8;
-  const size_t fixed = 128 + (win + 64) * 8;
-  const size_t panel32 = 32ull * ((kd_max + 63) / 64 * 64) * 8 + 2 * 32 * 33 * 8;
-  if (2 * stage32 + fixed <= 227 * 1024 && panel32 <= 227 * 1024) return 32;
-  return 16;
-}
-
 void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
   if (c->have_part && c->part_px == px && c->part_py == py && c->part_ov == ov &&
       c->part_nc == nc)
@@ -242,35 +226,38 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
     const int fw = fr[p].w(), fh = fr[p].h();
     kd_max = std::max(kd_max, nc * std::min(fw, fh));
   }
-  c->nb = choose_nb(kd_max);
-  // the band stores each NB x NB diagonal block (inv(L_BB) is dense lower triangular), so
-  // the stored half-bandwidth is at least NB-1 even for subdomains narrower than a block
-  kd_max = std::max(kd_max, c->nb - 1);
   c->kd_max = kd_max;
-  c->plan = asm_plan(c->nb, kd_max);
+  c->nbf = kd_max > 640 ? 16 : 32;
+  if (const char* e = std::getenv("FFB_NB")) {
+    const int v = std::atoi(e);
+    if (v == 16 || v == 32) c->nbf = v;
+  }
+  c->plan = solve_plan(kd_max);
   c->subs.assign(np, SubInfo{});
-  long long band_off = 0, vec_off = 0;
-  double fd = 0, sn = 0;
+  long long fac_off = 0, vec_off = 0;
+  double fd = 0, ad = 0, sn = 0;
   for (int p = 0; p < np; ++p) {
     SubInfo& s = c->subs[p];
     s.fx0 = fr[p].x0, s.fy0 = fr[p].y0, s.fw = fr[p].w(), s.fh = fr[p].h();
     if (s.fw < 1 || s.fh < 1) fail("schwarz.build_partition: empty subdomain");
     s.xfast = s.fw <= s.fh ? 1 : 0;
     s.S = s.xfast ? s.fw : s.fh;
-    const long long n = static_cast<long long>(nc) * s.fw * s.fh;
+    s.L = s.xfast ? s.fh : s.fw;
+    s.kd = nc * s.S;
+    const long long n = static_cast<long long>(s.kd) * s.L;
     if (n > (1LL << 30)) fail("schwarz: subdomain too large");
     s.n = static_cast<int>(n);
-    s.npad = (s.n + c->nb - 1) / c->nb * c->nb;
-    s.kd = std::max(nc * s.S, c->nb - 1);
-    s.nblk = s.npad / c->nb;
-    s.band_off = band_off;
+    s.line_sz = packed_line_size(s.kd);
+    s.fac_off = fac_off;
     s.vec_off = vec_off;
-    band_off += (static_cast<long long>(s.npad) * (s.kd + 1) + 31) / 32 * 32;
-    vec_off += (s.npad + 31) / 32 * 32;
-    fd += static_cast<double>(s.npad) * (s.kd + 1);
-    sn += s.n;
+    fac_off += (s.line_sz * s.L + 31) / 32 * 32;
+    vec_off += (n + 31) / 32 * 32;
+    fd += static_cast<double>(s.line_sz) * s.L;
+    ad += static_cast<double>(s.line_sz) * (2 * s.L - 1);  // forward all, backward L-1 lines
+    sn += static_cast<double>(n);
   }
   c->factor_doubles = fd;
+  c->apply_doubles = ad;
   c->sum_n = sn;
   // free-rectangle membership along each axis (free rect of part (i,j) = X_i x Y_j)
   std::vector<AxisMap> col(W, AxisMap{-1, 0, -1, 0}), row(H, AxisMap{-1, 0, -1, 0});
@@ -305,7 +292,8 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
                            c->st));
   FFB_CUDA(cudaMemcpyAsync(c->d_row.p, row.data(), H * sizeof(AxisMap), cudaMemcpyHostToDevice,
                            c->st));
-  c->band.ensure(band_off);
+  c->fac.ensure(fac_off);
+  c->dscratch.ensure(static_cast<size_t>(np) * kd_max * kd_max);
   c->ylocal.ensure(vec_off);
   c->zlocal.ensure(vec_off);
   c->d_bad.ensure(np);
@@ -320,9 +308,9 @@ void ensure_factor(ffb_ctx* c, int nc) {
   if (c->factor_key_a == c->alpha_version && c->factor_key_t == c->terms_version) return;
   ensure_coef(c, nc);
   const int np = static_cast<int>(c->subs.size());
-  band_assemble(c->d_subs.p, np, c->coef.p, c->W, c->N, nc, c->band.p, c->st);
   FFB_CUDA(cudaMemsetAsync(c->d_bad.p, 0x7f, np * sizeof(int), c->st));
-  band_factor(c->d_subs.p, np, c->nb, c->kd_max, c->band.p, c->d_bad.p, c->st);
+  line_factor(c->d_subs.p, np, c->nbf, c->kd_max, c->coef.p, c->N, c->W, nc, c->fac.p,
+              c->dscratch.p, static_cast<long long>(c->kd_max) * c->kd_max, c->d_bad.p, c->st);
   std::vector<int> bad(np);
   FFB_CUDA(cudaMemcpyAsync(bad.data(), c->d_bad.p, np * sizeof(int), cudaMemcpyDeviceToHost,
                            c->st));
@@ -344,8 +332,8 @@ void launch_asm(ffb_ctx* c, int nc, const double* rvec, const int* flags) {
     FFB_CUDA(cudaEventCreate(&ev->b));
     FFB_CUDA(cudaEventRecord(ev->a, c->st));
   }
-  asm_solve(c->d_subs.p, static_cast<int>(c->subs.size()), c->kd_max, c->plan, c->band.p, rvec,
-            c->ylocal.p, c->zlocal.p, c->W, nc, flags, c->st);
+  line_solve(c->d_subs.p, static_cast<int>(c->subs.size()), c->plan, c->fac.p, c->coef.p, c->N,
+             rvec, c->ylocal.p, c->zlocal.p, c->W, nc, flags, c->st);
   if (ev) FFB_CUDA(cudaEventRecord(ev->b, c->st));
 }
 
@@ -514,10 +502,11 @@ void run_dev(ffb_ctx* c, int W, int H, const double* f0, const double* f1,
     stats->ms_pcg = ms_pcg;
     stats->ms_adapt = ms_adapt;
     stats->ms_total = t_total;
-    stats->factor_doubles = c->factor_doubles;
-    // algorithmic bytes of one PCG iteration: the factor read twice (16 B per stored band
-    // entry) + the vector kernels (coefficients 80 B/px, ~14 vector passes of nc doubles)
-    stats->iter_bytes = 16.0 * c->factor_doubles + (80.0 + 14.0 * 8.0 * nc) * c->N;
+    // algorithmic bytes of one PCG iteration: the packed line inverses streamed forward
+    // (all lines) and backward (all but the last) + the vector kernels (coefficients
+    // 80 B/px, ~14 vector passes of nc doubles)
+    stats->factor_doubles = c->apply_doubles;
+    stats->iter_bytes = 8.0 * c->apply_doubles + (80.0 + 14.0 * 8.0 * nc) * c->N;
     stats->ms_asm_per_iter =
         c->asm_launches_timed ? c->asm_ms_total / c->asm_launches_timed : 0.0;
   }

@@ -61,19 +61,20 @@ void apply_op(const double* coef, int W, int H, int nc, const double* x, double*
 void planes_to_inter(const double* p3, double* x, long long N, int nc, cudaStream_t st);
 void inter_to_planes(const double* x, double* p3, long long N, int nc, cudaStream_t st);
 
-// ---- subdomain band factor / solve (band.cu) ------------------------------------------
+// ---- subdomain factor / solve (band.cu) -----------------------------------------------
 // Subdomain i of the partition: the free vertices of its extended rectangle (ext minus
-// the artificial Dirichlet ring, schwarz.cpp:93-112), ordered lexicographically with the
-// short side fast and components interleaved, giving a band of half-width kd = nc*S.
+// the artificial Dirichlet ring, schwarz.cpp:93-112), ordered line by line along the long
+// (slow) side; a line holds the S vertices of the short (fast) side x nc components.
 struct SubInfo {
   int fx0, fy0, fw, fh;  // free rectangle (global pixel coordinates)
-  int xfast;             // 1: local vertex = ly*fw + lx ; 0: lx*fh + ly
-  int S;                 // fast extent
-  int n;                 // nc*fw*fh scalar unknowns
-  int npad;              // n rounded up to the block size
-  int kd;                // stored half bandwidth max(nc*S, NB-1); the operator's is nc*S
-  int nblk;              // npad / NB
-  long long band_off;    // offset (doubles) of the row-major band, rows of kd+1
+  int xfast;             // 1: x is the fast axis (line = one row), 0: y is (line = one column)
+  int S;                 // fast extent (vertices per line)
+  int L;                 // slow extent (number of lines)
+  int kd;                // unknowns per line, nc*S
+  int n;                 // L*kd scalar unknowns
+  int pad_;
+  long long line_sz;     // doubles per line of the packed factor (packed_line_size(kd))
+  long long fac_off;     // offset (doubles) of the subdomain's factor
   long long vec_off;     // offset (doubles) into the per-subdomain vectors
 };
 
@@ -81,18 +82,18 @@ struct AxisMap {  // free-rectangle membership along one axis (<= 2 parts)
   int p0, l0, p1, l1;  // part index along the axis and local coordinate; p1 = -1 if none
 };
 
-void band_assemble(const SubInfo* d_subs, int nsub, const double* coef, int W, size_t N,
-                   int nc, double* band, cudaStream_t st);
-void band_factor(const SubInfo* d_subs, int nsub, int nb, int kd_max, double* band,
+long long packed_line_size(int kd);
+void line_factor(const SubInfo* d_subs, int nsub, int nb, int kd_max, const double* coef,
+                 size_t N, int W, int nc, double* fac, double* scratch, long long scratch_stride,
                  int* d_bad, cudaStream_t st);
-struct AsmLaunch {
-  int nb, stages, threads;
+struct SolvePlan {
+  int stages, cap, maxm;
   size_t smem;
 };
-AsmLaunch asm_plan(int nb, int kd_max);
-void asm_solve(const SubInfo* d_subs, int nsub, int kd_max, const AsmLaunch& pl,
-               const double* band, const double* r, double* ylocal, double* zlocal, int W,
-               int nc, const int* d_ctl_flags, cudaStream_t st);
+SolvePlan solve_plan(int kd_max);
+void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,
+                const double* coef, size_t N, const double* r, double* ylocal, double* zlocal,
+                int W, int nc, const int* flags, cudaStream_t st);
 
 // ---- PCG control block (solver.cu) ----------------------------------------------------
 struct PcgCtl {
