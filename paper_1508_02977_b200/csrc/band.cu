@@ -79,31 +79,72 @@ __device__ __forceinline__ double aline(const SubInfo& s, const double* __restri
   return 0.0;
 }
 
+// ----------------------------------------------------------------- cluster helpers
+// Every subdomain is owned by one thread-block cluster of C CTAs (C = 1, 2, 4 or 8, chosen
+// so that ~128 SMs take part); CTAs exchange partial results through distributed shared
+// memory and order their global-memory work with cluster barriers.
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+// barrier over the whole cluster with release/acquire ordering of shared and global memory
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+// address of `p` (a shared-memory variable of this CTA) in CTA `rank` of the cluster
+template <class T>
+__device__ __forceinline__ T* cl_map(T* p, unsigned rank) {
+  size_t out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(p), "r"(rank));
+  return reinterpret_cast<T*>(out);
+}
+
+// rows [row_lo(c), row_lo(c+1)) of a packed lower triangle of size kd: equal shares of the
+// kd(kd+1)/2 entries (cumulative work ~ i^2/2)
+__device__ __forceinline__ int row_lo(int c, int C, int kd) {
+  if (c <= 0) return 0;
+  if (c >= C) return kd;
+  int r = static_cast<int>(kd * sqrt(static_cast<double>(c) / C) + 0.5);
+  return min(max(r, c), kd - (C - c));
+}
+
 // ----------------------------------------------------------------- K5 factor
-constexpr int kFT = 256;  // factor threads
+constexpr int kFT = 256;  // factor threads per CTA
+constexpr int kFW = kFT / 32;
 
 template <int NB>
 __global__ void __launch_bounds__(kFT, 1)
     k_line_factor(const SubInfo* __restrict__ subs, const double* __restrict__ coef, size_t N,
                   int W, int nc, double* __restrict__ fac, double* __restrict__ scratch,
                   long long scratch_stride, int kdp, int* __restrict__ bad) {
-  const SubInfo s = subs[blockIdx.x];
+  const int C = static_cast<int>(cl_size()), crank = static_cast<int>(cl_rank());
+  const int sub = blockIdx.x / C;
+  const SubInfo s = subs[sub];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gtid = crank * kFT + tid, GT = C * kFT;       // cluster-wide thread id
+  const int gwarp = crank * kFW + warp, GW = C * kFW;     // cluster-wide warp id
   const int kd = s.kd;
-  double* D = scratch + blockIdx.x * scratch_stride;  // kd x kd row-major, lower used
+  double* D = scratch + sub * scratch_stride;  // kd x kd row-major, lower triangle used
   double* F = fac + s.fac_off;
   extern __shared__ __align__(16) double fsm[];
-  double* P = fsm;                // NB x (NB+1): pivot block, then Lc
-  double* Li = P + NB * (NB + 1); // NB x (NB+1): inv(Lc)
-  double* rcp = Li + NB * (NB + 1);  // NB
-  double* Z = rcp + NB;           // NB x kdp: Z[c*kdp + i]
+  double* P = fsm;                    // NB x (NB+1): Cholesky factor of the pivot block
+  double* Li = P + NB * (NB + 1);     // NB x (NB+1): its inverse
+  double* rcp = Li + NB * (NB + 1);   // NB: 1 / diag
+  double* Z = rcp + NB;               // NB x kdp: Z[c*kdp + i]
   for (int e = tid; e < NB * kdp; e += kFT) Z[e] = 0.0;
   int first_bad = 0x7fffffff;
 
   for (int l = 0; l < s.L; ++l) {
-    // ---- D_l = A_ll - B_l Dinv_{l-1} B_l  (lower triangle)
+    // ---- D_l = A_ll - B_l Dinv_{l-1} B_l  (lower triangle), rows shared by the cluster
     const double* Fp = F + static_cast<long long>(l - 1) * s.line_sz;
-    for (int i = warp; i < kd; i += kFT / 32) {
+    for (int i = gwarp; i < kd; i += GW) {
       const double bi = l > 0 ? bcoef(s, coef, N, W, nc, l, i) : 0.0;
       for (int j = lane; j <= i; j += 32) {
         double v = aline(s, coef, N, W, nc, l, i, j);
@@ -111,61 +152,61 @@ __global__ void __launch_bounds__(kFT, 1)
         D[static_cast<long long>(i) * kd + j] = v;
       }
     }
-    __syncthreads();
+    cl_sync();
     // ---- blocked symmetric sweep: D -> -D^{-1}
     for (int k0 = 0; k0 < kd; k0 += NB) {
       const int nbk = min(NB, kd - k0);
       const int k1 = k0 + nbk;
-      for (int e = tid; e < NB * NB; e += kFT) {
-        const int a = e / NB, b = e - a * NB;
-        P[a * (NB + 1) + b] =
-            (a < nbk && b <= a) ? D[static_cast<long long>(k0 + a) * kd + k0 + b] : 0.0;
-        Li[a * (NB + 1) + b] = 0.0;
-      }
-      __syncthreads();
       if (warp == 0) {
-        // Cholesky of the pivot block (linsolve.cpp:235-249 breakdown semantics)
-        for (int k = 0; k < nbk; ++k) {
-          double d = P[k * (NB + 1) + k];
-          if (!(d > 0.0) || !isfinite(d)) {
-            if (lane == 0) first_bad = min(first_bad, l * kd + k0 + k);
-            d = 1.0;
-          }
-          const double piv = sqrt(d), ip = 1.0 / piv;
-          __syncwarp();
-          for (int r = k + 1 + lane; r < nbk; r += 32) P[r * (NB + 1) + k] *= ip;
-          if (lane == 0) {
-            P[k * (NB + 1) + k] = piv;
-            rcp[k] = ip;
-          }
-          __syncwarp();
-          if (lane > k && lane < nbk) {
-            const double lrk = P[lane * (NB + 1) + k];
-            for (int c = k + 1; c <= lane; ++c) P[lane * (NB + 1) + c] -= lrk * P[c * (NB + 1) + k];
-          }
-          __syncwarp();
-        }
-        // Li = inv(Lc), lane c computes column c
-        if (lane < nbk) {
-          const int c = lane;
-          for (int r = 0; r < c; ++r) Li[r * (NB + 1) + c] = 0.0;
-          Li[c * (NB + 1) + c] = rcp[c];
-          for (int r = c + 1; r < nbk; ++r) {
-            double a0 = 0.0, a1 = 0.0;
-            int k = c;
-            for (; k + 1 < r; k += 2) {
-              a0 += P[r * (NB + 1) + k] * Li[k * (NB + 1) + c];
-              a1 += P[r * (NB + 1) + k + 1] * Li[(k + 1) * (NB + 1) + c];
+        // pivot block: Cholesky in registers (lane = row), breakdown semantics of
+        // linsolve.cpp:235-249; every CTA of the cluster computes it redundantly
+        const int r = lane;
+        double row[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          row[c] = (r < nbk && c <= r) ? D[static_cast<long long>(k0 + r) * kd + k0 + c] : 0.0;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          if (k < nbk) {
+            double dkk = __shfl_sync(0xffffffffu, row[k], k);
+            if (!(dkk > 0.0) || !isfinite(dkk)) {
+              if (lane == 0) first_bad = min(first_bad, l * kd + k0 + k);
+              dkk = 1.0;
             }
-            if (k < r) a0 += P[r * (NB + 1) + k] * Li[k * (NB + 1) + c];
-            Li[r * (NB + 1) + c] = -(a0 + a1) * rcp[r];
+            const double piv = sqrt(dkk), ip = 1.0 / piv;
+            const double lrk = r > k ? row[k] * ip : (r == k ? piv : 0.0);
+            row[k] = lrk;
+#pragma unroll
+            for (int c = k + 1; c < NB; ++c) {
+              const double lck = __shfl_sync(0xffffffffu, lrk, c);
+              if (r >= c) row[c] -= lrk * lck;
+            }
+            if (lane == 0) rcp[k] = ip;
           }
         }
+#pragma unroll
+        for (int c = 0; c < NB; ++c) P[r * (NB + 1) + c] = row[c];
+        __syncwarp();
+        // Li = inv(P): lane c owns column c
+        double col[NB];
+#pragma unroll
+        for (int rr = 0; rr < NB; ++rr) {
+          double a0 = rr == lane ? 1.0 : 0.0, a1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < rr; k += 2) {
+            a0 -= P[rr * (NB + 1) + k] * col[k];
+            if (k + 1 < rr) a1 -= P[rr * (NB + 1) + k + 1] * col[k + 1];
+          }
+          col[rr] = rr < nbk ? (a0 + a1) * rcp[rr] : 0.0;
+        }
+#pragma unroll
+        for (int rr = 0; rr < NB; ++rr) Li[rr * (NB + 1) + lane] = lane < nbk ? col[rr] : 0.0;
       }
       __syncthreads();
-      // ---- Z = A_RK Li^T for all rows outside K (rows inside K stay zero)
+      // ---- Z = A_RK Li^T for every row outside K (each CTA keeps the whole Z)
       for (int i = tid; i < kd; i += kFT) {
         if (i >= k0 && i < k1) {
+#pragma unroll
           for (int c = 0; c < NB; ++c) Z[c * kdp + i] = 0.0;
           continue;
         }
@@ -183,18 +224,19 @@ __global__ void __launch_bounds__(kFT, 1)
           Z[c * kdp + i] = acc;
         }
       }
-      __syncthreads();
-      // ---- A_RR -= Z Z^T over the lower triangle, K rows/columns excluded
+      cl_sync();  // Z complete everywhere; all reads of A_RK done before it is overwritten
+      // ---- A_RR -= Z Z^T over the lower triangle (K excluded): 64x32 warp tiles spread
+      // over the cluster's warps; thread tile 8x8 with rows ub0+16q+2ui+{0,1} and columns
+      // vb0+8q+2vi+{0,1} so that shared-memory reads are conflict-free double2 loads
       {
         const int ui = lane & 7, vi = lane >> 3;
-        const int nmu = (kd + 63) / 64;
+        const int nmu = (kd + 63) / 64, nmv_all = (kd + 31) / 32;
         int m = 0;
         for (int MU = 0; MU < nmu; ++MU) {
-          const int nmv = min((kd + 31) / 32, 2 * MU + 2);
+          const int nmv = min(nmv_all, 2 * MU + 2);
           for (int MV = 0; MV < nmv; ++MV, ++m) {
-            if ((m & 7) != warp) continue;
-            const int ub = 64 * MU + 8 * ui, vb = 32 * MV + 8 * vi;
-            if (vb > ub + 7 || ub >= kd) continue;
+            if (m % GW != gwarp) continue;
+            const int ub0 = 64 * MU + 2 * ui, vb0 = 32 * MV + 2 * vi;
             double acc[8][8];
 #pragma unroll
             for (int i = 0; i < 8; ++i)
@@ -202,12 +244,12 @@ __global__ void __launch_bounds__(kFT, 1)
               for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
 #pragma unroll 2
             for (int c = 0; c < nbk; ++c) {
-              const double2* pu = reinterpret_cast<const double2*>(Z + c * kdp + ub);
-              const double2* pv = reinterpret_cast<const double2*>(Z + c * kdp + vb);
+              const double* zc = Z + c * kdp;
               double a[8], b[8];
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-                const double2 x = pu[q], y = pv[q];
+                const double2 x = *reinterpret_cast<const double2*>(zc + ub0 + 16 * q);
+                const double2 y = *reinterpret_cast<const double2*>(zc + vb0 + 8 * q);
                 a[2 * q] = x.x, a[2 * q + 1] = x.y;
                 b[2 * q] = y.x, b[2 * q + 1] = y.y;
               }
@@ -218,13 +260,12 @@ __global__ void __launch_bounds__(kFT, 1)
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              const int u = ub + i;
-              if (u >= kd) break;
-              if (u >= k0 && u < k1) continue;
+              const int u = ub0 + 16 * (i >> 1) + (i & 1);
+              if (u >= kd || (u >= k0 && u < k1)) continue;
               double* rowp = D + static_cast<long long>(u) * kd;
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const int v = vb + j;
+                const int v = vb0 + 8 * (j >> 1) + (j & 1);
                 if (v <= u && (v < k0 || v >= k1)) rowp[v] -= acc[i][j];
               }
             }
@@ -232,42 +273,43 @@ __global__ void __launch_bounds__(kFT, 1)
         }
       }
       // ---- A_RK <- Z Li ; A_KK <- -Li^T Li   (entries disjoint from the update above)
-      for (int i = tid; i < kd; i += kFT) {
+      for (int i = gtid; i < kd; i += GT) {
         if (i >= k0 && i < k1) continue;
         double z[NB];
 #pragma unroll
         for (int c = 0; c < NB; ++c) z[c] = Z[c * kdp + i];
 #pragma unroll
         for (int c = 0; c < NB; ++c) {
-          if (c >= nbk) break;
-          double acc = 0.0;
+          if (c < nbk) {
+            double acc = 0.0;
 #pragma unroll
-          for (int c2 = c; c2 < NB; ++c2) acc = fma(z[c2], Li[c2 * (NB + 1) + c], acc);
-          if (i > k0)
-            D[static_cast<long long>(i) * kd + k0 + c] = acc;
-          else
-            D[static_cast<long long>(k0 + c) * kd + i] = acc;
+            for (int c2 = c; c2 < NB; ++c2) acc = fma(z[c2], Li[c2 * (NB + 1) + c], acc);
+            if (i > k0)
+              D[static_cast<long long>(i) * kd + k0 + c] = acc;
+            else
+              D[static_cast<long long>(k0 + c) * kd + i] = acc;
+          }
         }
       }
-      for (int e = tid; e < nbk * nbk; e += kFT) {
+      for (int e = gtid; e < nbk * nbk; e += GT) {
         const int a = e / nbk, b = e - a * nbk;
         if (b > a) continue;
         double acc = 0.0;
         for (int mm = a; mm < nbk; ++mm) acc += Li[mm * (NB + 1) + a] * Li[mm * (NB + 1) + b];
         D[static_cast<long long>(k0 + a) * kd + k0 + b] = -acc;
       }
-      __syncthreads();
+      cl_sync();
     }
     // ---- Dinv_l = -D, packed rows
     double* Fl = F + static_cast<long long>(l) * s.line_sz;
-    for (int i = warp; i < kd; i += kFT / 32) {
+    for (int i = gwarp; i < kd; i += GW) {
       const long long o = prow_off(i);
       for (int j = lane; j <= i; j += 32) Fl[o + j] = -D[static_cast<long long>(i) * kd + j];
       if ((i & 1) == 0 && lane == 0) Fl[o + i + 1] = 0.0;  // pad of even rows
     }
-    __syncthreads();
+    cl_sync();
   }
-  if (tid == 0 && first_bad != 0x7fffffff) atomicMin(bad + blockIdx.x, first_bad);
+  if (crank == 0 && tid == 0 && first_bad != 0x7fffffff) atomicMin(bad + sub, first_bad);
 }
 
 // ----------------------------------------------------------------- K6 solve
@@ -309,24 +351,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-constexpr int kSW = 16;  // solve warps
+constexpr int kSW = 16;  // solve warps per CTA
 constexpr int kST = kSW * 32;
 
-// Row chunking of one line's packed triangle: a chunk is the longest run of rows starting at
+// Row chunking of a CTA's rows [rlo, rhi) of one line: the longest run of rows starting at
 // r0 whose packed size fits `cap` doubles (at least one row). Identical on every thread.
-__device__ __forceinline__ int chunk_end(int r0, int kd, long long cap) {
+__device__ __forceinline__ int chunk_end(int r0, int rhi, long long cap) {
   const long long base = prow_off(r0);
   int r1 = r0 + 1;
-  // jump close with the closed form of prow_off, then fix up
   {
     const double t = static_cast<double>(base + cap);
-    int m = static_cast<int>((sqrt(1.0 + 2.0 * t) - 1.0) * 0.5);  // 2m(m+1) <= t
-    int guess = 2 * m;
-    if (guess > r1) r1 = guess;
+    const int m = static_cast<int>((sqrt(1.0 + 2.0 * t) - 1.0) * 0.5);  // 2m(m+1) <= t
+    if (2 * m > r1) r1 = 2 * m;
   }
-  if (r1 > kd) r1 = kd;
+  if (r1 > rhi) r1 = rhi;
   while (r1 > r0 + 1 && prow_off(r1) - base > cap) --r1;
-  while (r1 < kd && prow_off(r1 + 1) - base <= cap) ++r1;
+  while (r1 < rhi && prow_off(r1 + 1) - base <= cap) ++r1;
   return r1;
 }
 
@@ -335,21 +375,27 @@ __global__ void __launch_bounds__(kST, 1)
     k_line_solve(const SubInfo* __restrict__ subs, const double* __restrict__ fac,
                  const double* __restrict__ coef, size_t N, const double* __restrict__ r,
                  double* __restrict__ ylocal, double* __restrict__ zlocal, int W, int nc,
-                 int stages, int cap, const int* __restrict__ flags) {
-  if (flags && (flags[0] | flags[1])) return;  // PCG converged or failed
-  const SubInfo s = subs[blockIdx.x];
+                 int stages, int cap, int kd_max, const int* __restrict__ flags) {
+  if (flags && (flags[0] | flags[1])) return;  // PCG converged or failed (cluster-uniform)
+  const int C = static_cast<int>(cl_size()), crank = static_cast<int>(cl_rank());
+  const int sub = blockIdx.x / C;
+  const SubInfo s = subs[sub];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kd = s.kd, L = s.L;
+  const int rlo = row_lo(crank, C, kd), rhi = row_lo(crank + 1, C, kd);
+  const int share = (kd + C - 1) / C + kd;  // upper bound on any CTA's row count
   const double* F = fac + s.fac_off;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
   double* stage0 = reinterpret_cast<double*>(smem_raw + 128);
-  double* colpart = stage0 + static_cast<size_t>(stages) * cap;  // kSW x kd
-  double* wv = colpart + static_cast<size_t>(kSW) * kd;            // kd
-  double* yrow = wv + kd;                                          // kd
-  double* xprev = yrow + kd;                                       // kd
+  double* colpart = stage0 + static_cast<size_t>(stages) * cap;  // kSW x kd_max
+  double* wv = colpart + static_cast<size_t>(kSW) * kd_max;      // kd_max
+  double* yrow = wv + kd_max;                                    // kd_max (own rows)
+  double* xprev = yrow + kd_max;                                 // kd_max
+  double* red = xprev + kd_max;                                  // 8 x kd_max reduce slots
   double* yl = ylocal + s.vec_off;
   double* zl = zlocal + s.vec_off;
+  (void)share;
 
   if (tid == 0) {
     for (int q = 0; q < stages; ++q) mbar_init(&bar[q], 1);
@@ -357,15 +403,13 @@ __global__ void __launch_bounds__(kST, 1)
   }
   __syncthreads();
 
-  // producer state (thread 0): sequence of chunks over forward lines 0..L-1 then backward
-  // lines L-2..0; every thread tracks the consumer side identically
-  const int nlines_total = L + (L - 1);
-  int p_seq = 0, p_li = 0, p_r0 = 0;  // producer: next chunk
+  const int nlines_total = L + (L - 1);  // forward lines 0..L-1, backward L-2..0
   auto line_of = [&](int li) { return li < L ? li : (L - 2) - (li - L); };
-  auto produce = [&]() {  // issue one chunk if any remain (thread 0 only)
-    if (p_li >= nlines_total) return;
+  int p_seq = 0, p_li = 0, p_r0 = rlo;  // producer (thread 0)
+  auto produce = [&]() {
+    if (p_li >= nlines_total || rlo >= rhi) return;
     const int l = line_of(p_li);
-    const int r1 = chunk_end(p_r0, kd, cap);
+    const int r1 = chunk_end(p_r0, rhi, cap);
     const long long o0 = prow_off(p_r0), o1 = prow_off(r1);
     const int st = p_seq % stages;
     fence_proxy_async();
@@ -374,19 +418,19 @@ __global__ void __launch_bounds__(kST, 1)
              static_cast<uint32_t>((o1 - o0) * sizeof(double)), &bar[st]);
     ++p_seq;
     p_r0 = r1;
-    if (p_r0 >= kd) {
-      p_r0 = 0;
+    if (p_r0 >= rhi) {
+      p_r0 = rlo;
       ++p_li;
     }
   };
   if (tid == 0)
     for (int q = 0; q < stages; ++q) produce();
 
-  int c_seq = 0;  // consumer chunk counter
+  int c_seq = 0;
   for (int li = 0; li < nlines_total; ++li) {
     const bool fwd = li < L;
     const int l = line_of(li);
-    // operand of this line's GEMV
+    // operand of this line's GEMV (every CTA of the cluster builds the whole vector)
     for (int j = tid; j < kd; j += kST) {
       double w;
       if (fwd) {
@@ -401,9 +445,9 @@ __global__ void __launch_bounds__(kST, 1)
     double colacc[MAXM];
 #pragma unroll
     for (int m = 0; m < MAXM; ++m) colacc[m] = 0.0;
-    int r0 = 0;
-    while (r0 < kd) {
-      const int r1 = chunk_end(r0, kd, cap);
+    int r0 = rlo;
+    while (r0 < rhi) {
+      const int r1 = chunk_end(r0, rhi, cap);
       const int st = c_seq % stages;
       mbar_wait(&bar[st], (c_seq / stages) & 1);
       const double* Sb = stage0 + static_cast<size_t>(st) * cap - prow_off(r0);
@@ -433,25 +477,49 @@ __global__ void __launch_bounds__(kST, 1)
 #pragma unroll
     for (int m = 0; m < MAXM; ++m) {
       const int j = lane + 32 * m;
-      if (j < kd) colpart[warp * kd + j] = colacc[m];
+      if (j < rhi) colpart[warp * kd_max + j] = colacc[m];
     }
     __syncthreads();
-    for (int j = tid; j < kd; j += kST) {
-      double t = yrow[j];
+    // column partials of this CTA (+ its own row dots), reduced in a fixed warp order and
+    // scattered to the CTA that owns each row
+    int owner = 0;
+    for (int j = tid; j < rhi; j += kST) {
+      double t = (j >= rlo) ? yrow[j] : 0.0;
 #pragma unroll 4
-      for (int w = 0; w < kSW; ++w) t += colpart[w * kd + j];
+      for (int w = 0; w < kSW; ++w) t += colpart[w * kd_max + j];
+      while (owner + 1 < C && row_lo(owner + 1, C, kd) <= j) ++owner;
+      if (C == 1)
+        red[j] = t;
+      else
+        cl_map(red, static_cast<unsigned>(owner))[crank * kd_max + j] = t;
+    }
+    if (C == 1) __syncthreads(); else cl_sync();
+    // owners finish their rows (contributions from CTAs crank..C-1, ascending) and
+    // broadcast the line's result to every CTA
+    for (int j = rlo + tid; j < rhi; j += kST) {
+      double t = 0.0;
+      if (C == 1) {
+        t = red[j];
+      } else {
+        for (int c = crank; c < C; ++c) t += red[c * kd_max + j];
+      }
       const long long k = static_cast<long long>(l) * kd + j;
+      double v;
       if (fwd) {
         yl[k] = t;
-        xprev[j] = t;
         if (l == L - 1) zl[k] = t;  // x_{L-1} = y_{L-1}
+        v = t;
       } else {
-        const double x = yl[k] - t;
-        zl[k] = x;
-        xprev[j] = x;
+        v = yl[k] - t;
+        zl[k] = v;
+      }
+      if (C == 1) {
+        xprev[j] = v;
+      } else {
+        for (int c = 0; c < C; ++c) cl_map(xprev, static_cast<unsigned>(c))[j] = v;
       }
     }
-    __syncthreads();
+    if (C == 1) __syncthreads(); else cl_sync();
   }
 }
 
@@ -459,36 +527,53 @@ __global__ void __launch_bounds__(kST, 1)
 
 long long packed_line_size(int kd) { return prow_off(kd); }
 
-void line_factor(const SubInfo* d_subs, int nsub, int nb, int kd_max, const double* coef,
+template <class K, class... Args>
+static void launch_cluster(K kernel, int nblocks, int threads, size_t smem, int C,
+                           cudaStream_t st, Args... args) {
+  FFB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nblocks);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  FFB_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
+}
+
+void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max, const double* coef,
                  size_t N, int W, int nc, double* fac, double* scratch, long long scratch_stride,
                  int* d_bad, cudaStream_t st) {
   const int kdp = (kd_max + 63) / 64 * 64;
-  const size_t smem = (2 * nb * (nb + 1) + nb + static_cast<size_t>(nb) * kdp) * sizeof(double);
+  const size_t smem =
+      (2 * nb * (nb + 1) + nb + static_cast<size_t>(nb) * kdp) * sizeof(double);
   if (smem > 227 * 1024) fail("linsolve.cholesky: subdomain line too wide for shared memory");
-  if (nb == 32) {
-    FFB_CUDA(cudaFuncSetAttribute(k_line_factor<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    k_line_factor<32><<<nsub, kFT, smem, st>>>(d_subs, coef, N, W, nc, fac, scratch,
-                                               scratch_stride, kdp, d_bad);
-  } else if (nb == 16) {
-    FFB_CUDA(cudaFuncSetAttribute(k_line_factor<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    k_line_factor<16><<<nsub, kFT, smem, st>>>(d_subs, coef, N, W, nc, fac, scratch,
-                                               scratch_stride, kdp, d_bad);
-  } else {
+  if (nb == 32)
+    launch_cluster(k_line_factor<32>, nsub * C, kFT, smem, C, st, d_subs, coef, N, W, nc, fac,
+                   scratch, scratch_stride, kdp, d_bad);
+  else if (nb == 16)
+    launch_cluster(k_line_factor<16>, nsub * C, kFT, smem, C, st, d_subs, coef, N, W, nc, fac,
+                   scratch, scratch_stride, kdp, d_bad);
+  else
     fail("internal: unsupported pivot block size");
-  }
   FFB_LAUNCHED();
 }
 
-SolvePlan solve_plan(int kd_max) {
+SolvePlan solve_plan(int kd_max, int C) {
   SolvePlan pl{};
-  const size_t fixed = 128 + (static_cast<size_t>(kSW) * kd_max + 3 * kd_max) * sizeof(double);
+  pl.C = C;
+  const size_t fixed =
+      128 + (static_cast<size_t>(kSW) * kd_max + 3 * kd_max + 8 * kd_max) * sizeof(double);
   const size_t budget = 227 * 1024 - 1024;
   if (fixed + 2 * 1024 * sizeof(double) > budget)
     fail("linsolve.cholesky: subdomain line too wide for the solve kernel");
   const size_t avail = budget - fixed;
-  // 3 stages when each still holds >= 4 rows of the widest line, else 2
   int stages = 3;
   long long cap = static_cast<long long>(avail / (stages * sizeof(double))) & ~1LL;
   if (cap < 4LL * (kd_max + 2)) {
@@ -500,6 +585,7 @@ SolvePlan solve_plan(int kd_max) {
   pl.cap = static_cast<int>(cap);
   pl.smem = fixed + static_cast<size_t>(stages) * cap * sizeof(double);
   pl.maxm = (kd_max + 31) / 32;
+  pl.kd_max = kd_max;
   return pl;
 }
 
@@ -508,11 +594,8 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
                            const double* fac, const double* coef, size_t N, const double* r,
                            double* ylocal, double* zlocal, int W, int nc, const int* flags,
                            cudaStream_t st) {
-  auto k = k_line_solve<M>;
-  FFB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(pl.smem)));
-  k<<<nsub, kST, pl.smem, st>>>(d_subs, fac, coef, N, r, ylocal, zlocal, W, nc, pl.stages,
-                                pl.cap, flags);
+  launch_cluster(k_line_solve<M>, nsub * pl.C, kST, pl.smem, pl.C, st, d_subs, fac, coef, N, r,
+                 ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, flags);
 }
 
 void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,

@@ -102,7 +102,7 @@ struct ffb_ctx {
   bool have_part = false;
   int part_px = 0, part_py = 0, part_ov = -1, part_nc = 0;
   Partition decomp;
-  int nbf = 32, kd_max = 0;
+  int nbf = 32, kd_max = 0, ccl = 1;
   SolvePlan plan{};
   std::vector<SubInfo> subs;
   DBuf<SubInfo> d_subs;
@@ -232,7 +232,14 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
     const int v = std::atoi(e);
     if (v == 16 || v == 32) c->nbf = v;
   }
-  c->plan = solve_plan(kd_max);
+  // CTAs per subdomain (one thread-block cluster): enough that ~128 SMs take part
+  c->ccl = 1;
+  while (c->ccl < 8 && np * c->ccl * 2 <= 160) c->ccl *= 2;
+  if (const char* e = std::getenv("FFB_CLUSTER")) {
+    const int v = std::atoi(e);
+    if (v == 1 || v == 2 || v == 4 || v == 8) c->ccl = v;
+  }
+  c->plan = solve_plan(kd_max, c->ccl);
   c->subs.assign(np, SubInfo{});
   long long fac_off = 0, vec_off = 0;
   double fd = 0, ad = 0, sn = 0;
@@ -309,7 +316,7 @@ void ensure_factor(ffb_ctx* c, int nc) {
   ensure_coef(c, nc);
   const int np = static_cast<int>(c->subs.size());
   FFB_CUDA(cudaMemsetAsync(c->d_bad.p, 0x7f, np * sizeof(int), c->st));
-  line_factor(c->d_subs.p, np, c->nbf, c->kd_max, c->coef.p, c->N, c->W, nc, c->fac.p,
+  line_factor(c->d_subs.p, np, c->ccl, c->nbf, c->kd_max, c->coef.p, c->N, c->W, nc, c->fac.p,
               c->dscratch.p, static_cast<long long>(c->kd_max) * c->kd_max, c->d_bad.p, c->st);
   std::vector<int> bad(np);
   FFB_CUDA(cudaMemcpyAsync(bad.data(), c->d_bad.p, np * sizeof(int), cudaMemcpyDeviceToHost,

@@ -83,14 +83,14 @@ struct AxisMap {  // free-rectangle membership along one axis (<= 2 parts)
 };
 
 long long packed_line_size(int kd);
-void line_factor(const SubInfo* d_subs, int nsub, int nb, int kd_max, const double* coef,
+void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max, const double* coef,
                  size_t N, int W, int nc, double* fac, double* scratch, long long scratch_stride,
                  int* d_bad, cudaStream_t st);
 struct SolvePlan {
-  int stages, cap, maxm;
+  int stages, cap, maxm, C, kd_max;
   size_t smem;
 };
-SolvePlan solve_plan(int kd_max);
+SolvePlan solve_plan(int kd_max, int C);
 void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,
                 const double* coef, size_t N, const double* r, double* ylocal, double* zlocal,
                 int W, int nc, const int* flags, cudaStream_t st);
