@@ -138,7 +138,13 @@ __global__ void __launch_bounds__(kFT, 1)
   double* Li = P + NB * (NB + 1);     // NB x (NB+1): its inverse
   double* rcp = Li + NB * (NB + 1);   // NB: 1 / diag
   double* Z = rcp + NB;               // NB x kdp: Z[c*kdp + i]
+  __shared__ unsigned char tri_r[NB * (NB - 1) / 2 + 1], tri_c[NB * (NB - 1) / 2 + 1];
   for (int e = tid; e < NB * kdp; e += kFT) Z[e] = 0.0;
+  for (int rr = tid; rr < NB - 1; rr += kFT)  // strict-lower triangle index -> (row, col)
+    for (int cc = 0; cc <= rr; ++cc) {
+      tri_r[rr * (rr + 1) / 2 + cc] = static_cast<unsigned char>(rr);
+      tri_c[rr * (rr + 1) / 2 + cc] = static_cast<unsigned char>(cc);
+    }
   int first_bad = 0x7fffffff;
 
   for (int l = 0; l < s.L; ++l) {
@@ -157,50 +163,70 @@ __global__ void __launch_bounds__(kFT, 1)
     for (int k0 = 0; k0 < kd; k0 += NB) {
       const int nbk = min(NB, kd - k0);
       const int k1 = k0 + nbk;
-      if (warp == 0) {
-        // pivot block: Cholesky in registers (lane = row), breakdown semantics of
-        // linsolve.cpp:235-249; every CTA of the cluster computes it redundantly
-        const int r = lane;
-        double row[NB];
-#pragma unroll
-        for (int c = 0; c < NB; ++c)
-          row[c] = (r < nbk && c <= r) ? D[static_cast<long long>(k0 + r) * kd + k0 + c] : 0.0;
-#pragma unroll
-        for (int k = 0; k < NB; ++k) {
-          if (k < nbk) {
-            double dkk = __shfl_sync(0xffffffffu, row[k], k);
-            if (!(dkk > 0.0) || !isfinite(dkk)) {
-              if (lane == 0) first_bad = min(first_bad, l * kd + k0 + k);
-              dkk = 1.0;
-            }
-            const double piv = sqrt(dkk), ip = 1.0 / piv;
-            const double lrk = r > k ? row[k] * ip : (r == k ? piv : 0.0);
-            row[k] = lrk;
-#pragma unroll
-            for (int c = k + 1; c < NB; ++c) {
-              const double lck = __shfl_sync(0xffffffffu, lrk, c);
-              if (r >= c) row[c] -= lrk * lck;
-            }
-            if (lane == 0) rcp[k] = ip;
-          }
+      // ---- pivot block: Cholesky (all threads, one barrier per column; unscaled columns
+      // as in LDL^T, breakdown semantics of linsolve.cpp:235-249), redundantly per CTA
+      for (int e = tid; e < NB * NB; e += kFT) {
+        const int a = e / NB, b = e - a * NB;
+        P[a * (NB + 1) + b] =
+            (a < nbk && b <= a) ? D[static_cast<long long>(k0 + a) * kd + k0 + b] : 0.0;
+      }
+      __syncthreads();
+      for (int k = 0; k < nbk; ++k) {
+        double dkk = P[k * (NB + 1) + k];
+        if (!(dkk > 0.0) || !isfinite(dkk)) {
+          if (tid == 0) first_bad = min(first_bad, l * kd + k0 + k);
+          dkk = 1.0;
         }
+        const double inv = 1.0 / dkk;
+        const int m = nbk - 1 - k;
+        for (int e = tid; e < m * (m + 1) / 2; e += kFT) {
+          const int rr = tri_r[e], cc = tri_c[e];
+          const int r = k + 1 + rr, c = k + 1 + cc;
+          P[r * (NB + 1) + c] -= P[r * (NB + 1) + k] * P[c * (NB + 1) + k] * inv;
+        }
+        __syncthreads();
+      }
+      // scale: L[r][c] = P[r][c] / sqrt(P[c][c]) (into Li as scratch), then back to P
+      for (int e = tid; e < NB * NB; e += kFT) {
+        const int r = e / NB, c = e - r * NB;
+        double v = 0.0;
+        if (r < nbk && c <= r) {
+          double d = P[c * (NB + 1) + c];
+          if (!(d > 0.0) || !isfinite(d)) d = 1.0;
+          v = r == c ? sqrt(d) : P[r * (NB + 1) + c] / sqrt(d);
+        }
+        Li[r * (NB + 1) + c] = v;
+      }
+      __syncthreads();
+      for (int e = tid; e < NB * NB; e += kFT) {
+        const int r = e / NB, c = e - r * NB;
+        P[r * (NB + 1) + c] = Li[r * (NB + 1) + c];
+        if (c == 0) rcp[r] = r < nbk ? 1.0 / Li[r * (NB + 1) + r] : 0.0;
+      }
+      __syncthreads();
+      // Li = inv(P): 8 threads per column, rows in sequence, dot products split 8 ways
+      {
+        constexpr int TPC = kFT / NB;  // threads per column (8 for NB=32, 16 for NB=16)
+        const int c = tid / TPC, t = tid % TPC;
+        constexpr int Q = NB / TPC;
+        double colv[Q];  // entries k = t + TPC*q of this column of Li
 #pragma unroll
-        for (int c = 0; c < NB; ++c) P[r * (NB + 1) + c] = row[c];
-        __syncwarp();
-        // Li = inv(P): lane c owns column c
-        double col[NB];
+        for (int q = 0; q < Q; ++q) colv[q] = 0.0;
 #pragma unroll
         for (int rr = 0; rr < NB; ++rr) {
-          double a0 = rr == lane ? 1.0 : 0.0, a1 = 0.0;
+          double part = 0.0;
 #pragma unroll
-          for (int k = 0; k < rr; k += 2) {
-            a0 -= P[rr * (NB + 1) + k] * col[k];
-            if (k + 1 < rr) a1 -= P[rr * (NB + 1) + k + 1] * col[k + 1];
+          for (int q = 0; q < Q; ++q) {
+            const int k = t + TPC * q;
+            if (k < rr) part -= P[rr * (NB + 1) + k] * colv[q];
           }
-          col[rr] = rr < nbk ? (a0 + a1) * rcp[rr] : 0.0;
-        }
 #pragma unroll
-        for (int rr = 0; rr < NB; ++rr) Li[rr * (NB + 1) + lane] = lane < nbk ? col[rr] : 0.0;
+          for (int off = TPC / 2; off; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+          double v = rr < c ? 0.0 : ((rr == c ? 1.0 : 0.0) + part) * rcp[rr];
+          if (!(rr < nbk && c < nbk)) v = 0.0;
+          if ((rr % TPC) == t) colv[rr / TPC] = v;
+          if (t == 0) Li[rr * (NB + 1) + c] = v;
+        }
       }
       __syncthreads();
       // ---- Z = A_RK Li^T for every row outside K (each CTA keeps the whole Z)
@@ -231,11 +257,16 @@ __global__ void __launch_bounds__(kFT, 1)
       {
         const int ui = lane & 7, vi = lane >> 3;
         const int nmu = (kd + 63) / 64, nmv_all = (kd + 31) / 32;
-        int m = 0;
-        for (int MU = 0; MU < nmu; ++MU) {
-          const int nmv = min(nmv_all, 2 * MU + 2);
-          for (int MV = 0; MV < nmv; ++MV, ++m) {
-            if (m % GW != gwarp) continue;
+        int MU = 0, MV = 0, m = 0;  // walk the (MU, MV) list, taking every GW-th entry
+        auto advance = [&](int steps) {
+          while (steps-- > 0) {
+            if (++MV >= min(nmv_all, 2 * MU + 2)) MV = 0, ++MU;
+          }
+        };
+        advance(gwarp);
+        m = gwarp;
+        for (; MU < nmu; advance(GW), m += GW) {
+          {
             const int ub0 = 64 * MU + 2 * ui, vb0 = 32 * MV + 2 * vi;
             double acc[8][8];
 #pragma unroll
@@ -401,6 +432,7 @@ __global__ void __launch_bounds__(kST, 1)
     for (int q = 0; q < stages; ++q) mbar_init(&bar[q], 1);
     fence_barrier_init();
   }
+  for (int j = tid; j < kd_max; j += kST) xprev[j] = 0.0;
   __syncthreads();
 
   const int nlines_total = L + (L - 1);  // forward lines 0..L-1, backward L-2..0
@@ -426,21 +458,45 @@ __global__ void __launch_bounds__(kST, 1)
   if (tid == 0)
     for (int q = 0; q < stages; ++q) produce();
 
+  // operands of the next line are prefetched into registers one line ahead: r_l and B_l
+  // (forward), B_{l+1} and y_l of the owned rows (backward); only x_{l-1} / x_{l+1} (from
+  // the previous line, in shared memory) is on the line-to-line critical path
+  constexpr int PS = 2;  // j = tid + kST*q, kd <= 2*kST
+  double pf_r[PS], pf_b[PS], pf_y[PS];
+  auto prefetch = [&](int li) {
+#pragma unroll
+    for (int q = 0; q < PS; ++q) {
+      pf_r[q] = pf_b[q] = pf_y[q] = 0.0;
+      if (li >= nlines_total) continue;
+      const bool fw = li < L;
+      const int l = line_of(li);
+      const int j = tid + kST * q;
+      if (j < kd) {
+        if (fw) {
+          pf_r[q] = r[gidx(s, l, j, W, nc)];
+          if (l > 0) pf_b[q] = bcoef(s, coef, N, W, nc, l, j);
+        } else {
+          pf_b[q] = bcoef(s, coef, N, W, nc, l + 1, j);
+        }
+      }
+      const int jo = rlo + tid + kST * q;  // owned row
+      if (!fw && jo < rhi) pf_y[q] = yl[static_cast<long long>(l) * kd + jo];
+    }
+  };
+  prefetch(0);
+
   int c_seq = 0;
   for (int li = 0; li < nlines_total; ++li) {
     const bool fwd = li < L;
     const int l = line_of(li);
-    // operand of this line's GEMV (every CTA of the cluster builds the whole vector)
-    for (int j = tid; j < kd; j += kST) {
-      double w;
-      if (fwd) {
-        w = r[gidx(s, l, j, W, nc)];
-        if (l > 0) w -= bcoef(s, coef, N, W, nc, l, j) * xprev[j];
-      } else {
-        w = bcoef(s, coef, N, W, nc, l + 1, j) * xprev[j];
-      }
-      wv[j] = w;
+    double cur_y[PS];
+#pragma unroll
+    for (int q = 0; q < PS; ++q) {
+      const int j = tid + kST * q;
+      if (j < kd) wv[j] = fwd ? pf_r[q] - pf_b[q] * xprev[j] : pf_b[q] * xprev[j];
+      cur_y[q] = pf_y[q];
     }
+    prefetch(li + 1);
     __syncthreads();
     double colacc[MAXM];
 #pragma unroll
@@ -496,7 +552,10 @@ __global__ void __launch_bounds__(kST, 1)
     if (C == 1) __syncthreads(); else cl_sync();
     // owners finish their rows (contributions from CTAs crank..C-1, ascending) and
     // broadcast the line's result to every CTA
-    for (int j = rlo + tid; j < rhi; j += kST) {
+#pragma unroll
+    for (int q = 0; q < PS; ++q) {
+      const int j = rlo + tid + kST * q;
+      if (j >= rhi) continue;
       double t = 0.0;
       if (C == 1) {
         t = red[j];
@@ -510,7 +569,7 @@ __global__ void __launch_bounds__(kST, 1)
         if (l == L - 1) zl[k] = t;  // x_{L-1} = y_{L-1}
         v = t;
       } else {
-        v = yl[k] - t;
+        v = cur_y[q] - t;
         zl[k] = v;
       }
       if (C == 1) {
