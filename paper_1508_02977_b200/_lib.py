@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libflowfem_b200.so")
+LIB_PATH = os.environ.get("FFB_LIB", os.path.join(HERE, "libflowfem_b200.so"))
 
 MAX_SOLVES = 64
 

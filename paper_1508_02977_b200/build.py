@@ -14,13 +14,15 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libflowfem_b200.so")
+BUILD = os.path.join(HERE, "_build_prof" if os.environ.get("FFB_PROFILE") else "_build")
+LIB = os.environ.get("FFB_LIB_OUT", os.path.join(HERE, "libflowfem_b200.so"))
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", CSRC,
           "-I", os.path.join(ROOT, "include")]
+if os.environ.get("FFB_PROFILE"):
+    COMMON.append("-DFFB_PROFILE")
 CU = {
     "imaging.cu": ["--fmad=false"],
     "operator.cu": ["--fmad=false"],

@@ -33,6 +33,32 @@
 
 namespace ffb {
 
+#ifdef FFB_PROFILE
+__device__ unsigned long long g_prof[64];
+#define PROF_DECL unsigned long long prof_t = clock64(), prof_acc[16] = {0};
+#define PROF_MARK(i)                                   \
+  do {                                                 \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {         \
+      const unsigned long long t_ = clock64();         \
+      prof_acc[i] += t_ - prof_t;                      \
+      prof_t = t_;                                     \
+    }                                                  \
+  } while (0)
+#define PROF_FLUSH(base)                                                  \
+  do {                                                                    \
+    if (blockIdx.x == 0 && threadIdx.x == 0)                              \
+      for (int i_ = 0; i_ < 16; ++i_) g_prof[(base) + i_] += prof_acc[i_]; \
+  } while (0)
+#else
+#define PROF_DECL
+#define PROF_MARK(i) \
+  do {               \
+  } while (0)
+#define PROF_FLUSH(base) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace {
 
 // ----------------------------------------------------------------- packed row layout
@@ -69,8 +95,9 @@ __device__ __forceinline__ double aline(const SubInfo& s, const double* __restri
   const size_t v = static_cast<size_t>(s.fy0 + ly) * W + (s.fx0 + lx);
   if (ai == aj) {
     // m planes: 0 m11, 1 m12, 2 m13, 3 m22, 4 m23, 5 m33
-    const int mi[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
-    return coef[mi[ci][cj] * N + v];
+    const int sum = ci + cj;
+    const int plane = ci == cj ? (ci == 0 ? 0 : (ci == 1 ? 3 : 5)) : (sum == 1 ? 1 : (sum == 2 ? 2 : 4));
+    return coef[plane * N + v];
   }
   if (aj == ai - 1 && ci == cj) {
     const int k = ci < 2 ? 0 : 1;
@@ -119,7 +146,7 @@ __device__ __forceinline__ int row_lo(int c, int C, int kd) {
 constexpr int kFT = 256;  // factor threads per CTA
 constexpr int kFW = kFT / 32;
 
-template <int NB>
+template <int NB, int ZR>
 __global__ void __launch_bounds__(kFT, 1)
     k_line_factor(const SubInfo* __restrict__ subs, const double* __restrict__ coef, size_t N,
                   int W, int nc, double* __restrict__ fac, double* __restrict__ scratch,
@@ -138,14 +165,9 @@ __global__ void __launch_bounds__(kFT, 1)
   double* Li = P + NB * (NB + 1);     // NB x (NB+1): its inverse
   double* rcp = Li + NB * (NB + 1);   // NB: 1 / diag
   double* Z = rcp + NB;               // NB x kdp: Z[c*kdp + i]
-  __shared__ unsigned char tri_r[NB * (NB - 1) / 2 + 1], tri_c[NB * (NB - 1) / 2 + 1];
   for (int e = tid; e < NB * kdp; e += kFT) Z[e] = 0.0;
-  for (int rr = tid; rr < NB - 1; rr += kFT)  // strict-lower triangle index -> (row, col)
-    for (int cc = 0; cc <= rr; ++cc) {
-      tri_r[rr * (rr + 1) / 2 + cc] = static_cast<unsigned char>(rr);
-      tri_c[rr * (rr + 1) / 2 + cc] = static_cast<unsigned char>(cc);
-    }
   int first_bad = 0x7fffffff;
+  PROF_DECL
 
   for (int l = 0; l < s.L; ++l) {
     // ---- D_l = A_ll - B_l Dinv_{l-1} B_l  (lower triangle), rows shared by the cluster
@@ -159,98 +181,107 @@ __global__ void __launch_bounds__(kFT, 1)
       }
     }
     cl_sync();
+    PROF_MARK(0);
     // ---- blocked symmetric sweep: D -> -D^{-1}
     for (int k0 = 0; k0 < kd; k0 += NB) {
       const int nbk = min(NB, kd - k0);
       const int k1 = k0 + nbk;
-      // ---- pivot block: Cholesky (all threads, one barrier per column; unscaled columns
-      // as in LDL^T, breakdown semantics of linsolve.cpp:235-249), redundantly per CTA
-      for (int e = tid; e < NB * NB; e += kFT) {
-        const int a = e / NB, b = e - a * NB;
-        P[a * (NB + 1) + b] =
-            (a < nbk && b <= a) ? D[static_cast<long long>(k0 + a) * kd + k0 + b] : 0.0;
-      }
-      __syncthreads();
-      for (int k = 0; k < nbk; ++k) {
-        double dkk = P[k * (NB + 1) + k];
-        if (!(dkk > 0.0) || !isfinite(dkk)) {
-          if (tid == 0) first_bad = min(first_bad, l * kd + k0 + k);
-          dkk = 1.0;
-        }
-        const double inv = 1.0 / dkk;
-        const int m = nbk - 1 - k;
-        for (int e = tid; e < m * (m + 1) / 2; e += kFT) {
-          const int rr = tri_r[e], cc = tri_c[e];
-          const int r = k + 1 + rr, c = k + 1 + cc;
-          P[r * (NB + 1) + c] -= P[r * (NB + 1) + k] * P[c * (NB + 1) + k] * inv;
-        }
-        __syncthreads();
-      }
-      // scale: L[r][c] = P[r][c] / sqrt(P[c][c]) (into Li as scratch), then back to P
-      for (int e = tid; e < NB * NB; e += kFT) {
-        const int r = e / NB, c = e - r * NB;
-        double v = 0.0;
-        if (r < nbk && c <= r) {
-          double d = P[c * (NB + 1) + c];
-          if (!(d > 0.0) || !isfinite(d)) d = 1.0;
-          v = r == c ? sqrt(d) : P[r * (NB + 1) + c] / sqrt(d);
-        }
-        Li[r * (NB + 1) + c] = v;
-      }
-      __syncthreads();
-      for (int e = tid; e < NB * NB; e += kFT) {
-        const int r = e / NB, c = e - r * NB;
-        P[r * (NB + 1) + c] = Li[r * (NB + 1) + c];
-        if (c == 0) rcp[r] = r < nbk ? 1.0 / Li[r * (NB + 1) + r] : 0.0;
-      }
-      __syncthreads();
-      // Li = inv(P): 8 threads per column, rows in sequence, dot products split 8 ways
-      {
-        constexpr int TPC = kFT / NB;  // threads per column (8 for NB=32, 16 for NB=16)
-        const int c = tid / TPC, t = tid % TPC;
-        constexpr int Q = NB / TPC;
-        double colv[Q];  // entries k = t + TPC*q of this column of Li
+      // ---- prefetch this thread's rows of the column block A_RK into L1: their latency
+      // overlaps the pivot factorization below
 #pragma unroll
-        for (int q = 0; q < Q; ++q) colv[q] = 0.0;
-#pragma unroll
-        for (int rr = 0; rr < NB; ++rr) {
-          double part = 0.0;
-#pragma unroll
-          for (int q = 0; q < Q; ++q) {
-            const int k = t + TPC * q;
-            if (k < rr) part -= P[rr * (NB + 1) + k] * colv[q];
-          }
-#pragma unroll
-          for (int off = TPC / 2; off; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-          double v = rr < c ? 0.0 : ((rr == c ? 1.0 : 0.0) + part) * rcp[rr];
-          if (!(rr < nbk && c < nbk)) v = 0.0;
-          if ((rr % TPC) == t) colv[rr / TPC] = v;
-          if (t == 0) Li[rr * (NB + 1) + c] = v;
+      for (int q = 0; q < ZR; ++q) {
+        const int i = tid + kFT * q;
+        if (i >= kd || (i >= k0 && i < k1)) continue;
+        if (i > k0) {
+          const double* p = D + static_cast<long long>(i) * kd + k0;
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(p + NB - 1));
+        } else if ((i & 15) == 0) {
+          for (int c = 0; c < nbk; ++c)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(D + static_cast<long long>(k0 + c) * kd + i));
         }
       }
-      __syncthreads();
-      // ---- Z = A_RK Li^T for every row outside K (each CTA keeps the whole Z)
-      for (int i = tid; i < kd; i += kFT) {
-        if (i >= k0 && i < k1) {
-#pragma unroll
-          for (int c = 0; c < NB; ++c) Z[c * kdp + i] = 0.0;
-          continue;
-        }
-        double a[NB];
+      // ---- pivot block (warp 0, redundantly in every CTA): Cholesky with lane r holding
+      // row r in registers (breakdown semantics of linsolve.cpp:235-249), then Li = inv(L)
+      // with lane c producing column c from broadcast shared-memory reads
+      if (warp == 0) {
+        const int r = lane;
+        double row[NB];
 #pragma unroll
         for (int c = 0; c < NB; ++c)
-          a[c] = c < nbk ? (i > k0 ? D[static_cast<long long>(i) * kd + k0 + c]
-                                   : D[static_cast<long long>(k0 + c) * kd + i])
-                         : 0.0;
+          row[c] = (r < nbk && c <= r) ? D[static_cast<long long>(k0 + r) * kd + k0 + c]
+                                       : (r == c ? 1.0 : 0.0);
+        double my_rcp = 1.0;
+#pragma unroll NB
+        for (int k = 0; k < NB; ++k) {
+          double dkk = __shfl_sync(0xffffffffu, row[k], k);
+          if (!(dkk > 0.0) || !isfinite(dkk)) {
+            if (lane == 0 && k < nbk) first_bad = min(first_bad, l * kd + k0 + k);
+            dkk = 1.0;
+          }
+          const double piv = sqrt(dkk), ip = 1.0 / piv;
+          const double lk = r > k ? row[k] * ip : (r == k ? piv : 0.0);
+          row[k] = lk;
+          if (r == k) my_rcp = ip;
+#pragma unroll NB
+          for (int c = k + 1; c < NB; ++c) {
+            const double lck = __shfl_sync(0xffffffffu, lk, c);
+            if (r >= c) row[c] -= lk * lck;
+          }
+        }
 #pragma unroll
-        for (int c = 0; c < NB; ++c) {
-          double acc = 0.0;
+        for (int c = 0; c < NB; ++c) P[r * (NB + 1) + c] = c <= r ? row[c] : 0.0;
+        rcp[r] = my_rcp;
+        __syncwarp();
+        // Li = inv(L): lane c builds column c directly in shared memory
+        const int c = lane;
 #pragma unroll
-          for (int c2 = 0; c2 <= c; ++c2) acc = fma(a[c2], Li[c * (NB + 1) + c2], acc);
-          Z[c * kdp + i] = acc;
+        for (int rr = 0; rr < NB; ++rr) {
+          double a0 = rr == c ? 1.0 : 0.0, a1 = 0.0;
+          for (int k = c; k + 1 < rr; k += 2) {
+            a0 -= P[rr * (NB + 1) + k] * Li[k * (NB + 1) + c];
+            a1 -= P[rr * (NB + 1) + k + 1] * Li[(k + 1) * (NB + 1) + c];
+          }
+          if (((rr - c) & 1) && rr > c) a0 -= P[rr * (NB + 1) + rr - 1] * Li[(rr - 1) * (NB + 1) + c];
+          Li[rr * (NB + 1) + c] = (rr < nbk && c < nbk && rr >= c) ? (a0 + a1) * rcp[rr] : 0.0;
         }
       }
+      __syncthreads();
+      PROF_MARK(1);
+      double a[ZR][NB];
+#pragma unroll
+      for (int q = 0; q < ZR; ++q) {
+        const int i = tid + kFT * q;
+        const bool live = i < kd && (i < k0 || i >= k1);
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          a[q][c] = (live && c < nbk) ? (i > k0 ? D[static_cast<long long>(i) * kd + k0 + c]
+                                                : D[static_cast<long long>(k0 + c) * kd + i])
+                                      : 0.0;
+      }
+      PROF_MARK(2);
+      // ---- Z = A_RK Li^T for every row outside K (each CTA keeps the whole Z); each Li
+      // element read from shared memory feeds ZR rows
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        double acc[ZR];
+#pragma unroll
+        for (int q = 0; q < ZR; ++q) acc[q] = 0.0;
+#pragma unroll
+        for (int c2 = 0; c2 <= c; ++c2) {
+          const double li = Li[c * (NB + 1) + c2];
+#pragma unroll
+          for (int q = 0; q < ZR; ++q) acc[q] = fma(a[q][c2], li, acc[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < ZR; ++q) {
+          const int i = tid + kFT * q;
+          if (i < kdp) Z[c * kdp + i] = acc[q];
+        }
+      }
+      PROF_MARK(3);
       cl_sync();  // Z complete everywhere; all reads of A_RK done before it is overwritten
+      PROF_MARK(4);
       // ---- A_RR -= Z Z^T over the lower triangle (K excluded): 64x32 warp tiles spread
       // over the cluster's warps; thread tile 8x8 with rows ub0+16q+2ui+{0,1} and columns
       // vb0+8q+2vi+{0,1} so that shared-memory reads are conflict-free double2 loads
@@ -303,6 +334,7 @@ __global__ void __launch_bounds__(kFT, 1)
           }
         }
       }
+      PROF_MARK(5);
       // ---- A_RK <- Z Li ; A_KK <- -Li^T Li   (entries disjoint from the update above)
       for (int i = gtid; i < kd; i += GT) {
         if (i >= k0 && i < k1) continue;
@@ -329,7 +361,9 @@ __global__ void __launch_bounds__(kFT, 1)
         for (int mm = a; mm < nbk; ++mm) acc += Li[mm * (NB + 1) + a] * Li[mm * (NB + 1) + b];
         D[static_cast<long long>(k0 + a) * kd + k0 + b] = -acc;
       }
+      PROF_MARK(6);
       cl_sync();
+      PROF_MARK(7);
     }
     // ---- Dinv_l = -D, packed rows
     double* Fl = F + static_cast<long long>(l) * s.line_sz;
@@ -339,7 +373,9 @@ __global__ void __launch_bounds__(kFT, 1)
       if ((i & 1) == 0 && lane == 0) Fl[o + i + 1] = 0.0;  // pad of even rows
     }
     cl_sync();
+    PROF_MARK(8);
   }
+  PROF_FLUSH(0);
   if (crank == 0 && tid == 0 && first_bad != 0x7fffffff) atomicMin(bad + sub, first_bad);
 }
 
@@ -484,6 +520,7 @@ __global__ void __launch_bounds__(kST, 1)
     }
   };
   prefetch(0);
+  PROF_DECL
 
   int c_seq = 0;
   for (int li = 0; li < nlines_total; ++li) {
@@ -498,6 +535,7 @@ __global__ void __launch_bounds__(kST, 1)
     }
     prefetch(li + 1);
     __syncthreads();
+    PROF_MARK(0);
     double colacc[MAXM];
 #pragma unroll
     for (int m = 0; m < MAXM; ++m) colacc[m] = 0.0;
@@ -505,7 +543,9 @@ __global__ void __launch_bounds__(kST, 1)
     while (r0 < rhi) {
       const int r1 = chunk_end(r0, rhi, cap);
       const int st = c_seq % stages;
+      PROF_MARK(1);
       mbar_wait(&bar[st], (c_seq / stages) & 1);
+      PROF_MARK(2);
       const double* Sb = stage0 + static_cast<size_t>(st) * cap - prow_off(r0);
       for (int i = r0 + warp; i < r1; i += kSW) {
         const double* Si = Sb + prow_off(i);
@@ -525,7 +565,9 @@ __global__ void __launch_bounds__(kST, 1)
         for (int off = 16; off; off >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, off);
         if (lane == 0) yrow[i] = racc;
       }
+      PROF_MARK(3);
       __syncthreads();
+      PROF_MARK(4);
       if (tid == 0) produce();
       ++c_seq;
       r0 = r1;
@@ -536,6 +578,7 @@ __global__ void __launch_bounds__(kST, 1)
       if (j < rhi) colpart[warp * kd_max + j] = colacc[m];
     }
     __syncthreads();
+    PROF_MARK(5);
     // column partials of this CTA (+ its own row dots), reduced in a fixed warp order and
     // scattered to the CTA that owns each row
     int owner = 0;
@@ -549,7 +592,9 @@ __global__ void __launch_bounds__(kST, 1)
       else
         cl_map(red, static_cast<unsigned>(owner))[crank * kd_max + j] = t;
     }
+    PROF_MARK(6);
     if (C == 1) __syncthreads(); else cl_sync();
+    PROF_MARK(7);
     // owners finish their rows (contributions from CTAs crank..C-1, ascending) and
     // broadcast the line's result to every CTA
 #pragma unroll
@@ -578,13 +623,29 @@ __global__ void __launch_bounds__(kST, 1)
         for (int c = 0; c < C; ++c) cl_map(xprev, static_cast<unsigned>(c))[j] = v;
       }
     }
+    PROF_MARK(8);
     if (C == 1) __syncthreads(); else cl_sync();
+    PROF_MARK(9);
   }
+  PROF_FLUSH(16);
 }
 
 }  // namespace
 
 long long packed_line_size(int kd) { return prow_off(kd); }
+
+void debug_prof(unsigned long long* out, bool reset) {
+#ifdef FFB_PROFILE
+  FFB_CUDA(cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 64));
+  if (reset) {
+    static const unsigned long long z[64] = {0};
+    FFB_CUDA(cudaMemcpyToSymbol(g_prof, z, sizeof(z)));
+  }
+#else
+  for (int i = 0; i < 64; ++i) out[i] = 0;
+  (void)reset;
+#endif
+}
 
 template <class K, class... Args>
 static void launch_cluster(K kernel, int nblocks, int threads, size_t smem, int C,
@@ -613,14 +674,16 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max, con
   const size_t smem =
       (2 * nb * (nb + 1) + nb + static_cast<size_t>(nb) * kdp) * sizeof(double);
   if (smem > 227 * 1024) fail("linsolve.cholesky: subdomain line too wide for shared memory");
-  if (nb == 32)
-    launch_cluster(k_line_factor<32>, nsub * C, kFT, smem, C, st, d_subs, coef, N, W, nc, fac,
-                   scratch, scratch_stride, kdp, d_bad);
-  else if (nb == 16)
-    launch_cluster(k_line_factor<16>, nsub * C, kFT, smem, C, st, d_subs, coef, N, W, nc, fac,
-                   scratch, scratch_stride, kdp, d_bad);
-  else
-    fail("internal: unsupported pivot block size");
+  const int zr = (kdp + kFT - 1) / kFT;
+#define FFB_FACTOR(NBV, ZRV)                                                                 \
+  launch_cluster(k_line_factor<NBV, ZRV>, nsub * C, kFT, smem, C, st, d_subs, coef, N, W, nc, \
+                 fac, scratch, scratch_stride, kdp, d_bad)
+  if (nb == 32 && zr <= 1) FFB_FACTOR(32, 1);
+  else if (nb == 32 && zr <= 2) FFB_FACTOR(32, 2);
+  else if (nb == 16 && zr <= 2) FFB_FACTOR(16, 2);
+  else if (nb == 16 && zr <= 4) FFB_FACTOR(16, 4);
+  else fail("internal: unsupported pivot block / line width combination");
+#undef FFB_FACTOR
   FFB_LAUNCHED();
 }
 

@@ -40,6 +40,7 @@ void note_launch(long long n) { g_launches += n; }
 
 // fill kernels live in operator.cu's translation unit family; declared here
 void fill(double* p, double v, long long n, cudaStream_t st);
+void debug_prof(unsigned long long* out, bool reset);
 
 template <class T>
 struct DBuf {
@@ -227,7 +228,7 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
     kd_max = std::max(kd_max, nc * std::min(fw, fh));
   }
   c->kd_max = kd_max;
-  c->nbf = kd_max > 640 ? 16 : 32;
+  c->nbf = kd_max > 512 ? 16 : 32;
   if (const char* e = std::getenv("FFB_NB")) {
     const int v = std::atoi(e);
     if (v == 16 || v == 32) c->nbf = v;
@@ -558,6 +559,12 @@ int ffb_destroy(ffb_ctx* ctx) {
     cudaStreamSynchronize(ctx->st);
     delete ctx;
   });
+}
+
+// development probe: clock64 phase accumulators of the factor/solve kernels (zeros unless
+// built with FFB_PROFILE=1); not part of the public header
+int ffb_debug_prof(unsigned long long* out64, int reset) {
+  return guard([&] { debug_prof(out64, reset != 0); });
 }
 
 int ffb_set_stream(ffb_ctx* c, void* stream) {
