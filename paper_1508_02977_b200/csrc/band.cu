@@ -142,241 +142,352 @@ __device__ __forceinline__ int row_lo(int c, int C, int kd) {
   return min(max(r, c), kd - (C - c));
 }
 
+// Cholesky of a w x w (w <= 4) SPD block and the inverse of its factor, computed
+// redundantly by every thread. With `src` the block is read from shared memory (breakdown
+// recorded as row `row0 + k`); with `lsrc` an already factored block is read and only
+// inverted.
+__device__ __forceinline__ void chol4(const double* src, int ld, int w, double l[4][4],
+                                      double il[4][4], int& first_bad, int row0, int tid,
+                                      const double* lsrc = nullptr, int lld = 0) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      l[a][b] = 0.0;
+      il[a][b] = 0.0;
+    }
+  if (src) {
+    double d[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) d[a][b] = (a < w && b <= a) ? src[a * ld + b] : (a == b ? 1.0 : 0.0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double dk = d[k][k];
+      if (!(dk > 0.0) || !isfinite(dk)) {
+        if (tid == 0 && k < w) first_bad = min(first_bad, row0 + k);
+        dk = 1.0;
+      }
+      const double ir = rsqrt(dk);  // 1/sqrt, then one Newton step to full precision
+      const double irn = ir * (1.5 - 0.5 * dk * ir * ir);
+      l[k][k] = dk * irn;
+      il[k][k] = irn;
+#pragma unroll
+      for (int a = k + 1; a < 4; ++a) l[a][k] = d[a][k] * irn;
+#pragma unroll
+      for (int a = k + 1; a < 4; ++a)
+#pragma unroll
+        for (int b = k + 1; b <= a; ++b) d[a][b] -= l[a][k] * l[b][k];
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b) l[a][b] = (a < w) ? lsrc[a * lld + b] : (a == b ? 1.0 : 0.0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) il[c][c] = 1.0 / l[c][c];
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+#pragma unroll
+    for (int a = c + 1; a < 4; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = c; k < a; ++k) acc += l[a][k] * il[k][c];
+      il[a][c] = -acc * il[a][a];
+    }
+  }
+}
+
+// ----------------------------------------------------------------- twisted chains
+// Lines 0..m-1 are factored top-down (chain 0), lines L-1..m+1 bottom-up (chain 1), and the
+// middle line m closes both:
+//   chain 0:  D_l = A_ll - B_l D_{l-1}^-1 B_l,        chain 1:  E_l = A_ll - B_{l+1} E_{l+1}^-1 B_{l+1}
+//   middle:   T = A_mm - B_m D_{m-1}^-1 B_m - B_{m+1} E_{m+1}^-1 B_{m+1}
+// A_i^-1 r then runs forward from both ends to the middle and backward from the middle out,
+// halving the sequential depth of both the factorization and the solve.
+__host__ __device__ __forceinline__ int mid_line(int L) { return (L - 1) / 2; }
+
 // ----------------------------------------------------------------- K5 factor
-constexpr int kFT = 256;  // factor threads per CTA
+constexpr int kFT = 512;  // factor threads per CTA (16 warps)
 constexpr int kFW = kFT / 32;
 
-template <int NB, int ZR>
-__global__ void __launch_bounds__(kFT, 1)
-    k_line_factor(const SubInfo* __restrict__ subs, const double* __restrict__ coef, size_t N,
-                  int W, int nc, double* __restrict__ fac, double* __restrict__ scratch,
-                  long long scratch_stride, int kdp, int* __restrict__ bad) {
-  const int C = static_cast<int>(cl_size()), crank = static_cast<int>(cl_rank());
-  const int sub = blockIdx.x / C;
-  const SubInfo s = subs[sub];
+// In-place inversion of the SPD line matrix D (kd x kd row-major in global scratch, lower
+// triangle used) by the blocked symmetric sweep; leaves -D^{-1} in the lower triangle.
+template <int NB>
+__device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P, double* Li,
+                             double* pan, double* dinv4, double* Z, int& first_bad,
+                             int bad_base) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gtid = crank * kFT + tid, GT = C * kFT;       // cluster-wide thread id
-  const int gwarp = crank * kFW + warp, GW = C * kFW;     // cluster-wide warp id
-  const int kd = s.kd;
-  double* D = scratch + sub * scratch_stride;  // kd x kd row-major, lower triangle used
-  double* F = fac + s.fac_off;
-  extern __shared__ __align__(16) double fsm[];
-  double* P = fsm;                    // NB x (NB+1): Cholesky factor of the pivot block
-  double* Li = P + NB * (NB + 1);     // NB x (NB+1): its inverse
-  double* rcp = Li + NB * (NB + 1);   // NB: 1 / diag
-  double* Z = rcp + NB;               // NB x kdp: Z[c*kdp + i]
-  for (int e = tid; e < NB * kdp; e += kFT) Z[e] = 0.0;
-  int first_bad = 0x7fffffff;
-  PROF_DECL
-
-  for (int l = 0; l < s.L; ++l) {
-    // ---- D_l = A_ll - B_l Dinv_{l-1} B_l  (lower triangle), rows shared by the cluster
-    const double* Fp = F + static_cast<long long>(l - 1) * s.line_sz;
-    for (int i = gwarp; i < kd; i += GW) {
-      const double bi = l > 0 ? bcoef(s, coef, N, W, nc, l, i) : 0.0;
-      for (int j = lane; j <= i; j += 32) {
-        double v = aline(s, coef, N, W, nc, l, i, j);
-        if (l > 0) v -= bi * bcoef(s, coef, N, W, nc, l, j) * Fp[prow_off(i) + j];
-        D[static_cast<long long>(i) * kd + j] = v;
-      }
+  for (int k0 = 0; k0 < kd; k0 += NB) {
+    const int nbk = min(NB, kd - k0);
+    const int k1 = k0 + nbk;
+    // ---- pivot block: Cholesky blocked by 4 columns, Li = inv(L) blocked by 4 rows
+    for (int e = tid; e < NB * NB; e += kFT) {
+      const int a = e / NB, b = e - a * NB;
+      P[a * (NB + 1) + b] =
+          (a < nbk && b <= a) ? D[static_cast<long long>(k0 + a) * kd + k0 + b] : 0.0;
+      Li[a * (NB + 1) + b] = 0.0;
     }
-    cl_sync();
-    PROF_MARK(0);
-    // ---- blocked symmetric sweep: D -> -D^{-1}
-    for (int k0 = 0; k0 < kd; k0 += NB) {
-      const int nbk = min(NB, kd - k0);
-      const int k1 = k0 + nbk;
-      // ---- prefetch this thread's rows of the column block A_RK into L1: their latency
-      // overlaps the pivot factorization below
+    __syncthreads();
+#pragma unroll 1
+    for (int kb = 0; kb < nbk; kb += 4) {
+      const int w4 = min(4, nbk - kb);
+      double l4[4][4], i4[4][4];
+      chol4(P + kb * (NB + 1) + kb, NB + 1, w4, l4, i4, first_bad, bad_base + k0 + kb, tid);
+      for (int r = kb + w4 + tid; r < nbk; r += kFT) {
+        double p[4];
 #pragma unroll
-      for (int q = 0; q < ZR; ++q) {
-        const int i = tid + kFT * q;
-        if (i >= kd || (i >= k0 && i < k1)) continue;
-        if (i > k0) {
-          const double* p = D + static_cast<long long>(i) * kd + k0;
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(p + NB - 1));
-        } else if ((i & 15) == 0) {
-          for (int c = 0; c < nbk; ++c)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(D + static_cast<long long>(k0 + c) * kd + i));
-        }
-      }
-      // ---- pivot block (warp 0, redundantly in every CTA): Cholesky with lane r holding
-      // row r in registers (breakdown semantics of linsolve.cpp:235-249), then Li = inv(L)
-      // with lane c producing column c from broadcast shared-memory reads
-      if (warp == 0) {
-        const int r = lane;
-        double row[NB];
+        for (int t = 0; t < 4; ++t) p[t] = t < w4 ? P[r * (NB + 1) + kb + t] : 0.0;
 #pragma unroll
-        for (int c = 0; c < NB; ++c)
-          row[c] = (r < nbk && c <= r) ? D[static_cast<long long>(k0 + r) * kd + k0 + c]
-                                       : (r == c ? 1.0 : 0.0);
-        double my_rcp = 1.0;
-#pragma unroll NB
-        for (int k = 0; k < NB; ++k) {
-          double dkk = __shfl_sync(0xffffffffu, row[k], k);
-          if (!(dkk > 0.0) || !isfinite(dkk)) {
-            if (lane == 0 && k < nbk) first_bad = min(first_bad, l * kd + k0 + k);
-            dkk = 1.0;
-          }
-          const double piv = sqrt(dkk), ip = 1.0 / piv;
-          const double lk = r > k ? row[k] * ip : (r == k ? piv : 0.0);
-          row[k] = lk;
-          if (r == k) my_rcp = ip;
-#pragma unroll NB
-          for (int c = k + 1; c < NB; ++c) {
-            const double lck = __shfl_sync(0xffffffffu, lk, c);
-            if (r >= c) row[c] -= lk * lck;
-          }
-        }
+        for (int t = 0; t < 4; ++t) {
+          double acc = 0.0;
 #pragma unroll
-        for (int c = 0; c < NB; ++c) P[r * (NB + 1) + c] = c <= r ? row[c] : 0.0;
-        rcp[r] = my_rcp;
-        __syncwarp();
-        // Li = inv(L): lane c builds column c directly in shared memory
-        const int c = lane;
-#pragma unroll
-        for (int rr = 0; rr < NB; ++rr) {
-          double a0 = rr == c ? 1.0 : 0.0, a1 = 0.0;
-          for (int k = c; k + 1 < rr; k += 2) {
-            a0 -= P[rr * (NB + 1) + k] * Li[k * (NB + 1) + c];
-            a1 -= P[rr * (NB + 1) + k + 1] * Li[(k + 1) * (NB + 1) + c];
-          }
-          if (((rr - c) & 1) && rr > c) a0 -= P[rr * (NB + 1) + rr - 1] * Li[(rr - 1) * (NB + 1) + c];
-          Li[rr * (NB + 1) + c] = (rr < nbk && c < nbk && rr >= c) ? (a0 + a1) * rcp[rr] : 0.0;
+          for (int t2 = 0; t2 <= t; ++t2) acc += p[t2] * i4[t][t2];
+          pan[r * 4 + t] = acc;
         }
       }
       __syncthreads();
-      PROF_MARK(1);
-      double a[ZR][NB];
+      const int m = nbk - kb - w4;
+      for (int e = tid; e < m * m; e += kFT) {
+        const int rr = e / m, cc = e - rr * m;
+        if (cc > rr) continue;
+        const int r = kb + w4 + rr, c = kb + w4 + cc;
+        double acc = 0.0;
 #pragma unroll
-      for (int q = 0; q < ZR; ++q) {
-        const int i = tid + kFT * q;
-        const bool live = i < kd && (i < k0 || i >= k1);
-#pragma unroll
-        for (int c = 0; c < NB; ++c)
-          a[q][c] = (live && c < nbk) ? (i > k0 ? D[static_cast<long long>(i) * kd + k0 + c]
-                                                : D[static_cast<long long>(k0 + c) * kd + i])
-                                      : 0.0;
+        for (int t = 0; t < 4; ++t) acc += pan[r * 4 + t] * pan[c * 4 + t];
+        P[r * (NB + 1) + c] -= acc;
       }
-      PROF_MARK(2);
-      // ---- Z = A_RK Li^T for every row outside K (each CTA keeps the whole Z); each Li
-      // element read from shared memory feeds ZR rows
+      for (int e = tid; e < nbk * 4; e += kFT) {
+        const int r = e >> 2, t = e & 3;
+        if (t >= w4) continue;
+        if (r >= kb + w4) P[r * (NB + 1) + kb + t] = pan[r * 4 + t];
+        else if (r >= kb && r - kb >= t) P[r * (NB + 1) + kb + t] = l4[r - kb][t];
+      }
+      if (tid < 16) dinv4[(kb >> 2) * 16 + tid] = i4[tid >> 2][tid & 3];
+      __syncthreads();
+    }
+#pragma unroll 1
+    for (int rb = 0; rb < nbk; rb += 4) {
+      const int w4 = min(4, nbk - rb);
+      double i4[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) i4[a][b] = dinv4[(rb >> 2) * 16 + a * 4 + b];
+      for (int e = tid; e < 4 * rb; e += kFT) {
+        const int a = e / rb, c = e - a * rb;
+        double acc = 0.0;
+        if (a < w4)
+          for (int k = c; k < rb; ++k) acc += P[(rb + a) * (NB + 1) + k] * Li[k * (NB + 1) + c];
+        pan[a * NB + c] = acc;
+      }
+      __syncthreads();
+      for (int e = tid; e < 4 * (rb + 4); e += kFT) {
+        const int a = e / (rb + 4), c = e - a * (rb + 4);
+        if (a >= w4) continue;
+        double v;
+        if (c < rb) {
+          v = 0.0;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) v -= (t <= a ? i4[a][t] : 0.0) * (t < w4 ? pan[t * NB + c] : 0.0);
+        } else {
+          const int t = c - rb;
+          v = (t <= a && t < w4) ? i4[a][t] : 0.0;
+        }
+        Li[(rb + a) * (NB + 1) + c] = v;
+      }
+      __syncthreads();
+    }
+    PROF_MARK(1);
+    // ---- Z = A_RK Li^T, thread per row: all loads issued first, 32 independent chains
+    for (int i = tid; i < kdp; i += kFT) {
+      const bool live = i < kd && (i < k0 || i >= k1);
+      double a[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        a[c] = (live && c < nbk) ? (i > k0 ? D[static_cast<long long>(i) * kd + k0 + c]
+                                           : D[static_cast<long long>(k0 + c) * kd + i])
+                                 : 0.0;
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
-        double acc[ZR];
-#pragma unroll
-        for (int q = 0; q < ZR; ++q) acc[q] = 0.0;
-#pragma unroll
-        for (int c2 = 0; c2 <= c; ++c2) {
-          const double li = Li[c * (NB + 1) + c2];
-#pragma unroll
-          for (int q = 0; q < ZR; ++q) acc[q] = fma(a[q][c2], li, acc[q]);
-        }
-#pragma unroll
-        for (int q = 0; q < ZR; ++q) {
-          const int i = tid + kFT * q;
-          if (i < kdp) Z[c * kdp + i] = acc[q];
-        }
-      }
-      PROF_MARK(3);
-      cl_sync();  // Z complete everywhere; all reads of A_RK done before it is overwritten
-      PROF_MARK(4);
-      // ---- A_RR -= Z Z^T over the lower triangle (K excluded): 64x32 warp tiles spread
-      // over the cluster's warps; thread tile 8x8 with rows ub0+16q+2ui+{0,1} and columns
-      // vb0+8q+2vi+{0,1} so that shared-memory reads are conflict-free double2 loads
-      {
-        const int ui = lane & 7, vi = lane >> 3;
-        const int nmu = (kd + 63) / 64, nmv_all = (kd + 31) / 32;
-        int MU = 0, MV = 0, m = 0;  // walk the (MU, MV) list, taking every GW-th entry
-        auto advance = [&](int steps) {
-          while (steps-- > 0) {
-            if (++MV >= min(nmv_all, 2 * MU + 2)) MV = 0, ++MU;
-          }
-        };
-        advance(gwarp);
-        m = gwarp;
-        for (; MU < nmu; advance(GW), m += GW) {
-          {
-            const int ub0 = 64 * MU + 2 * ui, vb0 = 32 * MV + 2 * vi;
-            double acc[8][8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-#pragma unroll
-              for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-#pragma unroll 2
-            for (int c = 0; c < nbk; ++c) {
-              const double* zc = Z + c * kdp;
-              double a[8], b[8];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const double2 x = *reinterpret_cast<const double2*>(zc + ub0 + 16 * q);
-                const double2 y = *reinterpret_cast<const double2*>(zc + vb0 + 8 * q);
-                a[2 * q] = x.x, a[2 * q + 1] = x.y;
-                b[2 * q] = y.x, b[2 * q + 1] = y.y;
-              }
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int u = ub0 + 16 * (i >> 1) + (i & 1);
-              if (u >= kd || (u >= k0 && u < k1)) continue;
-              double* rowp = D + static_cast<long long>(u) * kd;
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const int v = vb0 + 8 * (j >> 1) + (j & 1);
-                if (v <= u && (v < k0 || v >= k1)) rowp[v] -= acc[i][j];
-              }
-            }
-          }
-        }
-      }
-      PROF_MARK(5);
-      // ---- A_RK <- Z Li ; A_KK <- -Li^T Li   (entries disjoint from the update above)
-      for (int i = gtid; i < kd; i += GT) {
-        if (i >= k0 && i < k1) continue;
-        double z[NB];
-#pragma unroll
-        for (int c = 0; c < NB; ++c) z[c] = Z[c * kdp + i];
-#pragma unroll
-        for (int c = 0; c < NB; ++c) {
-          if (c < nbk) {
-            double acc = 0.0;
-#pragma unroll
-            for (int c2 = c; c2 < NB; ++c2) acc = fma(z[c2], Li[c2 * (NB + 1) + c], acc);
-            if (i > k0)
-              D[static_cast<long long>(i) * kd + k0 + c] = acc;
-            else
-              D[static_cast<long long>(k0 + c) * kd + i] = acc;
-          }
-        }
-      }
-      for (int e = gtid; e < nbk * nbk; e += GT) {
-        const int a = e / nbk, b = e - a * nbk;
-        if (b > a) continue;
         double acc = 0.0;
-        for (int mm = a; mm < nbk; ++mm) acc += Li[mm * (NB + 1) + a] * Li[mm * (NB + 1) + b];
-        D[static_cast<long long>(k0 + a) * kd + k0 + b] = -acc;
+#pragma unroll
+        for (int c2 = 0; c2 <= c; ++c2) acc = fma(a[c2], Li[c * (NB + 1) + c2], acc);
+        Z[c * kdp + i] = acc;
       }
-      PROF_MARK(6);
-      cl_sync();
-      PROF_MARK(7);
     }
-    // ---- Dinv_l = -D, packed rows
-    double* Fl = F + static_cast<long long>(l) * s.line_sz;
-    for (int i = gwarp; i < kd; i += GW) {
-      const long long o = prow_off(i);
-      for (int j = lane; j <= i; j += 32) Fl[o + j] = -D[static_cast<long long>(i) * kd + j];
-      if ((i & 1) == 0 && lane == 0) Fl[o + i + 1] = 0.0;  // pad of even rows
+    __syncthreads();
+    PROF_MARK(2);
+    // ---- A_RR -= Z Z^T over the lower triangle (K excluded): 32x32 warp tiles, 4x8 thread
+    // tiles (rows ub0+16q+2ui+{0,1}, columns vb0+8q+2vi+{0,1}: conflict-free double2 reads)
+    {
+      const int ui = lane & 7, vi = lane >> 3;
+      const int nt = (kd + 31) / 32;
+      int TU = 0, TV = 0;
+      auto advance = [&](int steps) {
+        while (steps-- > 0) {
+          if (++TV > TU) TV = 0, ++TU;
+        }
+      };
+      advance(warp);
+      for (; TU < nt; advance(kFW)) {
+        const int ub0 = 32 * TU + 2 * ui, vb0 = 32 * TV + 2 * vi;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // the tile's read-modify-write targets -> L1
+          const int u = ub0 + 16 * (i >> 1) + (i & 1);
+          if (u < kd && (vi & 1) == 0)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(D + static_cast<long long>(u) * kd + 32 * TV + 8 * vi));
+        }
+        double acc[4][8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+#pragma unroll 2
+        for (int c = 0; c < nbk; ++c) {
+          const double* zc = Z + c * kdp;
+          double a[4], b[8];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const double2 x = *reinterpret_cast<const double2*>(zc + ub0 + 16 * q);
+            a[2 * q] = x.x, a[2 * q + 1] = x.y;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double2 y = *reinterpret_cast<const double2*>(zc + vb0 + 8 * q);
+            b[2 * q] = y.x, b[2 * q + 1] = y.y;
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int u = ub0 + 16 * (i >> 1) + (i & 1);
+          if (u >= kd || (u >= k0 && u < k1)) continue;
+          double* rowp = D + static_cast<long long>(u) * kd;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int v = vb0 + 8 * (j >> 1) + (j & 1);
+            if (v <= u && (v < k0 || v >= k1)) rowp[v] -= acc[i][j];
+          }
+        }
+      }
     }
-    cl_sync();
-    PROF_MARK(8);
+    PROF_MARK(3);
+    // ---- A_RK <- Z Li ; A_KK <- -Li^T Li   (entries disjoint from the update above)
+    for (int i = tid; i < kd; i += kFT) {
+      if (i >= k0 && i < k1) continue;
+      double z[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c) z[c] = Z[c * kdp + i];
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        if (c < nbk) {
+          double acc = 0.0;
+#pragma unroll
+          for (int c2 = c; c2 < NB; ++c2) acc = fma(z[c2], Li[c2 * (NB + 1) + c], acc);
+          if (i > k0)
+            D[static_cast<long long>(i) * kd + k0 + c] = acc;
+          else
+            D[static_cast<long long>(k0 + c) * kd + i] = acc;
+        }
+      }
+    }
+    for (int e = tid; e < nbk * nbk; e += kFT) {
+      const int a = e / nbk, b = e - a * nbk;
+      if (b > a) continue;
+      double acc = 0.0;
+      for (int mm = a; mm < nbk; ++mm) acc += Li[mm * (NB + 1) + a] * Li[mm * (NB + 1) + b];
+      D[static_cast<long long>(k0 + a) * kd + k0 + b] = -acc;
+    }
+    __syncthreads();
+    PROF_MARK(4);
+  }
+}
+
+// D <- A_ll - sum over the given neighbour lines of B (inv_nb) B  (lower triangle)
+__device__ void build_line(const SubInfo& s, const double* __restrict__ coef, size_t N, int W,
+                           int nc, int l, int nb0, int bl0, int nb1, int bl1,
+                           const double* __restrict__ F, double* __restrict__ D) {
+  // neighbour nbX (line index or -1) with coupling taken at line blX (bcoef(blX): between
+  // lines blX and blX-1)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kd = s.kd;
+  for (int i = warp; i < kd; i += kFW) {
+    const double b0i = nb0 >= 0 ? bcoef(s, coef, N, W, nc, bl0, i) : 0.0;
+    const double b1i = nb1 >= 0 ? bcoef(s, coef, N, W, nc, bl1, i) : 0.0;
+    const long long oi = prow_off(i);
+    for (int j = lane; j <= i; j += 32) {
+      double v = aline(s, coef, N, W, nc, l, i, j);
+      if (nb0 >= 0)
+        v -= b0i * bcoef(s, coef, N, W, nc, bl0, j) * F[static_cast<long long>(nb0) * s.line_sz + oi + j];
+      if (nb1 >= 0)
+        v -= b1i * bcoef(s, coef, N, W, nc, bl1, j) * F[static_cast<long long>(nb1) * s.line_sz + oi + j];
+      D[static_cast<long long>(i) * kd + j] = v;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ void pack_line(const SubInfo& s, int l, const double* __restrict__ D, double* F) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kd = s.kd;
+  double* Fl = F + static_cast<long long>(l) * s.line_sz;
+  for (int i = warp; i < kd; i += kFW) {
+    const long long o = prow_off(i);
+    for (int j = lane; j <= i; j += 32) Fl[o + j] = -D[static_cast<long long>(i) * kd + j];
+    if ((i & 1) == 0 && lane == 0) Fl[o + i + 1] = 0.0;  // pad of even rows
+  }
+  __syncthreads();
+}
+
+// one CTA per (subdomain, chain): chain 0 lines 0..m-1 downward, chain 1 lines L-1..m+1
+// upward; mid = 1 launches one CTA per subdomain for the middle line
+template <int NB>
+__global__ void __launch_bounds__(kFT, 1)
+    k_line_factor(const SubInfo* __restrict__ subs, const double* __restrict__ coef, size_t N,
+                  int W, int nc, double* __restrict__ fac, double* __restrict__ scratch,
+                  long long scratch_stride, int kdp, int mid, int* __restrict__ bad) {
+  const int sub = mid ? blockIdx.x : blockIdx.x >> 1;
+  const int chain = mid ? 0 : blockIdx.x & 1;
+  const SubInfo s = subs[sub];
+  const int tid = threadIdx.x;
+  const int kd = s.kd, L = s.L, m = mid_line(L);
+  double* D = scratch + (mid ? sub : blockIdx.x) * scratch_stride;
+  double* F = fac + s.fac_off;
+  extern __shared__ __align__(16) double fsm[];
+  double* P = fsm;                    // NB x (NB+1)
+  double* Li = P + NB * (NB + 1);     // NB x (NB+1)
+  double* pan = Li + NB * (NB + 1);   // 4 x NB
+  double* dinv4 = pan + 4 * NB;       // NB/4 x 16
+  double* Z = dinv4 + 4 * NB;         // NB x kdp
+  for (int e = tid; e < NB * kdp; e += kFT) Z[e] = 0.0;
+  int first_bad = 0x7fffffff;
+  PROF_DECL
+  if (mid) {
+    build_line(s, coef, N, W, nc, m, m > 0 ? m - 1 : -1, m, m < L - 1 ? m + 1 : -1, m + 1, F, D);
+    PROF_MARK(0);
+    sweep_invert<NB>(D, kd, kdp, fsm, Li, pan, dinv4, Z, first_bad, m * kd);
+    pack_line(s, m, D, F);
+  } else {
+    const int nlines = chain == 0 ? m : L - 1 - m;
+    for (int t = 0; t < nlines; ++t) {
+      const int l = chain == 0 ? t : L - 1 - t;
+      const int prev = t == 0 ? -1 : (chain == 0 ? l - 1 : l + 1);
+      const int bl = chain == 0 ? l : l + 1;  // coupling between l and prev
+      build_line(s, coef, N, W, nc, l, prev, bl, -1, 0, F, D);
+      PROF_MARK(0);
+      sweep_invert<NB>(D, kd, kdp, fsm, Li, pan, dinv4, Z, first_bad, l * kd);
+      pack_line(s, l, D, F);
+      PROF_MARK(5);
+    }
   }
   PROF_FLUSH(0);
-  if (crank == 0 && tid == 0 && first_bad != 0x7fffffff) atomicMin(bad + sub, first_bad);
+  if (tid == 0 && first_bad != 0x7fffffff) atomicMin(bad + sub, first_bad);
 }
 
 // ----------------------------------------------------------------- K6 solve
@@ -437,20 +548,37 @@ __device__ __forceinline__ int chunk_end(int r0, int rhi, long long cap) {
   return r1;
 }
 
+// Lines visited by (phase, chain): forward 0: 0..m-1, forward 1: L-1..m+1;
+// backward c: m first (the middle, computed by both chains), then m-1..0 / m+1..L-1.
+__device__ __forceinline__ int chain_len(int phase, int chain, int L) {
+  const int m = mid_line(L);
+  const int len = chain == 0 ? m : L - 1 - m;
+  return phase == 0 ? len : len + 1;
+}
+__device__ __forceinline__ int chain_line(int phase, int chain, int L, int t) {
+  const int m = mid_line(L);
+  if (phase == 0) return chain == 0 ? t : L - 1 - t;
+  return chain == 0 ? m - t : m + t;
+}
+
+// One sweep (phase 0 forward / 1 backward) of both chains of every subdomain: cluster of C
+// CTAs per (subdomain, chain); each line's packed rows are split over the cluster (equal
+// entry counts) and the symmetric products combined through distributed shared memory.
 template <int MAXM>
 __global__ void __launch_bounds__(kST, 1)
     k_line_solve(const SubInfo* __restrict__ subs, const double* __restrict__ fac,
                  const double* __restrict__ coef, size_t N, const double* __restrict__ r,
                  double* __restrict__ ylocal, double* __restrict__ zlocal, int W, int nc,
-                 int stages, int cap, int kd_max, const int* __restrict__ flags) {
-  if (flags && (flags[0] | flags[1])) return;  // PCG converged or failed (cluster-uniform)
+                 int stages, int cap, int kd_max, int phase, const int* __restrict__ flags) {
+  if (flags && (flags[0] | flags[1])) return;  // PCG converged or failed (grid-uniform)
   const int C = static_cast<int>(cl_size()), crank = static_cast<int>(cl_rank());
-  const int sub = blockIdx.x / C;
+  const int cid = blockIdx.x / C;  // (subdomain, chain)
+  const int sub = cid >> 1, chain = cid & 1;
   const SubInfo s = subs[sub];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int kd = s.kd, L = s.L;
+  const int kd = s.kd, L = s.L, m = mid_line(L);
+  const int nl = chain_len(phase, chain, L);
   const int rlo = row_lo(crank, C, kd), rhi = row_lo(crank + 1, C, kd);
-  const int share = (kd + C - 1) / C + kd;  // upper bound on any CTA's row count
   const double* F = fac + s.fac_off;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
@@ -462,7 +590,7 @@ __global__ void __launch_bounds__(kST, 1)
   double* red = xprev + kd_max;                                  // 8 x kd_max reduce slots
   double* yl = ylocal + s.vec_off;
   double* zl = zlocal + s.vec_off;
-  (void)share;
+  if (nl == 0) return;  // cluster-uniform
 
   if (tid == 0) {
     for (int q = 0; q < stages; ++q) mbar_init(&bar[q], 1);
@@ -471,12 +599,10 @@ __global__ void __launch_bounds__(kST, 1)
   for (int j = tid; j < kd_max; j += kST) xprev[j] = 0.0;
   __syncthreads();
 
-  const int nlines_total = L + (L - 1);  // forward lines 0..L-1, backward L-2..0
-  auto line_of = [&](int li) { return li < L ? li : (L - 2) - (li - L); };
-  int p_seq = 0, p_li = 0, p_r0 = rlo;  // producer (thread 0)
+  int p_seq = 0, p_t = 0, p_r0 = rlo;  // producer (thread 0)
   auto produce = [&]() {
-    if (p_li >= nlines_total || rlo >= rhi) return;
-    const int l = line_of(p_li);
+    if (p_t >= nl || rlo >= rhi) return;
+    const int l = chain_line(phase, chain, L, p_t);
     const int r1 = chunk_end(p_r0, rhi, cap);
     const long long o0 = prow_off(p_r0), o1 = prow_off(r1);
     const int st = p_seq % stages;
@@ -488,133 +614,139 @@ __global__ void __launch_bounds__(kST, 1)
     p_r0 = r1;
     if (p_r0 >= rhi) {
       p_r0 = rlo;
-      ++p_li;
+      ++p_t;
     }
   };
   if (tid == 0)
     for (int q = 0; q < stages; ++q) produce();
 
-  // operands of the next line are prefetched into registers one line ahead: r_l and B_l
-  // (forward), B_{l+1} and y_l of the owned rows (backward); only x_{l-1} / x_{l+1} (from
-  // the previous line, in shared memory) is on the line-to-line critical path
+  // operand of line step t, prefetched into registers one step ahead. Forward:
+  // w = r_l - b_prev o y_prev; backward middle: w = r_m - b_m y_{m-1} - b_{m+1} y_{m+1};
+  // backward chain: w = b_next o x_next and x_l = y_l - Dinv_l w.
   constexpr int PS = 2;  // j = tid + kST*q, kd <= 2*kST
   double pf_r[PS], pf_b[PS], pf_y[PS];
-  auto prefetch = [&](int li) {
+  auto prefetch = [&](int t) {
 #pragma unroll
     for (int q = 0; q < PS; ++q) {
       pf_r[q] = pf_b[q] = pf_y[q] = 0.0;
-      if (li >= nlines_total) continue;
-      const bool fw = li < L;
-      const int l = line_of(li);
+      if (t >= nl) continue;
+      const int l = chain_line(phase, chain, L, t);
       const int j = tid + kST * q;
       if (j < kd) {
-        if (fw) {
+        if (phase == 0) {
           pf_r[q] = r[gidx(s, l, j, W, nc)];
-          if (l > 0) pf_b[q] = bcoef(s, coef, N, W, nc, l, j);
+          if (t > 0) pf_b[q] = bcoef(s, coef, N, W, nc, chain == 0 ? l : l + 1, j);
+        } else if (t == 0) {  // middle line: both neighbours from the forward sweep
+          double w = r[gidx(s, l, j, W, nc)];
+          if (m > 0) w -= bcoef(s, coef, N, W, nc, m, j) * yl[static_cast<long long>(m - 1) * kd + j];
+          if (m < L - 1)
+            w -= bcoef(s, coef, N, W, nc, m + 1, j) * yl[static_cast<long long>(m + 1) * kd + j];
+          pf_r[q] = w;
         } else {
-          pf_b[q] = bcoef(s, coef, N, W, nc, l + 1, j);
+          pf_b[q] = bcoef(s, coef, N, W, nc, chain == 0 ? l + 1 : l, j);
         }
       }
       const int jo = rlo + tid + kST * q;  // owned row
-      if (!fw && jo < rhi) pf_y[q] = yl[static_cast<long long>(l) * kd + jo];
+      if (phase == 1 && t > 0 && jo < rhi) pf_y[q] = yl[static_cast<long long>(l) * kd + jo];
     }
   };
   prefetch(0);
   PROF_DECL
 
   int c_seq = 0;
-  for (int li = 0; li < nlines_total; ++li) {
-    const bool fwd = li < L;
-    const int l = line_of(li);
+  for (int t = 0; t < nl; ++t) {
+    const int l = chain_line(phase, chain, L, t);
+    const bool subtract = phase == 1 && t > 0;  // x_l = y_l - Dinv_l w
     double cur_y[PS];
 #pragma unroll
     for (int q = 0; q < PS; ++q) {
       const int j = tid + kST * q;
-      if (j < kd) wv[j] = fwd ? pf_r[q] - pf_b[q] * xprev[j] : pf_b[q] * xprev[j];
+      if (j < kd)
+        wv[j] = (phase == 0) ? pf_r[q] - pf_b[q] * xprev[j]
+                             : (t == 0 ? pf_r[q] : pf_b[q] * xprev[j]);
       cur_y[q] = pf_y[q];
     }
-    prefetch(li + 1);
+    prefetch(t + 1);
     __syncthreads();
     PROF_MARK(0);
     double colacc[MAXM];
 #pragma unroll
-    for (int m = 0; m < MAXM; ++m) colacc[m] = 0.0;
+    for (int mm = 0; mm < MAXM; ++mm) colacc[mm] = 0.0;
     int r0 = rlo;
     while (r0 < rhi) {
       const int r1 = chunk_end(r0, rhi, cap);
       const int st = c_seq % stages;
-      PROF_MARK(1);
       mbar_wait(&bar[st], (c_seq / stages) & 1);
-      PROF_MARK(2);
+      PROF_MARK(1);
       const double* Sb = stage0 + static_cast<size_t>(st) * cap - prow_off(r0);
       for (int i = r0 + warp; i < r1; i += kSW) {
         const double* Si = Sb + prow_off(i);
         const double wi = wv[i];
         double racc = 0.0;
 #pragma unroll
-        for (int m = 0; m < MAXM; ++m) {
-          const int j = lane + 32 * m;
-          if (32 * m > i) break;
+        for (int mm = 0; mm < MAXM; ++mm) {
+          const int j = lane + 32 * mm;
+          if (32 * mm > i) break;
           if (j <= i) {
             const double sij = Si[j];
             racc = fma(sij, wv[j], racc);
-            if (j < i) colacc[m] = fma(sij, wi, colacc[m]);
+            if (j < i) colacc[mm] = fma(sij, wi, colacc[mm]);
           }
         }
 #pragma unroll
         for (int off = 16; off; off >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, off);
         if (lane == 0) yrow[i] = racc;
       }
-      PROF_MARK(3);
       __syncthreads();
-      PROF_MARK(4);
+      PROF_MARK(2);
       if (tid == 0) produce();
       ++c_seq;
       r0 = r1;
     }
 #pragma unroll
-    for (int m = 0; m < MAXM; ++m) {
-      const int j = lane + 32 * m;
-      if (j < rhi) colpart[warp * kd_max + j] = colacc[m];
+    for (int mm = 0; mm < MAXM; ++mm) {
+      const int j = lane + 32 * mm;
+      if (j < rhi) colpart[warp * kd_max + j] = colacc[mm];
     }
     __syncthreads();
-    PROF_MARK(5);
+    PROF_MARK(3);
     // column partials of this CTA (+ its own row dots), reduced in a fixed warp order and
     // scattered to the CTA that owns each row
     int owner = 0;
     for (int j = tid; j < rhi; j += kST) {
-      double t = (j >= rlo) ? yrow[j] : 0.0;
+      double tv = (j >= rlo) ? yrow[j] : 0.0;
 #pragma unroll 4
-      for (int w = 0; w < kSW; ++w) t += colpart[w * kd_max + j];
+      for (int w = 0; w < kSW; ++w) tv += colpart[w * kd_max + j];
       while (owner + 1 < C && row_lo(owner + 1, C, kd) <= j) ++owner;
       if (C == 1)
-        red[j] = t;
+        red[j] = tv;
       else
-        cl_map(red, static_cast<unsigned>(owner))[crank * kd_max + j] = t;
+        cl_map(red, static_cast<unsigned>(owner))[crank * kd_max + j] = tv;
     }
-    PROF_MARK(6);
     if (C == 1) __syncthreads(); else cl_sync();
-    PROF_MARK(7);
-    // owners finish their rows (contributions from CTAs crank..C-1, ascending) and
-    // broadcast the line's result to every CTA
+    PROF_MARK(4);
 #pragma unroll
     for (int q = 0; q < PS; ++q) {
       const int j = rlo + tid + kST * q;
       if (j >= rhi) continue;
-      double t = 0.0;
+      double tv = 0.0;
       if (C == 1) {
-        t = red[j];
+        tv = red[j];
       } else {
-        for (int c = crank; c < C; ++c) t += red[c * kd_max + j];
+        for (int c = crank; c < C; ++c) tv += red[c * kd_max + j];
       }
       const long long k = static_cast<long long>(l) * kd + j;
       double v;
-      if (fwd) {
-        yl[k] = t;
-        if (l == L - 1) zl[k] = t;  // x_{L-1} = y_{L-1}
-        v = t;
+      if (!subtract) {
+        v = tv;
+        if (phase == 0) {
+          yl[k] = v;
+          if (L == 1) zl[k] = v;
+        } else if (chain == 0) {
+          zl[k] = v;  // middle line, written once
+        }
       } else {
-        v = cur_y[q] - t;
+        v = cur_y[q] - tv;
         zl[k] = v;
       }
       if (C == 1) {
@@ -623,9 +755,8 @@ __global__ void __launch_bounds__(kST, 1)
         for (int c = 0; c < C; ++c) cl_map(xprev, static_cast<unsigned>(c))[j] = v;
       }
     }
-    PROF_MARK(8);
     if (C == 1) __syncthreads(); else cl_sync();
-    PROF_MARK(9);
+    PROF_MARK(5);
   }
   PROF_FLUSH(16);
 }
@@ -667,24 +798,33 @@ static void launch_cluster(K kernel, int nblocks, int threads, size_t smem, int 
   FFB_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
 }
 
-void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max, const double* coef,
-                 size_t N, int W, int nc, double* fac, double* scratch, long long scratch_stride,
-                 int* d_bad, cudaStream_t st) {
-  const int kdp = (kd_max + 63) / 64 * 64;
-  const size_t smem =
-      (2 * nb * (nb + 1) + nb + static_cast<size_t>(nb) * kdp) * sizeof(double);
+size_t factor_scratch_doubles(int nsub, int kd_max) {
+  return static_cast<size_t>(2 * nsub) * kd_max * kd_max;
+}
+
+void line_factor(const SubInfo* d_subs, int nsub, int /*C*/, int nb, int kd_max,
+                 const double* coef, size_t N, int W, int nc, double* fac, double* scratch,
+                 long long scratch_stride, int* d_bad, cudaStream_t st) {
+  const int kdp = (kd_max + 31) / 32 * 32;
+  const size_t smem = (2 * nb * (nb + 1) + 8 * nb + static_cast<size_t>(nb) * kdp) * sizeof(double);
   if (smem > 227 * 1024) fail("linsolve.cholesky: subdomain line too wide for shared memory");
-  const int zr = (kdp + kFT - 1) / kFT;
-#define FFB_FACTOR(NBV, ZRV)                                                                 \
-  launch_cluster(k_line_factor<NBV, ZRV>, nsub * C, kFT, smem, C, st, d_subs, coef, N, W, nc, \
-                 fac, scratch, scratch_stride, kdp, d_bad)
-  if (nb == 32 && zr <= 1) FFB_FACTOR(32, 1);
-  else if (nb == 32 && zr <= 2) FFB_FACTOR(32, 2);
-  else if (nb == 16 && zr <= 2) FFB_FACTOR(16, 2);
-  else if (nb == 16 && zr <= 4) FFB_FACTOR(16, 4);
-  else fail("internal: unsupported pivot block / line width combination");
-#undef FFB_FACTOR
-  FFB_LAUNCHED();
+  for (int mid = 0; mid <= 1; ++mid) {
+    const int grid = mid ? nsub : 2 * nsub;
+    if (nb == 32) {
+      FFB_CUDA(cudaFuncSetAttribute(k_line_factor<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      k_line_factor<32><<<grid, kFT, smem, st>>>(d_subs, coef, N, W, nc, fac, scratch,
+                                                 scratch_stride, kdp, mid, d_bad);
+    } else if (nb == 16) {
+      FFB_CUDA(cudaFuncSetAttribute(k_line_factor<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      k_line_factor<16><<<grid, kFT, smem, st>>>(d_subs, coef, N, W, nc, fac, scratch,
+                                                 scratch_stride, kdp, mid, d_bad);
+    } else {
+      fail("internal: unsupported pivot block size");
+    }
+    FFB_LAUNCHED();
+  }
 }
 
 SolvePlan solve_plan(int kd_max, int C) {
@@ -693,7 +833,7 @@ SolvePlan solve_plan(int kd_max, int C) {
   const size_t fixed =
       128 + (static_cast<size_t>(kSW) * kd_max + 3 * kd_max + 8 * kd_max) * sizeof(double);
   const size_t budget = 227 * 1024 - 1024;
-  if (fixed + 2 * 1024 * sizeof(double) > budget)
+  if (kd_max > 2 * kST || fixed + 2 * 1024 * sizeof(double) > budget)
     fail("linsolve.cholesky: subdomain line too wide for the solve kernel");
   const size_t avail = budget - fixed;
   int stages = 3;
@@ -716,8 +856,11 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
                            const double* fac, const double* coef, size_t N, const double* r,
                            double* ylocal, double* zlocal, int W, int nc, const int* flags,
                            cudaStream_t st) {
-  launch_cluster(k_line_solve<M>, nsub * pl.C, kST, pl.smem, pl.C, st, d_subs, fac, coef, N, r,
-                 ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, flags);
+  for (int phase = 0; phase <= 1; ++phase) {
+    launch_cluster(k_line_solve<M>, 2 * nsub * pl.C, kST, pl.smem, pl.C, st, d_subs, fac, coef, N,
+                   r, ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, phase, flags);
+    FFB_LAUNCHED();
+  }
 }
 
 void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,
@@ -735,7 +878,6 @@ void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const doub
     launch_solve_m<26>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, st);
   else
     fail("linsolve.cholesky: subdomain line too wide (kd > 832)");
-  FFB_LAUNCHED();
 }
 
 }  // namespace ffb

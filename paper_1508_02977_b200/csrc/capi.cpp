@@ -235,7 +235,7 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
   }
   // CTAs per subdomain (one thread-block cluster): enough that ~128 SMs take part
   c->ccl = 1;
-  while (c->ccl < 8 && np * c->ccl * 2 <= 160) c->ccl *= 2;
+  while (c->ccl < 8 && 2 * np * c->ccl * 2 <= 160) c->ccl *= 2;  // 2 chains per subdomain
   if (const char* e = std::getenv("FFB_CLUSTER")) {
     const int v = std::atoi(e);
     if (v == 1 || v == 2 || v == 4 || v == 8) c->ccl = v;
@@ -301,7 +301,7 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
   FFB_CUDA(cudaMemcpyAsync(c->d_row.p, row.data(), H * sizeof(AxisMap), cudaMemcpyHostToDevice,
                            c->st));
   c->fac.ensure(fac_off);
-  c->dscratch.ensure(static_cast<size_t>(np) * kd_max * kd_max);
+  c->dscratch.ensure(factor_scratch_doubles(np, kd_max));
   c->ylocal.ensure(vec_off);
   c->zlocal.ensure(vec_off);
   c->d_bad.ensure(np);

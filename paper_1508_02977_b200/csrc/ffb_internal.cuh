@@ -83,6 +83,7 @@ struct AxisMap {  // free-rectangle membership along one axis (<= 2 parts)
 };
 
 long long packed_line_size(int kd);
+size_t factor_scratch_doubles(int nsub, int kd_max);
 void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max, const double* coef,
                  size_t N, int W, int nc, double* fac, double* scratch, long long scratch_stride,
                  int* d_bad, cudaStream_t st);

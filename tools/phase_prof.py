@@ -17,9 +17,9 @@ lib.ffb_debug_prof(buf, 1)
 r = ff.run_on_frames(f0, f1, rc, ctx)
 lib.ffb_debug_prof(buf, 1)
 print(name, "factor ms", r.stats.ms_factor, "pcg ms", r.stats.ms_pcg, "iters", r.stats.iters)
-fn = ["buildD", "chol", "Li", "Z", "sync1", "Rupd", "X", "sync2", "pack"]
-tot = sum(buf[i] for i in range(9)) or 1
-print("factor CTA0 cycles:", {fn[i]: f"{buf[i]/1e6:.1f}M ({100*buf[i]/tot:.0f}%)" for i in range(9)})
-sn = ["operand", "chunkpre", "mbarwait", "rows", "sync", "colflush", "reduce", "clsync1", "owner", "clsync2"]
-tot = sum(buf[16 + i] for i in range(10)) or 1
-print("solve CTA0 cycles:", {sn[i]: f"{buf[16+i]/1e6:.2f}M ({100*buf[16+i]/tot:.0f}%)" for i in range(10)})
+fn = ["buildD", "pivot", "Z", "Rupd", "X+sync", "pack"]
+tot = sum(buf[i] for i in range(6)) or 1
+print("factor CTA0 cycles:", {fn[i]: f"{buf[i]/1e6:.1f}M ({100*buf[i]/tot:.0f}%)" for i in range(6)})
+sn = ["operand", "mbarwait", "rows", "colflush", "reduce+sync", "owner+sync"]
+tot = sum(buf[16 + i] for i in range(6)) or 1
+print("solve CTA0 cycles:", {sn[i]: f"{buf[16+i]/1e6:.2f}M ({100*buf[16+i]/tot:.0f}%)" for i in range(6)})
