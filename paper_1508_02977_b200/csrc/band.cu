@@ -220,6 +220,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
                              double* pan, double* dinv4, double* Z, int& first_bad,
                              int bad_base) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  PROF_DECL
   for (int k0 = 0; k0 < kd; k0 += NB) {
     const int nbk = min(NB, kd - k0);
     const int k1 = k0 + nbk;
@@ -261,21 +262,24 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       }
       for (int e = tid; e < nbk * 4; e += kFT) {
         const int r = e >> 2, t = e & 3;
-        if (t >= w4) continue;
-        if (r >= kb + w4) P[r * (NB + 1) + kb + t] = pan[r * 4 + t];
-        else if (r >= kb && r - kb >= t) P[r * (NB + 1) + kb + t] = l4[r - kb][t];
+        if (t < w4 && r >= kb + w4) P[r * (NB + 1) + kb + t] = pan[r * 4 + t];
       }
-      if (tid < 16) dinv4[(kb >> 2) * 16 + tid] = i4[tid >> 2][tid & 3];
+      if (tid < 16) {  // static register indices only (no local-memory arrays)
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            if (tid == a * 4 + b) {
+              dinv4[(kb >> 2) * 16 + tid] = i4[a][b];
+              if (a < w4 && b <= a) P[(kb + a) * (NB + 1) + kb + b] = l4[a][b];
+            }
+      }
       __syncthreads();
     }
 #pragma unroll 1
     for (int rb = 0; rb < nbk; rb += 4) {
       const int w4 = min(4, nbk - rb);
-      double i4[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) i4[a][b] = dinv4[(rb >> 2) * 16 + a * 4 + b];
+      const double* i4 = dinv4 + (rb >> 2) * 16;  // inverse of the 4x4 diagonal block (smem)
       for (int e = tid; e < 4 * rb; e += kFT) {
         const int a = e / rb, c = e - a * rb;
         double acc = 0.0;
@@ -287,14 +291,12 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       for (int e = tid; e < 4 * (rb + 4); e += kFT) {
         const int a = e / (rb + 4), c = e - a * (rb + 4);
         if (a >= w4) continue;
-        double v;
+        double v = 0.0;
         if (c < rb) {
-          v = 0.0;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) v -= (t <= a ? i4[a][t] : 0.0) * (t < w4 ? pan[t * NB + c] : 0.0);
+          for (int t = 0; t <= a; ++t) v -= i4[a * 4 + t] * pan[t * NB + c];
         } else {
           const int t = c - rb;
-          v = (t <= a && t < w4) ? i4[a][t] : 0.0;
+          v = (t <= a && t < w4) ? i4[a * 4 + t] : 0.0;
         }
         Li[(rb + a) * (NB + 1) + c] = v;
       }
@@ -407,6 +409,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
     __syncthreads();
     PROF_MARK(4);
   }
+  PROF_FLUSH(32);
 }
 
 // D <- A_ll - sum over the given neighbour lines of B (inv_nb) B  (lower triangle)
@@ -679,23 +682,35 @@ __global__ void __launch_bounds__(kST, 1)
       mbar_wait(&bar[st], (c_seq / stages) & 1);
       PROF_MARK(1);
       const double* Sb = stage0 + static_cast<size_t>(st) * cap - prow_off(r0);
-      for (int i = r0 + warp; i < r1; i += kSW) {
-        const double* Si = Sb + prow_off(i);
-        const double wi = wv[i];
-        double racc = 0.0;
+      // each warp keeps 4 rows in flight (independent accumulation chains)
+      for (int i0 = r0 + warp; i0 < r1; i0 += 4 * kSW) {
+        double racc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int mm = 0; mm < MAXM; ++mm) {
-          const int j = lane + 32 * mm;
-          if (32 * mm > i) break;
-          if (j <= i) {
-            const double sij = Si[j];
-            racc = fma(sij, wv[j], racc);
-            if (j < i) colacc[mm] = fma(sij, wi, colacc[mm]);
+        for (int q = 0; q < 4; ++q) {
+          const int i = i0 + q * kSW;
+          if (i >= r1) break;
+          const double* Si = Sb + prow_off(i);
+          const double wi = wv[i];
+#pragma unroll
+          for (int mm = 0; mm < MAXM; ++mm) {
+            const int j = lane + 32 * mm;
+            if (32 * mm > i) break;
+            if (j <= i) {
+              const double sij = Si[j];
+              racc[q] = fma(sij, wv[j], racc[q]);
+              if (j < i) colacc[mm] = fma(sij, wi, colacc[mm]);
+            }
           }
         }
 #pragma unroll
-        for (int off = 16; off; off >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, off);
-        if (lane == 0) yrow[i] = racc;
+        for (int off = 16; off; off >>= 1)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) racc[q] += __shfl_xor_sync(0xffffffffu, racc[q], off);
+        if (lane < 4) {
+          const int i = i0 + lane * kSW;
+          const double v = lane == 0 ? racc[0] : lane == 1 ? racc[1] : lane == 2 ? racc[2] : racc[3];
+          if (i < r1) yrow[i] = v;
+        }
       }
       __syncthreads();
       PROF_MARK(2);

@@ -17,9 +17,10 @@ lib.ffb_debug_prof(buf, 1)
 r = ff.run_on_frames(f0, f1, rc, ctx)
 lib.ffb_debug_prof(buf, 1)
 print(name, "factor ms", r.stats.ms_factor, "pcg ms", r.stats.ms_pcg, "iters", r.stats.iters)
-fn = ["buildD", "pivot", "Z", "Rupd", "X+sync", "pack"]
-tot = sum(buf[i] for i in range(6)) or 1
-print("factor CTA0 cycles:", {fn[i]: f"{buf[i]/1e6:.1f}M ({100*buf[i]/tot:.0f}%)" for i in range(6)})
+fn = ["buildD", "pivot", "Z", "Rupd", "X+sync", "line"]
+vals = [buf[0], buf[33], buf[34], buf[35], buf[36], buf[5]]
+tot = sum(vals) or 1
+print("factor CTA0 cycles:", {fn[i]: f"{vals[i]/1e6:.1f}M ({100*vals[i]/tot:.0f}%)" for i in range(6)})
 sn = ["operand", "mbarwait", "rows", "colflush", "reduce+sync", "owner+sync"]
 tot = sum(buf[16 + i] for i in range(6)) or 1
 print("solve CTA0 cycles:", {sn[i]: f"{buf[16+i]/1e6:.2f}M ({100*buf[16+i]/tot:.0f}%)" for i in range(6)})
