@@ -169,8 +169,7 @@ __device__ __forceinline__ void chol4(const double* src, int ld, int w, double l
         if (tid == 0 && k < w) first_bad = min(first_bad, row0 + k);
         dk = 1.0;
       }
-      const double ir = rsqrt(dk);  // 1/sqrt, then one Newton step to full precision
-      const double irn = ir * (1.5 - 0.5 * dk * ir * ir);
+      const double irn = rsqrt(dk);
       l[k][k] = dk * irn;
       il[k][k] = irn;
 #pragma unroll
@@ -232,11 +231,13 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       Li[a * (NB + 1) + b] = 0.0;
     }
     __syncthreads();
+    PROF_MARK(5);
 #pragma unroll 1
     for (int kb = 0; kb < nbk; kb += 4) {
       const int w4 = min(4, nbk - kb);
       double l4[4][4], i4[4][4];
       chol4(P + kb * (NB + 1) + kb, NB + 1, w4, l4, i4, first_bad, bad_base + k0 + kb, tid);
+      // panel of L below the 4-block
       for (int r = kb + w4 + tid; r < nbk; r += kFT) {
         double p[4];
 #pragma unroll
@@ -248,6 +249,32 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
           for (int t2 = 0; t2 <= t; ++t2) acc += p[t2] * i4[t][t2];
           pan[r * 4 + t] = acc;
         }
+      }
+      // block row kb of Li (rows kb.. of L left of the block are final):
+      //   Li[kb+a][c] = -sum_t i4[a][t] sum_{k=c}^{kb-1} L[kb+t][k] Li[k][c],  c < kb
+      for (int c = tid; c < kb; c += kFT) {
+        double sv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          double acc = 0.0;
+          if (t < w4)
+            for (int k = c; k < kb; ++k) acc += P[(kb + t) * (NB + 1) + k] * Li[k * (NB + 1) + c];
+          sv[t] = acc;
+        }
+#pragma unroll
+        for (int a2 = 0; a2 < 4; ++a2) {
+          double v = 0.0;
+#pragma unroll
+          for (int t = 0; t <= a2; ++t) v -= i4[a2][t] * sv[t];
+          if (a2 < w4) Li[(kb + a2) * (NB + 1) + c] = v;
+        }
+      }
+      if (tid < 16) {  // diagonal blocks of L and Li (static register indices only)
+#pragma unroll
+        for (int a2 = 0; a2 < 4; ++a2)
+#pragma unroll
+          for (int b2 = 0; b2 < 4; ++b2)
+            if (tid == a2 * 4 + b2 && a2 < w4 && b2 <= a2) Li[(kb + a2) * (NB + 1) + kb + b2] = i4[a2][b2];
       }
       __syncthreads();
       const int m = nbk - kb - w4;
@@ -264,44 +291,16 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
         const int r = e >> 2, t = e & 3;
         if (t < w4 && r >= kb + w4) P[r * (NB + 1) + kb + t] = pan[r * 4 + t];
       }
-      if (tid < 16) {  // static register indices only (no local-memory arrays)
+      if (tid < 16) {
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a2 = 0; a2 < 4; ++a2)
 #pragma unroll
-          for (int b = 0; b < 4; ++b)
-            if (tid == a * 4 + b) {
-              dinv4[(kb >> 2) * 16 + tid] = i4[a][b];
-              if (a < w4 && b <= a) P[(kb + a) * (NB + 1) + kb + b] = l4[a][b];
-            }
+          for (int b2 = 0; b2 < 4; ++b2)
+            if (tid == a2 * 4 + b2 && a2 < w4 && b2 <= a2) P[(kb + a2) * (NB + 1) + kb + b2] = l4[a2][b2];
       }
       __syncthreads();
     }
-#pragma unroll 1
-    for (int rb = 0; rb < nbk; rb += 4) {
-      const int w4 = min(4, nbk - rb);
-      const double* i4 = dinv4 + (rb >> 2) * 16;  // inverse of the 4x4 diagonal block (smem)
-      for (int e = tid; e < 4 * rb; e += kFT) {
-        const int a = e / rb, c = e - a * rb;
-        double acc = 0.0;
-        if (a < w4)
-          for (int k = c; k < rb; ++k) acc += P[(rb + a) * (NB + 1) + k] * Li[k * (NB + 1) + c];
-        pan[a * NB + c] = acc;
-      }
-      __syncthreads();
-      for (int e = tid; e < 4 * (rb + 4); e += kFT) {
-        const int a = e / (rb + 4), c = e - a * (rb + 4);
-        if (a >= w4) continue;
-        double v = 0.0;
-        if (c < rb) {
-          for (int t = 0; t <= a; ++t) v -= i4[a * 4 + t] * pan[t * NB + c];
-        } else {
-          const int t = c - rb;
-          v = (t <= a && t < w4) ? i4[a * 4 + t] : 0.0;
-        }
-        Li[(rb + a) * (NB + 1) + c] = v;
-      }
-      __syncthreads();
-    }
+    PROF_MARK(6);
     PROF_MARK(1);
     // ---- Z = A_RK Li^T, thread per row: all loads issued first, 32 independent chains
     for (int i = tid; i < kdp; i += kFT) {
@@ -682,35 +681,23 @@ __global__ void __launch_bounds__(kST, 1)
       mbar_wait(&bar[st], (c_seq / stages) & 1);
       PROF_MARK(1);
       const double* Sb = stage0 + static_cast<size_t>(st) * cap - prow_off(r0);
-      // each warp keeps 4 rows in flight (independent accumulation chains)
-      for (int i0 = r0 + warp; i0 < r1; i0 += 4 * kSW) {
-        double racc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int i = r0 + warp; i < r1; i += kSW) {
+        const double* Si = Sb + prow_off(i);
+        const double wi = wv[i];
+        double racc = 0.0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int i = i0 + q * kSW;
-          if (i >= r1) break;
-          const double* Si = Sb + prow_off(i);
-          const double wi = wv[i];
-#pragma unroll
-          for (int mm = 0; mm < MAXM; ++mm) {
-            const int j = lane + 32 * mm;
-            if (32 * mm > i) break;
-            if (j <= i) {
-              const double sij = Si[j];
-              racc[q] = fma(sij, wv[j], racc[q]);
-              if (j < i) colacc[mm] = fma(sij, wi, colacc[mm]);
-            }
+        for (int mm = 0; mm < MAXM; ++mm) {
+          const int j = lane + 32 * mm;
+          if (32 * mm > i) break;
+          if (j <= i) {
+            const double sij = Si[j];
+            racc = fma(sij, wv[j], racc);
+            if (j < i) colacc[mm] = fma(sij, wi, colacc[mm]);
           }
         }
 #pragma unroll
-        for (int off = 16; off; off >>= 1)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) racc[q] += __shfl_xor_sync(0xffffffffu, racc[q], off);
-        if (lane < 4) {
-          const int i = i0 + lane * kSW;
-          const double v = lane == 0 ? racc[0] : lane == 1 ? racc[1] : lane == 2 ? racc[2] : racc[3];
-          if (i < r1) yrow[i] = v;
-        }
+        for (int off = 16; off; off >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, off);
+        if (lane == 0) yrow[i] = racc;
       }
       __syncthreads();
       PROF_MARK(2);
