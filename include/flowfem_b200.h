@@ -147,6 +147,24 @@ int ffb_pcg_solve(ffb_ctx* ctx, int nc, double tol, int max_iters, int warm, dou
 int ffb_adapt(ffb_ctx* ctx, int nc, double kappa, double eta_thr, double alpha_th,
               double* eta_max);
 
+/* ---- multi-GPU: subdomains sharded over ranks (one process per GPU) ------------------
+ * Rank r of `world` factors and solves subdomains [lo, hi) (contiguous in partition order);
+ * vectors are replicated, so the only exchange per CG iteration is the sum of the
+ * preconditioned residual z over ranks, done by the caller (e.g. an NCCL all-reduce on
+ * the buffer from ffb_device_buffer) between the two stages:
+ *   ffb_pcg_begin; allreduce(z); ffb_pcg_stage(1);
+ *   repeat { ffb_pcg_stage(0); allreduce(z); ffb_pcg_stage(1); }  (status every few)
+ *   ffb_pcg_end.
+ * With world == 1 the same protocol reproduces ffb_pcg_solve. */
+int ffb_shard_range(int n_parts, int rank, int world, int* lo, int* hi);
+int ffb_set_shard(ffb_ctx* ctx, int rank, int world);
+int ffb_pcg_begin(ffb_ctx* ctx, int nc, double tol, int max_iters, int warm, const double* u3);
+int ffb_pcg_stage(ffb_ctx* ctx, int stage);
+int ffb_pcg_status(ffb_ctx* ctx, int* done, int* iters, double* residual, int* err);
+int ffb_pcg_end(ffb_ctx* ctx, double* u3, int* iters, double* residual);
+/* which = 0: the interleaved z vector (nc * W * H doubles) */
+int ffb_device_buffer(ffb_ctx* ctx, int which, void** ptr, long long* n_doubles);
+
 /* run_on_frames (pipeline.hpp:53, pipeline.cpp:38-78) under the converged-pass protocol:
  * n_passes x {solve to tol, error_indicator, update_alpha} + one final solve.
  * u3: planes3 out; alpha: per-triangle out (may be NULL); stats may be NULL. */

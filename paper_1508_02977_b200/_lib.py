@@ -63,6 +63,13 @@ SIGNATURES = {
     "ffb_set_partition": (_i, [_vp, _i, _i, _i]),
     "ffb_pcg_solve": (_i, [_vp, _i, _d, _i, _i, _vp, _vp, _vp]),
     "ffb_adapt": (_i, [_vp, _i, _d, _d, _d, _vp]),
+    "ffb_shard_range": (_i, [_i, _i, _i, _vp, _vp]),
+    "ffb_set_shard": (_i, [_vp, _i, _i]),
+    "ffb_pcg_begin": (_i, [_vp, _i, _d, _i, _i, _vp]),
+    "ffb_pcg_stage": (_i, [_vp, _i]),
+    "ffb_pcg_status": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "ffb_pcg_end": (_i, [_vp, _vp, _vp, _vp]),
+    "ffb_device_buffer": (_i, [_vp, _i, _vp, _vp]),
     "ffb_run_on_frames": (_i, [_vp, _i, _i, _vp, _vp, C.POINTER(RunConfigC), _vp, _vp,
                                C.POINTER(RunStatsC)]),
     "ffb_run_on_frames_dev": (_i, [_vp, _i, _i, _vp, _vp, C.POINTER(RunConfigC), _vp,

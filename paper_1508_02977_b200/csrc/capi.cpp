@@ -104,6 +104,9 @@ struct ffb_ctx {
   int part_px = 0, part_py = 0, part_ov = -1, part_nc = 0;
   Partition decomp;
   int nbf = 32, kd_max = 0, ccl = 1;
+  int shard_rank = 0, shard_world = 1, s_lo = 0, s_hi = 0;  // multi-GPU: own subdomains
+  int stage_nc = 0, stage_max_iters = 0;
+  double stage_tol = 0;
   SolvePlan plan{};
   std::vector<SubInfo> subs;
   DBuf<SubInfo> d_subs;
@@ -242,6 +245,9 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
   }
   c->plan = solve_plan(kd_max, c->ccl);
   c->subs.assign(np, SubInfo{});
+  // subdomains [s_lo, s_hi) are factored and solved here (all of them on a single GPU)
+  c->s_lo = static_cast<int>(static_cast<long long>(c->shard_rank) * np / c->shard_world);
+  c->s_hi = static_cast<int>(static_cast<long long>(c->shard_rank + 1) * np / c->shard_world);
   long long fac_off = 0, vec_off = 0;
   double fd = 0, ad = 0, sn = 0;
   for (int p = 0; p < np; ++p) {
@@ -258,6 +264,7 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
     s.line_sz = packed_line_size(s.kd);
     s.fac_off = fac_off;
     s.vec_off = vec_off;
+    if (p < c->s_lo || p >= c->s_hi) continue;  // another rank's subdomain: no storage here
     fac_off += (s.line_sz * s.L + 31) / 32 * 32;
     vec_off += (n + 31) / 32 * 32;
     fd += static_cast<double>(s.line_sz) * s.L;
@@ -301,7 +308,7 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
   FFB_CUDA(cudaMemcpyAsync(c->d_row.p, row.data(), H * sizeof(AxisMap), cudaMemcpyHostToDevice,
                            c->st));
   c->fac.ensure(fac_off);
-  c->dscratch.ensure(factor_scratch_doubles(np, kd_max));
+  c->dscratch.ensure(factor_scratch_doubles(c->s_hi - c->s_lo, kd_max));
   c->ylocal.ensure(vec_off);
   c->zlocal.ensure(vec_off);
   c->d_bad.ensure(np);
@@ -315,10 +322,11 @@ void ensure_factor(ffb_ctx* c, int nc) {
   if (c->part_nc != nc) ensure_partition(c, c->part_px, c->part_py, c->part_ov, nc);
   if (c->factor_key_a == c->alpha_version && c->factor_key_t == c->terms_version) return;
   ensure_coef(c, nc);
-  const int np = static_cast<int>(c->subs.size());
+  const int np = c->s_hi - c->s_lo;
   FFB_CUDA(cudaMemsetAsync(c->d_bad.p, 0x7f, np * sizeof(int), c->st));
-  line_factor(c->d_subs.p, np, c->ccl, c->nbf, c->kd_max, c->coef.p, c->N, c->W, nc, c->fac.p,
-              c->dscratch.p, static_cast<long long>(c->kd_max) * c->kd_max, c->d_bad.p, c->st);
+  line_factor(c->d_subs.p + c->s_lo, np, c->ccl, c->nbf, c->kd_max, c->coef.p, c->N, c->W, nc,
+              c->fac.p, c->dscratch.p, static_cast<long long>(c->kd_max) * c->kd_max, c->d_bad.p,
+              c->st);
   std::vector<int> bad(np);
   FFB_CUDA(cudaMemcpyAsync(bad.data(), c->d_bad.p, np * sizeof(int), cudaMemcpyDeviceToHost,
                            c->st));
@@ -326,7 +334,7 @@ void ensure_factor(ffb_ctx* c, int nc) {
   for (int p = 0; p < np; ++p)
     if (bad[p] != 0x7f7f7f7f)
       fail("linsolve.cholesky: breakdown at pivot " + std::to_string(bad[p]) + " of subdomain " +
-           std::to_string(p) + ": matrix is not positive definite");
+           std::to_string(p + c->s_lo) + ": matrix is not positive definite");
   c->factor_key_a = c->alpha_version;
   c->factor_key_t = c->terms_version;
 }
@@ -340,8 +348,8 @@ void launch_asm(ffb_ctx* c, int nc, const double* rvec, const int* flags) {
     FFB_CUDA(cudaEventCreate(&ev->b));
     FFB_CUDA(cudaEventRecord(ev->a, c->st));
   }
-  line_solve(c->d_subs.p, static_cast<int>(c->subs.size()), c->plan, c->fac.p, c->coef.p, c->N,
-             rvec, c->ylocal.p, c->zlocal.p, c->W, nc, flags, c->st);
+  line_solve(c->d_subs.p + c->s_lo, c->s_hi - c->s_lo, c->plan, c->fac.p, c->coef.p, c->N, rvec,
+             c->ylocal.p, c->zlocal.p, c->W, nc, flags, c->st);
   if (ev) FFB_CUDA(cudaEventRecord(ev->b, c->st));
 }
 
@@ -390,8 +398,9 @@ PcgResult pcg(ffb_ctx* c, int nc, double tol, int max_iters, bool warm) {
   const int px = c->part_px;
   pcg_init(nc, c->coef.p, c->b.p, x, r, c->W, c->H, ctl, part, c->st);
   launch_asm(c, nc, r, flags);
+  if (c->shard_world != 1) fail("schwarz.schwarz_solve: sharded context: use the staged solve");
   pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, px, c->zlocal.p, r, z, c->W, c->H, ctl,
-              part, c->st);
+              part, 0, c->s_hi, 0, c->st);
   const int chunk = 8;
   for (;;) {
     for (int it = 0; it < chunk; ++it) {
@@ -399,7 +408,7 @@ PcgResult pcg(ffb_ctx* c, int nc, double tol, int max_iters, bool warm) {
       pcg_update(nc, x, r, P0, P1, q, nvec, max_iters, ctl, part, c->st);
       launch_asm(c, nc, r, flags);
       pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, px, c->zlocal.p, r, z, c->W, c->H,
-                  ctl, part, c->st);
+                  ctl, part, 0, c->s_hi, 0, c->st);
     }
     FFB_CUDA(cudaMemcpyAsync(c->h_ctl, ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, c->st));
     sync(c);
@@ -832,6 +841,145 @@ int ffb_pcg_solve(ffb_ctx* c, int nc, double tol, int max_iters, int warm, doubl
     sync(c);
     if (iters) *iters = r.iters;
     if (residual) *residual = r.res;
+  });
+}
+
+// ---- multi-GPU staged solve -----------------------------------------------------------
+int ffb_shard_range(int n_parts, int rank, int world, int* lo, int* hi) {
+  return guard([&] {
+    if (world < 1 || rank < 0 || rank >= world) fail("schwarz: invalid shard rank/world");
+    *lo = static_cast<int>(static_cast<long long>(rank) * n_parts / world);
+    *hi = static_cast<int>(static_cast<long long>(rank + 1) * n_parts / world);
+  });
+}
+
+int ffb_set_shard(ffb_ctx* c, int rank, int world) {
+  return guard([&] {
+    check_ctx(c);
+    if (world < 1 || rank < 0 || rank >= world) fail("schwarz: invalid shard rank/world");
+    c->shard_rank = rank;
+    c->shard_world = world;
+    c->have_part = false;
+    c->factor_key_a = c->factor_key_t = -1;
+  });
+}
+
+int ffb_pcg_begin(ffb_ctx* c, int nc, double tol, int max_iters, int warm, const double* u3) {
+  return guard([&] {
+    check_ctx(c);
+    if (nc != 2 && nc != 3) fail("assembly.assemble: components must be 2 or 3");
+    if (!c->alpha.p) fail("assembly.assemble: no regularization set");
+    if (!c->have_part) fail("schwarz.schwarz_solve: no partition set");
+    ensure_coef(c, nc);
+    ensure_rhs(c, nc);
+    ensure_factor(c, nc);
+    const size_t N = c->N;
+    const long long nvec = static_cast<long long>(N) * nc;
+    double* x = c->x.ensure(3 * N);
+    double* r = c->r.ensure(3 * N);
+    double* z = c->z.ensure(3 * N);
+    c->p0.ensure(3 * N);
+    c->p1.ensure(3 * N);
+    c->q.ensure(3 * N);
+    double* part = c->part.ensure(4 * kRedBlocks);
+    PcgCtl* ctl = c->ctl.ensure(1);
+    if (!c->h_ctl) FFB_CUDA(cudaMallocHost(&c->h_ctl, sizeof(PcgCtl)));
+    if (warm && u3) {
+      double* w = c->work.ensure(3 * N);
+      upload(w, u3, 3 * N, c->st);
+      planes_to_inter(w, x, static_cast<long long>(N), nc, c->st);
+    } else if (!warm) {
+      FFB_CUDA(cudaMemsetAsync(x, 0, nvec * sizeof(double), c->st));
+    }
+    c->stage_max_iters =
+        max_iters > 0 ? max_iters : static_cast<int>(std::min<long long>(10 * nvec, 1 << 30));
+    c->stage_nc = nc;
+    c->stage_tol = tol;
+    std::memset(c->h_ctl, 0, sizeof(PcgCtl));
+    c->h_ctl->tol = tol;
+    FFB_CUDA(cudaMemcpyAsync(ctl, c->h_ctl, sizeof(PcgCtl), cudaMemcpyHostToDevice, c->st));
+    pcg_init(nc, c->coef.p, c->b.p, x, r, c->W, c->H, ctl, part, c->st);
+    launch_asm(c, nc, r, &ctl->done);
+    pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, c->part_px, c->zlocal.p, r, z, c->W, c->H,
+                ctl, part, c->s_lo, c->s_hi, 1, c->st);
+  });
+}
+
+int ffb_pcg_stage(ffb_ctx* c, int stage) {
+  return guard([&] {
+    check_ctx(c);
+    if (!c->stage_nc) fail("linsolve.cg: no staged solve in progress");
+    const int nc = c->stage_nc;
+    const long long nvec = static_cast<long long>(c->N) * nc;
+    PcgCtl* ctl = c->ctl.p;
+    double* part = c->part.p;
+    if (stage == 0) {  // A: p, q = A p, x/r update, own subdomain solves, partial z
+      pcg_spmv_p(nc, c->coef.p, c->z.p, c->p0.p, c->p1.p, c->q.p, c->W, c->H, ctl, part, c->st);
+      pcg_update(nc, c->x.p, c->r.p, c->p0.p, c->p1.p, c->q.p, nvec, c->stage_max_iters, ctl, part,
+                 c->st);
+      launch_asm(c, nc, c->r.p, &ctl->done);
+      pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, c->part_px, c->zlocal.p, c->r.p, c->z.p,
+                  c->W, c->H, ctl, part, c->s_lo, c->s_hi, 1, c->st);
+    } else if (stage == 1) {  // B: r.z of the all-reduced z
+      pcg_rz(c->r.p, c->z.p, nvec, ctl, part, c->st);
+    } else {
+      fail("linsolve.cg: unknown stage");
+    }
+  });
+}
+
+int ffb_pcg_status(ffb_ctx* c, int* done, int* iters, double* residual, int* err) {
+  return guard([&] {
+    check_ctx(c);
+    if (!c->stage_nc) fail("linsolve.cg: no staged solve in progress");
+    FFB_CUDA(cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(PcgCtl), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    if (c->time_asm) harvest_asm_events(c);
+    if (done) *done = c->h_ctl->done;
+    if (iters) *iters = c->h_ctl->iters;
+    if (residual) *residual = c->h_ctl->res;
+    if (err) *err = c->h_ctl->err;
+  });
+}
+
+int ffb_pcg_end(ffb_ctx* c, double* u3, int* iters, double* residual) {
+  return guard([&] {
+    check_ctx(c);
+    if (!c->stage_nc) fail("linsolve.cg: no staged solve in progress");
+    const int nc = c->stage_nc;
+    c->stage_nc = 0;
+    FFB_CUDA(cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(PcgCtl), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    const PcgCtl& h = *c->h_ctl;
+    if (h.err)
+      fail("linsolve.cg: indefinite matrix detected at iteration " + std::to_string(h.err_it));
+    if (h.zero_rhs)
+      FFB_CUDA(cudaMemsetAsync(c->x.p, 0, static_cast<long long>(c->N) * nc * sizeof(double), c->st));
+    else if (!(h.res <= c->stage_tol)) {
+      char buf[160];
+      std::snprintf(buf, sizeof buf,
+                    "linsolve.cg: no convergence after %d iterations, relative residual %f",
+                    h.iters, h.res);
+      fail(buf);
+    }
+    if (u3) {
+      double* w = c->work.ensure(3 * c->N);
+      inter_to_planes(c->x.p, w, static_cast<long long>(c->N), nc, c->st);
+      download(u3, w, 3 * c->N, c->st);
+      sync(c);
+    }
+    if (iters) *iters = h.zero_rhs ? 0 : h.iters;
+    if (residual) *residual = h.zero_rhs ? 0.0 : h.res;
+  });
+}
+
+int ffb_device_buffer(ffb_ctx* c, int which, void** ptr, long long* n_doubles) {
+  return guard([&] {
+    check_ctx(c);
+    if (which != 0) fail("ffb: unknown device buffer");
+    if (!c->z.p) fail("ffb: buffer not allocated yet");
+    *ptr = c->z.p;
+    *n_doubles = static_cast<long long>(c->N) * (c->stage_nc ? c->stage_nc : 3);
   });
 }
 

@@ -113,7 +113,9 @@ void pcg_init(int nc, const double* coef, const double* b, const double* x, doub
               int H, PcgCtl* ctl, double* part, cudaStream_t st);
 void pcg_combine(int nc, const SubInfo* subs, const AxisMap* colmap, const AxisMap* rowmap,
                  int px, const double* zlocal, const double* r, double* z, int W, int H,
-                 PcgCtl* ctl, double* part, cudaStream_t st);
+                 PcgCtl* ctl, double* part, int s_lo, int s_hi, int partial, cudaStream_t st);
+void pcg_rz(const double* r, const double* z, long long nvec, PcgCtl* ctl, double* part,
+            cudaStream_t st);
 void pcg_spmv_p(int nc, const double* coef, const double* z, double* P0, double* P1, double* q,
                 int W, int H, PcgCtl* ctl, double* part, cudaStream_t st);
 void pcg_update(int nc, double* x, double* r, const double* P0, const double* P1,

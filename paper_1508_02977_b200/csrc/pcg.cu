@@ -157,6 +157,8 @@ __global__ void __launch_bounds__(T) k_init(const double* __restrict__ coef,
 }
 
 // combine: z = sum_i R_i^T z_i (ascending subdomain id), r.z; k++
+// With a shard [s_lo, s_hi) (multi-GPU) only this rank's subdomains contribute and the
+// result is a partial z that the host all-reduces before k_rz forms r.z.
 template <int NC>
 __global__ void __launch_bounds__(T) k_combine(const SubInfo* __restrict__ subs,
                                                const AxisMap* __restrict__ colmap,
@@ -164,7 +166,8 @@ __global__ void __launch_bounds__(T) k_combine(const SubInfo* __restrict__ subs,
                                                const double* __restrict__ zlocal,
                                                const double* __restrict__ r,
                                                double* __restrict__ z, int W, int H,
-                                               PcgCtl* ctl, double* part) {
+                                               PcgCtl* ctl, double* part, int s_lo, int s_hi,
+                                               int partial) {
   if (ctl->done | ctl->err) return;
   __shared__ double sm[32];
   const size_t n = static_cast<size_t>(W) * H;
@@ -184,7 +187,9 @@ __global__ void __launch_bounds__(T) k_combine(const SubInfo* __restrict__ subs,
         const int i = ii ? cm.p1 : cm.p0;
         if (i < 0) continue;
         const int lx = ii ? cm.l1 : cm.l0;
-        const SubInfo& s = subs[j * px + i];
+        const int sid = j * px + i;
+        if (sid < s_lo || sid >= s_hi) continue;
+        const SubInfo& s = subs[sid];
         const long long vl = s.xfast ? static_cast<long long>(ly) * s.fw + lx
                                      : static_cast<long long>(lx) * s.fh + ly;
         const double* zl = zlocal + s.vec_off + vl * NC;
@@ -198,6 +203,34 @@ __global__ void __launch_bounds__(T) k_combine(const SubInfo* __restrict__ subs,
       rz += r[v * NC + c] * acc[c];
     }
   }
+  if (partial) return;
+  rz = block_sum(rz, sm);
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = rz;
+    last = arrive_last(&ctl->counter[1]);
+  }
+  __syncthreads();
+  if (!last) return;
+  const double RZ = final_sum(part, gridDim.x, sm);
+  if (threadIdx.x == 0) {
+    ctl->counter[1] = 0;
+    ctl->rz_old = ctl->rz;
+    ctl->rz = RZ;
+    ctl->k += 1;
+  }
+}
+
+// r.z of the all-reduced z (multi-GPU stage B); k++
+__global__ void __launch_bounds__(T) k_rz(const double* __restrict__ r,
+                                          const double* __restrict__ z, long long nvec,
+                                          PcgCtl* ctl, double* part) {
+  if (ctl->done | ctl->err) return;
+  __shared__ double sm[32];
+  double rz = 0.0;
+  for (long long i = static_cast<long long>(blockIdx.x) * T + threadIdx.x; i < nvec;
+       i += static_cast<long long>(gridDim.x) * T)
+    rz += r[i] * z[i];
   rz = block_sum(rz, sm);
   __shared__ bool last;
   if (threadIdx.x == 0) {
@@ -326,11 +359,19 @@ void pcg_init(int nc, const double* coef, const double* b, const double* x, doub
 
 void pcg_combine(int nc, const SubInfo* subs, const AxisMap* colmap, const AxisMap* rowmap,
                  int px, const double* zlocal, const double* r, double* z, int W, int H,
-                 PcgCtl* ctl, double* part, cudaStream_t st) {
+                 PcgCtl* ctl, double* part, int s_lo, int s_hi, int partial, cudaStream_t st) {
   if (nc == 3)
-    k_combine<3><<<kRedBlocks, T, 0, st>>>(subs, colmap, rowmap, px, zlocal, r, z, W, H, ctl, part);
+    k_combine<3><<<kRedBlocks, T, 0, st>>>(subs, colmap, rowmap, px, zlocal, r, z, W, H, ctl, part,
+                                           s_lo, s_hi, partial);
   else
-    k_combine<2><<<kRedBlocks, T, 0, st>>>(subs, colmap, rowmap, px, zlocal, r, z, W, H, ctl, part);
+    k_combine<2><<<kRedBlocks, T, 0, st>>>(subs, colmap, rowmap, px, zlocal, r, z, W, H, ctl, part,
+                                           s_lo, s_hi, partial);
+  FFB_LAUNCHED();
+}
+
+void pcg_rz(const double* r, const double* z, long long nvec, PcgCtl* ctl, double* part,
+            cudaStream_t st) {
+  k_rz<<<kRedBlocks, T, 0, st>>>(r, z, nvec, ctl, part);
   FFB_LAUNCHED();
 }
 
