@@ -194,7 +194,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
     ctx = ff.Context(local)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # the launching stream: library kernels + timing events
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     rc = run_config_for(cfg, ff)
     H, W = cfg.H, cfg.W

@@ -82,9 +82,10 @@ long long ffb_kernel_launches(void);
 /* ---- context (one GPU) ------------------------------------------------------------ */
 int ffb_create(ffb_ctx** ctx, int device);
 int ffb_destroy(ffb_ctx* ctx);
-/* Launch on the caller's CUDA stream (cudaStream_t passed as void*); NULL restores the
- * context's own stream. Lets a host framework bracket the solve with its own events. */
-int ffb_set_stream(ffb_ctx* ctx, void* stream);
+/* Launch on the caller's CUDA stream (cudaStream_t passed as void*; 0 is the legacy
+ * default stream) when own == 0, or on the context's own stream when own != 0. Lets a host
+ * framework order the solve with its own work and bracket it with its own events. */
+int ffb_set_stream(ffb_ctx* ctx, void* stream, int own);
 
 /* ---- imaging: include/flowfem/imaging.hpp ----------------------------------------- */
 /* gaussian_smooth (imaging.hpp:42-44, imaging.cpp:33-63) */
@@ -162,7 +163,7 @@ int ffb_pcg_begin(ffb_ctx* ctx, int nc, double tol, int max_iters, int warm, con
 int ffb_pcg_stage(ffb_ctx* ctx, int stage);
 int ffb_pcg_status(ffb_ctx* ctx, int* done, int* iters, double* residual, int* err);
 int ffb_pcg_end(ffb_ctx* ctx, double* u3, int* iters, double* residual);
-/* which = 0: the interleaved z vector (nc * W * H doubles) */
+/* interleaved CG vectors (nc * W * H doubles): 0 z, 1 r, 2 x, 3/4 the two p buffers */
 int ffb_device_buffer(ffb_ctx* ctx, int which, void** ptr, long long* n_doubles);
 
 /* run_on_frames (pipeline.hpp:53, pipeline.cpp:38-78) under the converged-pass protocol:

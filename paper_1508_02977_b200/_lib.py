@@ -44,7 +44,7 @@ SIGNATURES = {
     "ffb_kernel_launches": (C.c_longlong, []),
     "ffb_create": (_i, [C.POINTER(_vp), _i]),
     "ffb_destroy": (_i, [_vp]),
-    "ffb_set_stream": (_i, [_vp, _vp]),
+    "ffb_set_stream": (_i, [_vp, _vp, _i]),
     "ffb_gaussian_smooth": (_i, [_vp, _i, _i, _vp, _d, _vp]),
     "ffb_compute_derivatives": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ffb_build_data_terms": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _d, _vp]),

@@ -576,11 +576,11 @@ int ffb_debug_prof(unsigned long long* out64, int reset) {
   return guard([&] { debug_prof(out64, reset != 0); });
 }
 
-int ffb_set_stream(ffb_ctx* c, void* stream) {
+int ffb_set_stream(ffb_ctx* c, void* stream, int own) {
   return guard([&] {
     check_ctx(c);
     FFB_CUDA(cudaStreamSynchronize(c->st));
-    c->st = stream ? static_cast<cudaStream_t>(stream) : c->own_st;
+    c->st = own ? c->own_st : static_cast<cudaStream_t>(stream);
   });
 }
 
@@ -976,9 +976,10 @@ int ffb_pcg_end(ffb_ctx* c, double* u3, int* iters, double* residual) {
 int ffb_device_buffer(ffb_ctx* c, int which, void** ptr, long long* n_doubles) {
   return guard([&] {
     check_ctx(c);
-    if (which != 0) fail("ffb: unknown device buffer");
-    if (!c->z.p) fail("ffb: buffer not allocated yet");
-    *ptr = c->z.p;
+    double* bufs[5] = {c->z.p, c->r.p, c->x.p, c->p0.p, c->p1.p};
+    if (which < 0 || which > 4) fail("ffb: unknown device buffer");
+    if (!bufs[which]) fail("ffb: buffer not allocated yet");
+    *ptr = bufs[which];
     *n_doubles = static_cast<long long>(c->N) * (c->stage_nc ? c->stage_nc : 3);
   });
 }

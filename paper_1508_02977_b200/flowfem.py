@@ -57,8 +57,11 @@ class Context:
         return self._h
 
     def set_stream(self, stream_handle: int | None):
-        """Launch on an external CUDA stream (e.g. torch.cuda.current_stream().cuda_stream)."""
-        _check(self.lib.ffb_set_stream(self._h, C.c_void_p(stream_handle or 0)))
+        """Launch on an external CUDA stream (e.g. torch.cuda.current_stream().cuda_stream,
+        where 0 is the legacy default stream); None restores the context's own stream."""
+        own = stream_handle is None
+        _check(self.lib.ffb_set_stream(self._h, C.c_void_p(0 if own else stream_handle),
+                                       int(own)))
 
     def close(self):
         if getattr(self, "_h", None):

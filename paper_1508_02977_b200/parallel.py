@@ -78,11 +78,12 @@ class DeviceBackend:
         _check(self.lib.ffb_pcg_end(self.ctx.handle, _p(u3), C.byref(it), C.byref(res)))
         return u3, it.value, res.value
 
-    def z_buffer(self):
-        """torch CUDA view of the device z vector (zero copy) for the collective."""
+    def z_buffer(self, which: int = 0):
+        """torch CUDA view (zero copy) of the device z vector, the operand of the collective
+        (which = 1..4: r, x and the two p buffers, for diagnostics)."""
         import torch
         ptr, n = C.c_void_p(), C.c_longlong()
-        _check(self.lib.ffb_device_buffer(self.ctx.handle, 0, C.byref(ptr), C.byref(n)))
+        _check(self.lib.ffb_device_buffer(self.ctx.handle, which, C.byref(ptr), C.byref(n)))
 
         class _Arr:  # __cuda_array_interface__ shim
             __cuda_array_interface__ = {"shape": (n.value,), "typestr": "<f8",
