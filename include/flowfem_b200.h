@@ -148,6 +148,18 @@ int ffb_pcg_solve(ffb_ctx* ctx, int nc, double tol, int max_iters, int warm, dou
 int ffb_adapt(ffb_ctx* ctx, int nc, double kappa, double eta_thr, double alpha_th,
               double* eta_max);
 
+/* schwarz_solve (schwarz.hpp:79-81, schwarz.cpp:162-319): the reference's own synchronous
+ * restricted-additive-Schwarz loop on the resident terms / reg / partition — per iteration
+ * every subdomain solves with Dirichlet traces from the previous composed field (one step of
+ * iterative refinement when refine != 0, as the reference's Cholesky path), cores are
+ * composed, increments[it] = max-norm change; when adapt != 0 alpha is updated after each of
+ * the first n_adapt iterations (eta_max[k] recorded) and the factors are refreshed. u3:
+ * planes3 out; increments: n_iters; eta_max: min(n_adapt, n_iters). Resident alpha is
+ * updated in place (RegField& reg). */
+int ffb_schwarz_solve(ffb_ctx* ctx, int n_iters, int nc, int adapt, int n_adapt, double kappa,
+                      double eta_thr, double alpha_th, int refine, double* u3,
+                      double* increments, double* eta_max);
+
 /* ---- multi-GPU: subdomains sharded over ranks (one process per GPU) ------------------
  * Rank r of `world` factors and solves subdomains [lo, hi) (contiguous in partition order);
  * vectors are replicated, so the only exchange per CG iteration is the sum of the

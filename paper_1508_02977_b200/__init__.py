@@ -7,10 +7,11 @@ reference's ``flowfem::`` API on top of it.
 """
 from .flowfem import (AdaptConfig, Context, DataTerms, DerivativeField, FlowfemError,
                       FlowState, IndicatorField, Partition, RegField, RunConfig, RunResult,
-                      SchwarzSolver, SplitChoice, assemble_apply, assign_workers,
+                      SchwarzOptions, SchwarzSolver, SchwarzStats, SplitChoice, assemble_apply, assign_workers,
                       build_data_terms, build_partition, choose_split, compute_derivatives,
                       default_context, enumerate_splits, error_indicator, frames_to_terms,
                       gaussian_smooth, kernel_launches, run_on_frames, run_on_frames_device,
+                      schwarz_solve,
                       uniform_reg, update_alpha)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

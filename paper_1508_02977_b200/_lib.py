@@ -63,6 +63,7 @@ SIGNATURES = {
     "ffb_set_partition": (_i, [_vp, _i, _i, _i]),
     "ffb_pcg_solve": (_i, [_vp, _i, _d, _i, _i, _vp, _vp, _vp]),
     "ffb_adapt": (_i, [_vp, _i, _d, _d, _d, _vp]),
+    "ffb_schwarz_solve": (_i, [_vp, _i, _i, _i, _i, _d, _d, _d, _i, _vp, _vp, _vp]),
     "ffb_shard_range": (_i, [_i, _i, _i, _vp, _vp]),
     "ffb_set_shard": (_i, [_vp, _i, _i]),
     "ffb_pcg_begin": (_i, [_vp, _i, _d, _i, _i, _vp]),

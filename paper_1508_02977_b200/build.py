@@ -29,6 +29,7 @@ CU = {
     "adapt.cu": ["--fmad=false"],
     "band.cu": ["-Xptxas", "-v"] if os.environ.get("FFB_PTXAS_V") else [],
     "pcg.cu": [],
+    "ras.cu": ["--fmad=false"],
 }
 CPP = ["capi.cpp", "partition.cpp"]
 HEADERS = ["ffb_internal.cuh", "partition.hpp"]

@@ -571,7 +571,8 @@ __global__ void __launch_bounds__(kST, 1)
     k_line_solve(const SubInfo* __restrict__ subs, const double* __restrict__ fac,
                  const double* __restrict__ coef, size_t N, const double* __restrict__ r,
                  double* __restrict__ ylocal, double* __restrict__ zlocal, int W, int nc,
-                 int stages, int cap, int kd_max, int phase, const int* __restrict__ flags) {
+                 int stages, int cap, int kd_max, int phase, const int* __restrict__ flags,
+                 const double* __restrict__ rlocal) {
   if (flags && (flags[0] | flags[1])) return;  // PCG converged or failed (grid-uniform)
   const int C = static_cast<int>(cl_size()), crank = static_cast<int>(cl_rank());
   const int cid = blockIdx.x / C;  // (subdomain, chain)
@@ -592,6 +593,7 @@ __global__ void __launch_bounds__(kST, 1)
   double* red = xprev + kd_max;                                  // 8 x kd_max reduce slots
   double* yl = ylocal + s.vec_off;
   double* zl = zlocal + s.vec_off;
+  const double* rl = rlocal ? rlocal + s.vec_off : nullptr;  // per-subdomain rhs (RAS mode)
   if (nl == 0) return;  // cluster-uniform
 
   if (tid == 0) {
@@ -636,10 +638,10 @@ __global__ void __launch_bounds__(kST, 1)
       const int j = tid + kST * q;
       if (j < kd) {
         if (phase == 0) {
-          pf_r[q] = r[gidx(s, l, j, W, nc)];
+          pf_r[q] = rl ? rl[static_cast<long long>(l) * kd + j] : r[gidx(s, l, j, W, nc)];
           if (t > 0) pf_b[q] = bcoef(s, coef, N, W, nc, chain == 0 ? l : l + 1, j);
         } else if (t == 0) {  // middle line: both neighbours from the forward sweep
-          double w = r[gidx(s, l, j, W, nc)];
+          double w = rl ? rl[static_cast<long long>(l) * kd + j] : r[gidx(s, l, j, W, nc)];
           if (m > 0) w -= bcoef(s, coef, N, W, nc, m, j) * yl[static_cast<long long>(m - 1) * kd + j];
           if (m < L - 1)
             w -= bcoef(s, coef, N, W, nc, m + 1, j) * yl[static_cast<long long>(m + 1) * kd + j];
@@ -857,27 +859,27 @@ template <int M>
 static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
                            const double* fac, const double* coef, size_t N, const double* r,
                            double* ylocal, double* zlocal, int W, int nc, const int* flags,
-                           cudaStream_t st) {
+                           const double* rlocal, cudaStream_t st) {
   for (int phase = 0; phase <= 1; ++phase) {
     launch_cluster(k_line_solve<M>, 2 * nsub * pl.C, kST, pl.smem, pl.C, st, d_subs, fac, coef, N,
-                   r, ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, phase, flags);
+                   r, ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, phase, flags, rlocal);
     FFB_LAUNCHED();
   }
 }
 
 void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,
                 const double* coef, size_t N, const double* r, double* ylocal, double* zlocal,
-                int W, int nc, const int* flags, cudaStream_t st) {
+                int W, int nc, const int* flags, cudaStream_t st, const double* rlocal) {
   if (pl.maxm <= 4)
-    launch_solve_m<4>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, st);
+    launch_solve_m<4>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st);
   else if (pl.maxm <= 8)
-    launch_solve_m<8>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, st);
+    launch_solve_m<8>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st);
   else if (pl.maxm <= 14)
-    launch_solve_m<14>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, st);
+    launch_solve_m<14>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st);
   else if (pl.maxm <= 20)
-    launch_solve_m<20>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, st);
+    launch_solve_m<20>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st);
   else if (pl.maxm <= 26)
-    launch_solve_m<26>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, st);
+    launch_solve_m<26>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st);
   else
     fail("linsolve.cholesky: subdomain line too wide (kd > 832)");
 }

@@ -111,7 +111,8 @@ struct ffb_ctx {
   std::vector<SubInfo> subs;
   DBuf<SubInfo> d_subs;
   DBuf<AxisMap> d_col, d_row;
-  DBuf<double> fac, dscratch, ylocal, zlocal;
+  DBuf<double> fac, dscratch, ylocal, zlocal, rlocal, xlocal, G0, G1, incs;
+  DBuf<int> own_col, own_row;
   DBuf<int> d_bad;
   double factor_doubles = 0, apply_doubles = 0, sum_n = 0;
   // asm kernel timing
@@ -981,6 +982,88 @@ int ffb_device_buffer(ffb_ctx* c, int which, void** ptr, long long* n_doubles) {
     if (!bufs[which]) fail("ffb: buffer not allocated yet");
     *ptr = bufs[which];
     *n_doubles = static_cast<long long>(c->N) * (c->stage_nc ? c->stage_nc : 3);
+  });
+}
+
+// ---- the reference's literal Schwarz loop (schwarz.cpp:162-319) ----------------------
+int ffb_schwarz_solve(ffb_ctx* c, int n_iters, int nc, int adapt, int n_adapt, double kappa,
+                      double eta_thr, double alpha_th, int refine, double* u3,
+                      double* increments, double* eta_max) {
+  return guard([&] {
+    check_ctx(c);
+    if (nc != 2 && nc != 3) fail("assembly.assemble: components must be 2 or 3");
+    if (!c->alpha.p) fail("assembly.assemble: no regularization set");
+    if (!c->have_part) fail("schwarz.schwarz_solve: no partition set");
+    if (c->shard_world != 1) fail("schwarz.schwarz_solve: sharded context");
+    if (n_iters < 0) fail("schwarz.schwarz_solve: n_iters must be >= 0");
+    if (c->part_nc != nc) ensure_partition(c, c->part_px, c->part_py, c->part_ov, nc);
+    ensure_coef(c, nc);
+    ensure_rhs(c, nc);
+    const size_t N = c->N;
+    const int np = static_cast<int>(c->subs.size());
+    const long long vec_len = c->ylocal.n;
+    double* rl = c->rlocal.ensure(vec_len);
+    double* xl = c->xlocal.ensure(vec_len);
+    double* G = c->G0.ensure(3 * N);
+    double* Gn = c->G1.ensure(3 * N);
+    double* inc = c->incs.ensure(std::max(n_iters, 1));
+    double* em = c->eta_hist.ensure(std::max(n_iters, FFB_MAX_SOLVES));
+    double* eta = c->eta.ensure(c->ntri);
+    double* blockmax = c->part.ensure(4 * kRedBlocks);
+    unsigned* counter = c->counter.ensure(1);
+    FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
+    FFB_CUDA(cudaMemsetAsync(G, 0, 3 * N * sizeof(double), c->st));  // G = 0 (schwarz.cpp:190)
+    // owner (core) of every column / row (schwarz.cpp:87-91)
+    {
+      const Partition& P = c->decomp;
+      std::vector<int> oc(c->W), orow(c->H);
+      for (int x = 0; x < c->W; ++x)
+        oc[x] = int(std::upper_bound(P.xs.begin(), P.xs.end(), x) - P.xs.begin()) - 1;
+      for (int y = 0; y < c->H; ++y)
+        orow[y] = int(std::upper_bound(P.ys.begin(), P.ys.end(), y) - P.ys.begin()) - 1;
+      FFB_CUDA(cudaMemcpyAsync(c->own_col.ensure(c->W), oc.data(), c->W * sizeof(int),
+                               cudaMemcpyHostToDevice, c->st));
+      FFB_CUDA(cudaMemcpyAsync(c->own_row.ensure(c->H), orow.data(), c->H * sizeof(int),
+                               cudaMemcpyHostToDevice, c->st));
+      sync(c);
+    }
+    int n_upd = 0;
+    for (int iter = 0; iter < n_iters; ++iter) {
+      ensure_coef(c, nc);
+      ensure_factor(c, nc);  // refactors iff alpha changed (schwarz.cpp:238-241)
+      ras_rhs(c->d_subs.p, np, c->coef.p, c->b.p, G, N, c->W, c->H, nc, rl, c->st);
+      line_solve(c->d_subs.p, np, c->plan, c->fac.p, c->coef.p, N, nullptr, c->ylocal.p,
+                 c->zlocal.p, c->W, nc, nullptr, c->st, rl);
+      const double* dl = nullptr;
+      if (refine) {  // x += A^-1 (rhs - A x)   (schwarz.cpp:242-247)
+        vec_copy(xl, c->zlocal.p, vec_len, c->st);
+        ras_residual(c->d_subs.p, np, c->coef.p, N, c->W, nc, rl, xl, rl, c->st);
+        line_solve(c->d_subs.p, np, c->plan, c->fac.p, c->coef.p, N, nullptr, c->ylocal.p,
+                   c->zlocal.p, c->W, nc, nullptr, c->st, rl);
+        dl = c->zlocal.p;
+      } else {
+        vec_copy(xl, c->zlocal.p, vec_len, c->st);
+      }
+      ras_compose(c->own_col.p, c->own_row.p, c->d_subs.p, c->part_px, xl, dl, G, Gn, c->W, c->H,
+                  nc, blockmax, inc + iter, counter, c->st);
+      std::swap(G, Gn);
+      if (adapt && iter < n_adapt) {  // schwarz.cpp:303-311
+        double* u = c->work.ensure(3 * N);
+        inter_to_planes(G, u, static_cast<long long>(N), nc, c->st);
+        error_indicator(c->t10.p, c->alpha.p, c->lambda.p, u, c->W, c->H, nc, eta, em + n_upd,
+                        blockmax, counter, c->st);
+        update_alpha(c->alpha.p, c->alpha.p, eta, em + n_upd, c->ntri, kappa, eta_thr, alpha_th,
+                     c->st);
+        c->alpha_version++;
+        ++n_upd;
+      }
+    }
+    double* u = c->work.ensure(3 * N);
+    inter_to_planes(G, u, static_cast<long long>(N), nc, c->st);
+    if (u3) download(u3, u, 3 * N, c->st);
+    if (increments && n_iters > 0) download(increments, inc, n_iters, c->st);
+    if (eta_max && n_upd > 0) download(eta_max, em, n_upd, c->st);
+    sync(c);
   });
 }
 

@@ -94,7 +94,18 @@ struct SolvePlan {
 SolvePlan solve_plan(int kd_max, int C);
 void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,
                 const double* coef, size_t N, const double* r, double* ylocal, double* zlocal,
-                int W, int nc, const int* flags, cudaStream_t st);
+                int W, int nc, const int* flags, cudaStream_t st,
+                const double* rlocal = nullptr);
+
+// ---- literal Schwarz iteration (ras.cu) ---------------------------------------------------
+void ras_rhs(const SubInfo* d_subs, int nsub, const double* coef, const double* b,
+             const double* G, size_t N, int W, int H, int nc, double* rl, cudaStream_t st);
+void ras_residual(const SubInfo* d_subs, int nsub, const double* coef, size_t N, int W, int nc,
+                  const double* rl, const double* xl, double* res, cudaStream_t st);
+void ras_compose(const int* own_col, const int* own_row, const SubInfo* d_subs, int px,
+                 const double* xl, const double* dl, const double* G, double* Gnew, int W, int H,
+                 int nc, double* blockmax, double* inc_out, unsigned* counter, cudaStream_t st);
+void vec_copy(double* dst, const double* src, long long n, cudaStream_t st);
 
 // ---- PCG control block (solver.cu) ----------------------------------------------------
 struct PcgCtl {

@@ -424,6 +424,49 @@ class SchwarzSolver:
         return em.value
 
 
+@dataclass
+class SchwarzOptions:
+    """schwarz.hpp:59-66 (workers only affects CPU threading in the reference and is accepted
+    for signature compatibility)."""
+    n_iters: int = 10
+    workers: int = 1
+    components: int = 3
+    adapt: AdaptConfig = field(default_factory=AdaptConfig)
+    refine: bool = True
+
+
+@dataclass
+class SchwarzStats:
+    increments: List[float]
+    eta_max: List[float]
+
+
+def schwarz_solve(terms: DataTerms, reg: RegField, parts_x: int, parts_y: int, overlap: int,
+                  opt: SchwarzOptions, ctx: Context | None = None):
+    """schwarz_solve (schwarz.hpp:79-81): the reference's synchronous RAS loop on the device.
+
+    ``reg`` is updated in place when adapting (RegField& reg). Returns (FlowState, stats)."""
+    ctx = ctx or default_context()
+    t = terms.planes
+    _, H, W = t.shape
+    lib = ctx.lib
+    _check(lib.ffb_set_terms(ctx.handle, W, H, _p(t)))
+    reg.alpha = _f64(reg.alpha)
+    _check(lib.ffb_set_reg(ctx.handle, _p(reg.alpha), _p(_f64(reg.lambda_))))
+    _check(lib.ffb_set_partition(ctx.handle, parts_x, parts_y, overlap))
+    u3 = np.zeros((3, H, W))
+    inc = np.zeros(max(opt.n_iters, 1))
+    a = opt.adapt
+    n_upd = min(a.n_adapt, opt.n_iters) if a.enabled else 0
+    em = np.zeros(max(n_upd, 1))
+    _check(lib.ffb_schwarz_solve(ctx.handle, opt.n_iters, opt.components, int(a.enabled),
+                                 a.n_adapt, float(a.kappa), float(a.eta_threshold),
+                                 float(a.alpha_th), int(opt.refine), _p(u3), _p(inc), _p(em)))
+    if a.enabled:
+        _check(lib.ffb_get_reg(ctx.handle, _p(reg.alpha), None))
+    return FlowState.from_planes(u3), SchwarzStats(list(inc[:opt.n_iters]), list(em[:n_upd]))
+
+
 # ------------------------------------------------------------------------- pipeline
 @dataclass
 class RunConfig:
