@@ -531,8 +531,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-constexpr int kSW = 16;  // solve warps per CTA
+constexpr int kSW = 16;  // solve warps per CTA: 15 compute + 1 producer
 constexpr int kST = kSW * 32;
+constexpr int kCW = kSW - 1;
+constexpr int kCT = kCW * 32;
 
 // Row chunking of a CTA's rows [rlo, rhi) of one line: the longest run of rows starting at
 // r0 whose packed size fits `cap` doubles (at least one row). Identical on every thread.
@@ -563,9 +565,20 @@ __device__ __forceinline__ int chain_line(int phase, int chain, int L, int t) {
   return chain == 0 ? m - t : m + t;
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// barrier among the compute warps only (the producer warp streams on independently)
+__device__ __forceinline__ void compute_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kCT) : "memory");
+}
+
 // One sweep (phase 0 forward / 1 backward) of both chains of every subdomain: cluster of C
 // CTAs per (subdomain, chain); each line's packed rows are split over the cluster (equal
 // entry counts) and the symmetric products combined through distributed shared memory.
+// Warp 15 is a producer that streams the CTA's share of every line through the shared-memory
+// ring (cp.async.bulk, full/empty mbarriers) independently of the compute warps, so the bulk
+// copy engine keeps running across the per-line reductions.
 template <int MAXM>
 __global__ void __launch_bounds__(kST, 1)
     k_line_solve(const SubInfo* __restrict__ subs, const double* __restrict__ fac,
@@ -584,10 +597,11 @@ __global__ void __launch_bounds__(kST, 1)
   const int rlo = row_lo(crank, C, kd), rhi = row_lo(crank + 1, C, kd);
   const double* F = fac + s.fac_off;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + 8;
   double* stage0 = reinterpret_cast<double*>(smem_raw + 128);
-  double* colpart = stage0 + static_cast<size_t>(stages) * cap;  // kSW x kd_max
-  double* wv = colpart + static_cast<size_t>(kSW) * kd_max;      // kd_max
+  double* colpart = stage0 + static_cast<size_t>(stages) * cap;  // kCW x kd_max
+  double* wv = colpart + static_cast<size_t>(kCW) * kd_max;      // kd_max
   double* yrow = wv + kd_max;                                    // kd_max (own rows)
   double* xprev = yrow + kd_max;                                 // kd_max
   double* red = xprev + kd_max;                                  // 8 x kd_max reduce slots
@@ -597,37 +611,75 @@ __global__ void __launch_bounds__(kST, 1)
   if (nl == 0) return;  // cluster-uniform
 
   if (tid == 0) {
-    for (int q = 0; q < stages; ++q) mbar_init(&bar[q], 1);
+    for (int q = 0; q < stages; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], kCW);
+    }
     fence_barrier_init();
   }
   for (int j = tid; j < kd_max; j += kST) xprev[j] = 0.0;
   __syncthreads();
 
-  int p_seq = 0, p_t = 0, p_r0 = rlo;  // producer (thread 0)
-  auto produce = [&]() {
-    if (p_t >= nl || rlo >= rhi) return;
-    const int l = chain_line(phase, chain, L, p_t);
-    const int r1 = chunk_end(p_r0, rhi, cap);
-    const long long o0 = prow_off(p_r0), o1 = prow_off(r1);
-    const int st = p_seq % stages;
-    fence_proxy_async();
-    mbar_expect_tx(&bar[st], static_cast<uint32_t>((o1 - o0) * sizeof(double)));
-    bulk_g2s(stage0 + static_cast<size_t>(st) * cap, F + static_cast<long long>(l) * s.line_sz + o0,
-             static_cast<uint32_t>((o1 - o0) * sizeof(double)), &bar[st]);
-    ++p_seq;
-    p_r0 = r1;
-    if (p_r0 >= rhi) {
-      p_r0 = rlo;
-      ++p_t;
+  // ------------------------------------------------------------------ producer warp
+  if (warp == kCW) {
+    if (rlo >= rhi) {  // no rows here: still take part in the cluster barriers
+      for (int t = 0; t < nl && C > 1; ++t) {
+        cl_sync();
+        cl_sync();
+      }
+      return;
     }
-  };
-  if (tid == 0)
-    for (int q = 0; q < stages; ++q) produce();
+    int q = 0, t_i = 0, r_i = rlo;
+    int line_of[8];  // line of the chunk last placed in each stage
+#pragma unroll
+    for (int k = 0; k < 8; ++k) line_of[k] = -1;
+    auto issue_until = [&](int t_sync) {
+      // place chunks in FIFO order while they belong to lines <= t_sync + 1 and the stage's
+      // previous occupant belongs to a line the consumers finish before barrier t_sync
+      while (t_i < nl) {
+        if (C > 1 && t_i > t_sync + 1) break;
+        const int st = q % stages;
+        int prev_line = -1;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k == st) prev_line = line_of[k];
+        if (C > 1 && prev_line > t_sync) break;
+        if (q >= stages) mbar_wait(&empty[st], ((q / stages) - 1) & 1);
+        const int l = chain_line(phase, chain, L, t_i);
+        const int r1 = chunk_end(r_i, rhi, cap);
+        const long long o0 = prow_off(r_i), o1 = prow_off(r1);
+        if (lane == 0) {
+          fence_proxy_async();
+          mbar_expect_tx(&full[st], static_cast<uint32_t>((o1 - o0) * sizeof(double)));
+          bulk_g2s(stage0 + static_cast<size_t>(st) * cap, F + static_cast<long long>(l) * s.line_sz + o0,
+                   static_cast<uint32_t>((o1 - o0) * sizeof(double)), &full[st]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k == st) line_of[k] = t_i;
+        ++q;
+        r_i = r1;
+        if (r_i >= rhi) r_i = rlo, ++t_i;
+      }
+    };
+    if (C == 1) {
+      issue_until(1 << 30);
+    } else {
+      for (int t = 0; t < nl; ++t) {
+        issue_until(t);
+        cl_sync();
+        cl_sync();
+      }
+    }
+    return;
+  }
 
+  // ------------------------------------------------------------------ compute warps
   // operand of line step t, prefetched into registers one step ahead. Forward:
   // w = r_l - b_prev o y_prev; backward middle: w = r_m - b_m y_{m-1} - b_{m+1} y_{m+1};
   // backward chain: w = b_next o x_next and x_l = y_l - Dinv_l w.
-  constexpr int PS = 2;  // j = tid + kST*q, kd <= 2*kST
+  constexpr int PS = 2;  // j = tid + kCT*q, kd <= 2*kCT
   double pf_r[PS], pf_b[PS], pf_y[PS];
   auto prefetch = [&](int t) {
 #pragma unroll
@@ -635,7 +687,7 @@ __global__ void __launch_bounds__(kST, 1)
       pf_r[q] = pf_b[q] = pf_y[q] = 0.0;
       if (t >= nl) continue;
       const int l = chain_line(phase, chain, L, t);
-      const int j = tid + kST * q;
+      const int j = tid + kCT * q;
       if (j < kd) {
         if (phase == 0) {
           pf_r[q] = rl ? rl[static_cast<long long>(l) * kd + j] : r[gidx(s, l, j, W, nc)];
@@ -650,7 +702,7 @@ __global__ void __launch_bounds__(kST, 1)
           pf_b[q] = bcoef(s, coef, N, W, nc, chain == 0 ? l + 1 : l, j);
         }
       }
-      const int jo = rlo + tid + kST * q;  // owned row
+      const int jo = rlo + tid + kCT * q;  // owned row
       if (phase == 1 && t > 0 && jo < rhi) pf_y[q] = yl[static_cast<long long>(l) * kd + jo];
     }
   };
@@ -664,14 +716,14 @@ __global__ void __launch_bounds__(kST, 1)
     double cur_y[PS];
 #pragma unroll
     for (int q = 0; q < PS; ++q) {
-      const int j = tid + kST * q;
+      const int j = tid + kCT * q;
       if (j < kd)
         wv[j] = (phase == 0) ? pf_r[q] - pf_b[q] * xprev[j]
                              : (t == 0 ? pf_r[q] : pf_b[q] * xprev[j]);
       cur_y[q] = pf_y[q];
     }
     prefetch(t + 1);
-    __syncthreads();
+    compute_bar();
     PROF_MARK(0);
     double colacc[MAXM];
 #pragma unroll
@@ -680,10 +732,10 @@ __global__ void __launch_bounds__(kST, 1)
     while (r0 < rhi) {
       const int r1 = chunk_end(r0, rhi, cap);
       const int st = c_seq % stages;
-      mbar_wait(&bar[st], (c_seq / stages) & 1);
+      mbar_wait(&full[st], (c_seq / stages) & 1);
       PROF_MARK(1);
       const double* Sb = stage0 + static_cast<size_t>(st) * cap - prow_off(r0);
-      for (int i = r0 + warp; i < r1; i += kSW) {
+      for (int i = r0 + warp; i < r1; i += kCW) {
         const double* Si = Sb + prow_off(i);
         const double wi = wv[i];
         double racc = 0.0;
@@ -701,9 +753,9 @@ __global__ void __launch_bounds__(kST, 1)
         for (int off = 16; off; off >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, off);
         if (lane == 0) yrow[i] = racc;
       }
-      __syncthreads();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
       PROF_MARK(2);
-      if (tid == 0) produce();
       ++c_seq;
       r0 = r1;
     }
@@ -712,26 +764,26 @@ __global__ void __launch_bounds__(kST, 1)
       const int j = lane + 32 * mm;
       if (j < rhi) colpart[warp * kd_max + j] = colacc[mm];
     }
-    __syncthreads();
+    compute_bar();
     PROF_MARK(3);
     // column partials of this CTA (+ its own row dots), reduced in a fixed warp order and
     // scattered to the CTA that owns each row
     int owner = 0;
-    for (int j = tid; j < rhi; j += kST) {
+    for (int j = tid; j < rhi; j += kCT) {
       double tv = (j >= rlo) ? yrow[j] : 0.0;
-#pragma unroll 4
-      for (int w = 0; w < kSW; ++w) tv += colpart[w * kd_max + j];
+#pragma unroll 5
+      for (int w = 0; w < kCW; ++w) tv += colpart[w * kd_max + j];
       while (owner + 1 < C && row_lo(owner + 1, C, kd) <= j) ++owner;
       if (C == 1)
         red[j] = tv;
       else
         cl_map(red, static_cast<unsigned>(owner))[crank * kd_max + j] = tv;
     }
-    if (C == 1) __syncthreads(); else cl_sync();
+    if (C == 1) compute_bar(); else cl_sync();
     PROF_MARK(4);
 #pragma unroll
     for (int q = 0; q < PS; ++q) {
-      const int j = rlo + tid + kST * q;
+      const int j = rlo + tid + kCT * q;
       if (j >= rhi) continue;
       double tv = 0.0;
       if (C == 1) {
@@ -759,7 +811,7 @@ __global__ void __launch_bounds__(kST, 1)
         for (int c = 0; c < C; ++c) cl_map(xprev, static_cast<unsigned>(c))[j] = v;
       }
     }
-    if (C == 1) __syncthreads(); else cl_sync();
+    if (C == 1) compute_bar(); else cl_sync();
     PROF_MARK(5);
   }
   PROF_FLUSH(16);
@@ -835,14 +887,19 @@ SolvePlan solve_plan(int kd_max, int C) {
   SolvePlan pl{};
   pl.C = C;
   const size_t fixed =
-      128 + (static_cast<size_t>(kSW) * kd_max + 3 * kd_max + 8 * kd_max) * sizeof(double);
+      128 + (static_cast<size_t>(kCW) * kd_max + 3 * kd_max + 8 * kd_max) * sizeof(double);
   const size_t budget = 227 * 1024 - 1024;
-  if (kd_max > 2 * kST || fixed + 2 * 1024 * sizeof(double) > budget)
+  if (kd_max > 2 * kCT || fixed + 2 * 1024 * sizeof(double) > budget)
     fail("linsolve.cholesky: subdomain line too wide for the solve kernel");
   const size_t avail = budget - fixed;
-  int stages = 3;
-  long long cap = static_cast<long long>(avail / (stages * sizeof(double))) & ~1LL;
-  if (cap < 4LL * (kd_max + 2)) {
+  // as many ring stages (<= 8) as keep each stage >= 2 rows of the widest line and >= 16 KB
+  int stages = 8;
+  long long cap = 0;
+  for (; stages >= 2; --stages) {
+    cap = static_cast<long long>(avail / (stages * sizeof(double))) & ~1LL;
+    if (cap >= 2LL * (kd_max + 2) && cap * 8 >= 16384) break;
+  }
+  if (stages < 2) {
     stages = 2;
     cap = static_cast<long long>(avail / (stages * sizeof(double))) & ~1LL;
   }
