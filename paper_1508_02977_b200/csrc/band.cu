@@ -30,6 +30,8 @@
 #include "ffb_internal.cuh"
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 namespace ffb {
 
@@ -817,6 +819,188 @@ __global__ void __launch_bounds__(kST, 1)
   PROF_FLUSH(16);
 }
 
+// Variant without shared-memory staging: every warp streams its rows straight from global
+// memory into registers (ld.global.nc, no L1 allocation), keeping the next row's loads in
+// flight while it computes the current one — also across line boundaries, so the loads
+// overlap the per-line reductions. All 16 warps compute.
+__device__ __forceinline__ double ldg_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+template <int MAXM>
+__global__ void __launch_bounds__(kST, 1)
+    k_line_solve_ldg(const SubInfo* __restrict__ subs, const double* __restrict__ fac,
+                     const double* __restrict__ coef, size_t N, const double* __restrict__ r,
+                     double* __restrict__ ylocal, double* __restrict__ zlocal, int W, int nc,
+                     int kd_max, int phase, const int* __restrict__ flags,
+                     const double* __restrict__ rlocal) {
+  if (flags && (flags[0] | flags[1])) return;
+  const int C = static_cast<int>(cl_size()), crank = static_cast<int>(cl_rank());
+  const int cid = blockIdx.x / C;
+  const int sub = cid >> 1, chain = cid & 1;
+  const SubInfo s = subs[sub];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kd = s.kd, L = s.L, m = mid_line(L);
+  const int nl = chain_len(phase, chain, L);
+  const int rlo = row_lo(crank, C, kd), rhi = row_lo(crank + 1, C, kd);
+  const double* F = fac + s.fac_off;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* colpart = reinterpret_cast<double*>(smem_raw);  // kSW x kd_max
+  double* wv = colpart + static_cast<size_t>(kSW) * kd_max;
+  double* yrow = wv + kd_max;
+  double* xprev = yrow + kd_max;
+  double* red = xprev + kd_max;
+  double* yl = ylocal + s.vec_off;
+  double* zl = zlocal + s.vec_off;
+  const double* rl = rlocal ? rlocal + s.vec_off : nullptr;
+  if (nl == 0) return;
+  for (int j = tid; j < kd_max; j += kST) xprev[j] = 0.0;
+
+  // the warp's row stream: (line step t, row i) with i = rlo + warp + kSW*k
+  double buf[MAXM];
+  int nt = 0, ni = rlo + warp;  // next row to load
+  auto load_next = [&]() {      // issue the loads of the next row of this warp's stream
+    while (nt < nl && ni >= rhi) ++nt, ni = rlo + warp;
+    if (nt >= nl) return;
+    const int l = chain_line(phase, chain, L, nt);
+    const double* Si = F + static_cast<long long>(l) * s.line_sz + prow_off(ni);
+#pragma unroll
+    for (int mm = 0; mm < MAXM; ++mm) {
+      const int j = lane + 32 * mm;
+      buf[mm] = (32 * mm <= ni && j <= ni) ? ldg_stream(Si + j) : 0.0;
+    }
+  };
+  load_next();
+
+  constexpr int PS = 2;
+  double pf_r[PS], pf_b[PS], pf_y[PS];
+  auto prefetch = [&](int t) {
+#pragma unroll
+    for (int q = 0; q < PS; ++q) {
+      pf_r[q] = pf_b[q] = pf_y[q] = 0.0;
+      if (t >= nl) continue;
+      const int l = chain_line(phase, chain, L, t);
+      const int j = tid + kST * q;
+      if (j < kd) {
+        if (phase == 0) {
+          pf_r[q] = rl ? rl[static_cast<long long>(l) * kd + j] : r[gidx(s, l, j, W, nc)];
+          if (t > 0) pf_b[q] = bcoef(s, coef, N, W, nc, chain == 0 ? l : l + 1, j);
+        } else if (t == 0) {
+          double w = rl ? rl[static_cast<long long>(l) * kd + j] : r[gidx(s, l, j, W, nc)];
+          if (m > 0) w -= bcoef(s, coef, N, W, nc, m, j) * yl[static_cast<long long>(m - 1) * kd + j];
+          if (m < L - 1)
+            w -= bcoef(s, coef, N, W, nc, m + 1, j) * yl[static_cast<long long>(m + 1) * kd + j];
+          pf_r[q] = w;
+        } else {
+          pf_b[q] = bcoef(s, coef, N, W, nc, chain == 0 ? l + 1 : l, j);
+        }
+      }
+      const int jo = rlo + tid + kST * q;
+      if (phase == 1 && t > 0 && jo < rhi) pf_y[q] = yl[static_cast<long long>(l) * kd + jo];
+    }
+  };
+  prefetch(0);
+  __syncthreads();
+  PROF_DECL
+
+  for (int t = 0; t < nl; ++t) {
+    const int l = chain_line(phase, chain, L, t);
+    const bool subtract = phase == 1 && t > 0;
+    double cur_y[PS];
+#pragma unroll
+    for (int q = 0; q < PS; ++q) {
+      const int j = tid + kST * q;
+      if (j < kd)
+        wv[j] = (phase == 0) ? pf_r[q] - pf_b[q] * xprev[j]
+                             : (t == 0 ? pf_r[q] : pf_b[q] * xprev[j]);
+      cur_y[q] = pf_y[q];
+    }
+    prefetch(t + 1);
+    __syncthreads();
+    PROF_MARK(0);
+    double colacc[MAXM];
+#pragma unroll
+    for (int mm = 0; mm < MAXM; ++mm) colacc[mm] = 0.0;
+    for (int i = rlo + warp; i < rhi; i += kSW) {
+      double cur[MAXM];
+#pragma unroll
+      for (int mm = 0; mm < MAXM; ++mm) cur[mm] = buf[mm];
+      ni += kSW;
+      load_next();  // next row (possibly of the next line) in flight during this row
+      const double wi = wv[i];
+      double racc = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < MAXM; ++mm) {
+        const int j = lane + 32 * mm;
+        if (32 * mm > i) break;
+        if (j <= i) {
+          racc = fma(cur[mm], wv[j], racc);
+          if (j < i) colacc[mm] = fma(cur[mm], wi, colacc[mm]);
+        }
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, off);
+      if (lane == 0) yrow[i] = racc;
+    }
+    PROF_MARK(2);
+#pragma unroll
+    for (int mm = 0; mm < MAXM; ++mm) {
+      const int j = lane + 32 * mm;
+      if (j < rhi) colpart[warp * kd_max + j] = colacc[mm];
+    }
+    __syncthreads();
+    PROF_MARK(3);
+    int owner = 0;
+    for (int j = tid; j < rhi; j += kST) {
+      double tv = (j >= rlo) ? yrow[j] : 0.0;
+#pragma unroll 4
+      for (int w = 0; w < kSW; ++w) tv += colpart[w * kd_max + j];
+      while (owner + 1 < C && row_lo(owner + 1, C, kd) <= j) ++owner;
+      if (C == 1)
+        red[j] = tv;
+      else
+        cl_map(red, static_cast<unsigned>(owner))[crank * kd_max + j] = tv;
+    }
+    if (C == 1) __syncthreads(); else cl_sync();
+    PROF_MARK(4);
+#pragma unroll
+    for (int q = 0; q < PS; ++q) {
+      const int j = rlo + tid + kST * q;
+      if (j >= rhi) continue;
+      double tv = 0.0;
+      if (C == 1) {
+        tv = red[j];
+      } else {
+        for (int c = crank; c < C; ++c) tv += red[c * kd_max + j];
+      }
+      const long long k = static_cast<long long>(l) * kd + j;
+      double v;
+      if (!subtract) {
+        v = tv;
+        if (phase == 0) {
+          yl[k] = v;
+          if (L == 1) zl[k] = v;
+        } else if (chain == 0) {
+          zl[k] = v;
+        }
+      } else {
+        v = cur_y[q] - tv;
+        zl[k] = v;
+      }
+      if (C == 1) {
+        xprev[j] = v;
+      } else {
+        for (int c = 0; c < C; ++c) cl_map(xprev, static_cast<unsigned>(c))[j] = v;
+      }
+    }
+    if (C == 1) __syncthreads(); else cl_sync();
+    PROF_MARK(5);
+  }
+  PROF_FLUSH(16);
+}
+
 }  // namespace
 
 long long packed_line_size(int kd) { return prow_off(kd); }
@@ -893,7 +1077,9 @@ SolvePlan solve_plan(int kd_max, int C) {
     fail("linsolve.cholesky: subdomain line too wide for the solve kernel");
   const size_t avail = budget - fixed;
   // as many ring stages (<= 8) as keep each stage >= 2 rows of the widest line and >= 16 KB
-  int stages = 8;
+  int max_stages = 2;  // measured: two large stages beat 3-8 smaller ones (bulk-copy size)
+  if (const char* e = std::getenv("FFB_STAGES")) max_stages = std::max(2, std::min(8, std::atoi(e)));
+  int stages = max_stages;
   long long cap = 0;
   for (; stages >= 2; --stages) {
     cap = static_cast<long long>(avail / (stages * sizeof(double))) & ~1LL;
@@ -909,6 +1095,8 @@ SolvePlan solve_plan(int kd_max, int C) {
   pl.smem = fixed + static_cast<size_t>(stages) * cap * sizeof(double);
   pl.maxm = (kd_max + 31) / 32;
   pl.kd_max = kd_max;
+  pl.ldg = 0;
+  if (const char* e = std::getenv("FFB_SOLVE")) pl.ldg = std::string(e) == "ldg";
   return pl;
 }
 
@@ -918,8 +1106,15 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
                            double* ylocal, double* zlocal, int W, int nc, const int* flags,
                            const double* rlocal, cudaStream_t st) {
   for (int phase = 0; phase <= 1; ++phase) {
-    launch_cluster(k_line_solve<M>, 2 * nsub * pl.C, kST, pl.smem, pl.C, st, d_subs, fac, coef, N,
-                   r, ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, phase, flags, rlocal);
+    if (pl.ldg) {
+      const size_t smem = (static_cast<size_t>(kSW) * pl.kd_max + 11 * pl.kd_max) * sizeof(double);
+      launch_cluster(k_line_solve_ldg<M>, 2 * nsub * pl.C, kST, smem, pl.C, st, d_subs, fac, coef,
+                     N, r, ylocal, zlocal, W, nc, pl.kd_max, phase, flags, rlocal);
+    } else {
+      launch_cluster(k_line_solve<M>, 2 * nsub * pl.C, kST, pl.smem, pl.C, st, d_subs, fac, coef,
+                     N, r, ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, phase, flags,
+                     rlocal);
+    }
     FFB_LAUNCHED();
   }
 }

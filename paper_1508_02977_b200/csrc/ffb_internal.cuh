@@ -88,7 +88,7 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max, con
                  size_t N, int W, int nc, double* fac, double* scratch, long long scratch_stride,
                  int* d_bad, cudaStream_t st);
 struct SolvePlan {
-  int stages, cap, maxm, C, kd_max;
+  int stages, cap, maxm, C, kd_max, ldg;
   size_t smem;
 };
 SolvePlan solve_plan(int kd_max, int C);
