@@ -455,12 +455,18 @@ template <int NB>
 __global__ void __launch_bounds__(kFT, 1)
     k_line_factor(const SubInfo* __restrict__ subs, const double* __restrict__ coef, size_t N,
                   int W, int nc, double* __restrict__ fac, double* __restrict__ scratch,
-                  long long scratch_stride, int kdp, int mid, int* __restrict__ bad) {
+                  long long scratch_stride, int kdp, int mid, int* __restrict__ bad,
+                  const int2* __restrict__ changed) {
   const int sub = mid ? blockIdx.x : blockIdx.x >> 1;
   const int chain = mid ? 0 : blockIdx.x & 1;
   const SubInfo s = subs[sub];
   const int tid = threadIdx.x;
   const int kd = s.kd, L = s.L, m = mid_line(L);
+  // lines [lo, hi] of this subdomain whose operator changed since the last factorisation
+  // (all of them on a full refactorisation): chain 0 restarts at lo, chain 1 at hi, and the
+  // untouched prefix of each chain keeps its inverses (D_l depends on lines <= l only)
+  const int2 chg = changed ? changed[sub] : make_int2(0, L - 1);
+  if (chg.x > chg.y) return;  // nothing changed in this subdomain
   double* D = scratch + (mid ? sub : blockIdx.x) * scratch_stride;
   double* F = fac + s.fac_off;
   extern __shared__ __align__(16) double fsm[];
@@ -479,7 +485,8 @@ __global__ void __launch_bounds__(kFT, 1)
     pack_line(s, m, D, F);
   } else {
     const int nlines = chain == 0 ? m : L - 1 - m;
-    for (int t = 0; t < nlines; ++t) {
+    const int t0 = chain == 0 ? chg.x : L - 1 - chg.y;
+    for (int t = max(t0, 0); t < nlines; ++t) {
       const int l = chain == 0 ? t : L - 1 - t;
       const int prev = t == 0 ? -1 : (chain == 0 ? l - 1 : l + 1);
       const int bl = chain == 0 ? l : l + 1;  // coupling between l and prev
@@ -727,9 +734,17 @@ __global__ void __launch_bounds__(kST, 1)
     prefetch(t + 1);
     compute_bar();
     PROF_MARK(0);
-    double colacc[MAXM];
+    // lane owns the column pairs j = 64 mm + 2 lane + {0, 1}: operand in registers for the
+    // whole line, rows read as 16-byte pairs (row starts are 16-byte aligned)
+    constexpr int M2 = (MAXM + 1) / 2;
+    double2 wreg[M2], cacc[M2];
 #pragma unroll
-    for (int mm = 0; mm < MAXM; ++mm) colacc[mm] = 0.0;
+    for (int mm = 0; mm < M2; ++mm) {
+      const int j = 64 * mm + 2 * lane;
+      wreg[mm].x = j < kd ? wv[j] : 0.0;
+      wreg[mm].y = j + 1 < kd ? wv[j + 1] : 0.0;
+      cacc[mm].x = cacc[mm].y = 0.0;
+    }
     int r0 = rlo;
     while (r0 < rhi) {
       const int r1 = chunk_end(r0, rhi, cap);
@@ -737,23 +752,56 @@ __global__ void __launch_bounds__(kST, 1)
       mbar_wait(&full[st], (c_seq / stages) & 1);
       PROF_MARK(1);
       const double* Sb = stage0 + static_cast<size_t>(st) * cap - prow_off(r0);
-      for (int i = r0 + warp; i < r1; i += kCW) {
-        const double* Si = Sb + prow_off(i);
-        const double wi = wv[i];
-        double racc = 0.0;
+      // batches of 8 rows per warp: 8 independent accumulation chains, one transpose
+      // reduction (9 shuffles) per batch instead of 5 per row
+      for (int i0 = r0 + warp; i0 < r1; i0 += 8 * kCW) {
+        double racc[8];
 #pragma unroll
-        for (int mm = 0; mm < MAXM; ++mm) {
-          const int j = lane + 32 * mm;
-          if (32 * mm > i) break;
-          if (j <= i) {
-            const double sij = Si[j];
-            racc = fma(sij, wv[j], racc);
-            if (j < i) colacc[mm] = fma(sij, wi, colacc[mm]);
+        for (int k = 0; k < 8; ++k) {
+          racc[k] = 0.0;
+          const int i = i0 + k * kCW;
+          if (i >= r1) continue;
+          const double* Si = Sb + prow_off(i);
+          const double wi = wv[i];
+#pragma unroll
+          for (int mm = 0; mm < M2; ++mm) {
+            const int j = 64 * mm + 2 * lane;
+            if (64 * mm > i) break;
+            if (j <= i) {
+              const double2 v = *reinterpret_cast<const double2*>(Si + j);
+              const double vy = j + 1 <= i ? v.y : 0.0;
+              racc[k] = fma(v.x, wreg[mm].x, racc[k]);
+              racc[k] = fma(vy, wreg[mm].y, racc[k]);
+              if (j < i) cacc[mm].x = fma(v.x, wi, cacc[mm].x);
+              if (j + 1 < i) cacc[mm].y = fma(v.y, wi, cacc[mm].y);
+            }
           }
         }
+        {  // transpose reduction: lane ends with the total of row k(lane)
+          const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
 #pragma unroll
-        for (int off = 16; off; off >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, off);
-        if (lane == 0) yrow[i] = racc;
+          for (int k = 0; k < 4; ++k) {
+            const double send = b4 ? racc[k] : racc[k + 4];
+            const double keep = b4 ? racc[k + 4] : racc[k];
+            racc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+          }
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const double send = b3 ? racc[k] : racc[k + 2];
+            const double keep = b3 ? racc[k + 2] : racc[k];
+            racc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+          }
+          {
+            const double send = b2 ? racc[0] : racc[1];
+            const double keep = b2 ? racc[1] : racc[0];
+            racc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+          }
+          racc[0] += __shfl_xor_sync(0xffffffffu, racc[0], 2);
+          racc[0] += __shfl_xor_sync(0xffffffffu, racc[0], 1);
+          const int k = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
+          const int i = i0 + k * kCW;
+          if ((lane & 3) == 0 && i < r1) yrow[i] = racc[0];
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
@@ -762,9 +810,10 @@ __global__ void __launch_bounds__(kST, 1)
       r0 = r1;
     }
 #pragma unroll
-    for (int mm = 0; mm < MAXM; ++mm) {
-      const int j = lane + 32 * mm;
-      if (j < rhi) colpart[warp * kd_max + j] = colacc[mm];
+    for (int mm = 0; mm < M2; ++mm) {
+      const int j = 64 * mm + 2 * lane;
+      if (j < rhi) colpart[warp * kd_max + j] = cacc[mm].x;
+      if (j + 1 < rhi) colpart[warp * kd_max + j + 1] = cacc[mm].y;
     }
     compute_bar();
     PROF_MARK(3);
@@ -1042,9 +1091,52 @@ size_t factor_scratch_doubles(int nsub, int kd_max) {
   return static_cast<size_t>(2 * nsub) * kd_max * kd_max;
 }
 
+// changed[sub] = (first, last) local line touched by a triangle whose alpha differs from
+// alpha_fact (a triangle touches the lines of its three vertices); (INT_MAX, -1) if none
+__global__ void k_changed_lines(const SubInfo* __restrict__ subs, const double* __restrict__ alpha,
+                                const double* __restrict__ alpha_fact, int W, int H,
+                                int2* __restrict__ changed) {
+  const SubInfo s = subs[blockIdx.x];
+  int lo = 0x7fffffff, hi = -1;
+  const int cx0 = max(s.fx0 - 1, 0), cx1 = min(s.fx0 + s.fw, W - 1);
+  const int cy0 = max(s.fy0 - 1, 0), cy1 = min(s.fy0 + s.fh, H - 1);
+  const int ncx = cx1 - cx0, ncy = cy1 - cy0;
+  for (int e = threadIdx.x; e < ncx * ncy; e += blockDim.x) {
+    const int cx = cx0 + e % ncx, cy = cy0 + e / ncx;
+    const long long t = 2LL * (static_cast<long long>(cy) * (W - 1) + cx);
+    if (alpha[t] == alpha_fact[t] && alpha[t + 1] == alpha_fact[t + 1]) continue;
+    // the cell's vertices (cx..cx+1, cy..cy+1) inside the free rectangle -> their lines
+    for (int dy = 0; dy <= 1; ++dy)
+      for (int dx = 0; dx <= 1; ++dx) {
+        const int lx = cx + dx - s.fx0, ly = cy + dy - s.fy0;
+        if (lx < 0 || ly < 0 || lx >= s.fw || ly >= s.fh) continue;
+        const int l = s.xfast ? ly : lx;
+        lo = min(lo, l);
+        hi = max(hi, l);
+      }
+  }
+  __shared__ int slo[32], shi[32];
+  for (int off = 16; off; off >>= 1) {
+    lo = min(lo, __shfl_xor_sync(~0u, lo, off));
+    hi = max(hi, __shfl_xor_sync(~0u, hi, off));
+  }
+  if ((threadIdx.x & 31) == 0) slo[threadIdx.x >> 5] = lo, shi[threadIdx.x >> 5] = hi;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (blockDim.x >> 5); ++w) lo = min(lo, slo[w]), hi = max(hi, shi[w]);
+    changed[blockIdx.x] = make_int2(lo, hi);
+  }
+}
+
+void changed_lines(const SubInfo* d_subs, int nsub, const double* alpha, const double* alpha_fact,
+                   int W, int H, int2* changed, cudaStream_t st) {
+  k_changed_lines<<<nsub, 256, 0, st>>>(d_subs, alpha, alpha_fact, W, H, changed);
+  FFB_LAUNCHED();
+}
+
 void line_factor(const SubInfo* d_subs, int nsub, int /*C*/, int nb, int kd_max,
                  const double* coef, size_t N, int W, int nc, double* fac, double* scratch,
-                 long long scratch_stride, int* d_bad, cudaStream_t st) {
+                 long long scratch_stride, int* d_bad, cudaStream_t st, const int2* changed) {
   const int kdp = (kd_max + 31) / 32 * 32;
   const size_t smem = (2 * nb * (nb + 1) + 8 * nb + static_cast<size_t>(nb) * kdp) * sizeof(double);
   if (smem > 227 * 1024) fail("linsolve.cholesky: subdomain line too wide for shared memory");
@@ -1054,12 +1146,12 @@ void line_factor(const SubInfo* d_subs, int nsub, int /*C*/, int nb, int kd_max,
       FFB_CUDA(cudaFuncSetAttribute(k_line_factor<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
       k_line_factor<32><<<grid, kFT, smem, st>>>(d_subs, coef, N, W, nc, fac, scratch,
-                                                 scratch_stride, kdp, mid, d_bad);
+                                                 scratch_stride, kdp, mid, d_bad, changed);
     } else if (nb == 16) {
       FFB_CUDA(cudaFuncSetAttribute(k_line_factor<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
       k_line_factor<16><<<grid, kFT, smem, st>>>(d_subs, coef, N, W, nc, fac, scratch,
-                                                 scratch_stride, kdp, mid, d_bad);
+                                                 scratch_stride, kdp, mid, d_bad, changed);
     } else {
       fail("internal: unsupported pivot block size");
     }

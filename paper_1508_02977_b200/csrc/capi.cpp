@@ -113,6 +113,11 @@ struct ffb_ctx {
   DBuf<AxisMap> d_col, d_row;
   DBuf<double> fac, dscratch, ylocal, zlocal, rlocal, xlocal, G0, G1, incs;
   DBuf<int> own_col, own_row;
+  DBuf<double> alpha_fact;  // alpha of the resident factorisation (incremental refactor)
+  DBuf<int2> d_changed;
+  long long fact_key_t_full = -1;  // terms version / partition of the last full factorisation
+  int fact_valid = 0;
+  bool incremental = true;
   DBuf<int> d_bad;
   double factor_doubles = 0, apply_doubles = 0, sum_n = 0;
   // asm kernel timing
@@ -221,6 +226,7 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
     return;
   c->have_part = false;
   c->factor_key_a = c->factor_key_t = -1;
+  c->fact_valid = 0;
   const int W = c->W, H = c->H;
   c->decomp = build_partition(W, H, px, py, ov);
   const int np = px * py;
@@ -233,6 +239,7 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
   }
   c->kd_max = kd_max;
   c->nbf = kd_max > 512 ? 16 : 32;
+  c->incremental = !std::getenv("FFB_FULL_REFACTOR");
   if (const char* e = std::getenv("FFB_NB")) {
     const int v = std::atoi(e);
     if (v == 16 || v == 32) c->nbf = v;
@@ -325,9 +332,22 @@ void ensure_factor(ffb_ctx* c, int nc) {
   ensure_coef(c, nc);
   const int np = c->s_hi - c->s_lo;
   FFB_CUDA(cudaMemsetAsync(c->d_bad.p, 0x7f, np * sizeof(int), c->st));
+  // Only alpha changed since the last (successful) factorisation of this partition and these
+  // terms: refactor each chain from the first line the change touches (exact).
+  const bool incr = c->incremental && c->fact_valid && c->factor_key_t == c->terms_version &&
+                    c->alpha_fact.p != nullptr;
+  const int2* changed = nullptr;
+  c->fact_valid = 0;  // until this factorisation has succeeded
+  if (incr) {
+    int2* ch = c->d_changed.ensure(np);
+    changed_lines(c->d_subs.p + c->s_lo, np, c->alpha.p, c->alpha_fact.p, c->W, c->H, ch, c->st);
+    changed = ch;
+  }
   line_factor(c->d_subs.p + c->s_lo, np, c->ccl, c->nbf, c->kd_max, c->coef.p, c->N, c->W, nc,
               c->fac.p, c->dscratch.p, static_cast<long long>(c->kd_max) * c->kd_max, c->d_bad.p,
-              c->st);
+              c->st, changed);
+  FFB_CUDA(cudaMemcpyAsync(c->alpha_fact.ensure(c->ntri), c->alpha.p, c->ntri * sizeof(double),
+                           cudaMemcpyDeviceToDevice, c->st));
   std::vector<int> bad(np);
   FFB_CUDA(cudaMemcpyAsync(bad.data(), c->d_bad.p, np * sizeof(int), cudaMemcpyDeviceToHost,
                            c->st));
@@ -338,6 +358,7 @@ void ensure_factor(ffb_ctx* c, int nc) {
            std::to_string(p + c->s_lo) + ": matrix is not positive definite");
   c->factor_key_a = c->alpha_version;
   c->factor_key_t = c->terms_version;
+  c->fact_valid = 1;
 }
 
 void launch_asm(ffb_ctx* c, int nc, const double* rvec, const int* flags) {
@@ -456,6 +477,7 @@ void run_dev(ffb_ctx* c, int W, int H, const double* f0, const double* f1,
   fill(c->alpha.p, cfg->alpha0, c->ntri, c->st);
   fill(c->lambda.p, cfg->lambda0, c->ntri, c->st);
   c->alpha_version++;
+  c->fact_valid = 0;
   const Split sp = choose_split(W, H, cfg->parts);
   ensure_partition(c, sp.px, sp.py, cfg->overlap, nc);
   FFB_CUDA(cudaEventRecord(ev[1], c->st));
@@ -801,6 +823,7 @@ int ffb_set_reg(ffb_ctx* c, const double* alpha, const double* lambda) {
     upload(c->alpha.p, alpha, c->ntri, c->st);
     upload(c->lambda.p, lambda, c->ntri, c->st);
     c->alpha_version++;
+    c->fact_valid = 0;  // lambda may have changed too: no incremental refactorisation
     sync(c);
   });
 }
