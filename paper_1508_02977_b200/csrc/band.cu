@@ -20,7 +20,7 @@
 //
 // Factor (K5, one CTA per subdomain): per line, build D_l in an L2-resident kd x kd scratch
 // and invert it in place with a blocked symmetric sweep (Gauss-Jordan for SPD):
-//     pivot block K: Lc = chol(A_KK), Li = Lc^-1, Z = A_RK Li^T,
+//     pivot block K (one warp, in registers): Lc = chol(A_KK), Li = Lc^-1, Z = A_RK Li^T,
 //     A_RR -= Z Z^T (8x8 register tiles, FP64 FMA), A_RK <- Z Li, A_KK <- -Li^T Li,
 // which leaves -D^{-1}; the flops equal a banded Cholesky's (n kd^2 / 2 FMAs).
 // Solve (K6, one CTA per subdomain): the packed rows of each line are streamed through a
@@ -28,6 +28,7 @@
 // rows, producing the row dot products and, for the symmetric half, per-lane column partial
 // sums in registers, combined in a fixed order (deterministic).
 #include "ffb_internal.cuh"
+#include "pivot.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -144,63 +145,6 @@ __device__ __forceinline__ int row_lo(int c, int C, int kd) {
   return min(max(r, c), kd - (C - c));
 }
 
-// Cholesky of a w x w (w <= 4) SPD block and the inverse of its factor, computed
-// redundantly by every thread. With `src` the block is read from shared memory (breakdown
-// recorded as row `row0 + k`); with `lsrc` an already factored block is read and only
-// inverted.
-__device__ __forceinline__ void chol4(const double* src, int ld, int w, double l[4][4],
-                                      double il[4][4], int& first_bad, int row0, int tid,
-                                      const double* lsrc = nullptr, int lld = 0) {
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      l[a][b] = 0.0;
-      il[a][b] = 0.0;
-    }
-  if (src) {
-    double d[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) d[a][b] = (a < w && b <= a) ? src[a * ld + b] : (a == b ? 1.0 : 0.0);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      double dk = d[k][k];
-      if (!(dk > 0.0) || !isfinite(dk)) {
-        if (tid == 0 && k < w) first_bad = min(first_bad, row0 + k);
-        dk = 1.0;
-      }
-      const double irn = rsqrt(dk);
-      l[k][k] = dk * irn;
-      il[k][k] = irn;
-#pragma unroll
-      for (int a = k + 1; a < 4; ++a) l[a][k] = d[a][k] * irn;
-#pragma unroll
-      for (int a = k + 1; a < 4; ++a)
-#pragma unroll
-        for (int b = k + 1; b <= a; ++b) d[a][b] -= l[a][k] * l[b][k];
-    }
-  } else {
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b <= a; ++b) l[a][b] = (a < w) ? lsrc[a * lld + b] : (a == b ? 1.0 : 0.0);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) il[c][c] = 1.0 / l[c][c];
-  }
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-#pragma unroll
-    for (int a = c + 1; a < 4; ++a) {
-      double acc = 0.0;
-#pragma unroll
-      for (int k = c; k < a; ++k) acc += l[a][k] * il[k][c];
-      il[a][c] = -acc * il[a][a];
-    }
-  }
-}
-
 // ----------------------------------------------------------------- twisted chains
 // Lines 0..m-1 are factored top-down (chain 0), lines L-1..m+1 bottom-up (chain 1), and the
 // middle line m closes both:
@@ -214,95 +158,81 @@ __host__ __device__ __forceinline__ int mid_line(int L) { return (L - 1) / 2; }
 constexpr int kFT = 512;  // factor threads per CTA (16 warps)
 constexpr int kFW = kFT / 32;
 
+// A_RR -= Z Z^T on the 32x32 tile (TU, TV) of the lower triangle (rows/columns of K
+// excluded): 4x8 thread tiles (rows ub0+16q+2ui+{0,1}, columns vb0+8q+2vi+{0,1}:
+// conflict-free double2 reads of Z)
+__device__ __forceinline__ void rupd_tile(double* __restrict__ D, int kd, int kdp,
+                                          const double* __restrict__ Z, int nbk, int k0, int k1,
+                                          int TU, int TV, int lane) {
+  const int ui = lane & 7, vi = lane >> 3;
+  const int ub0 = 32 * TU + 2 * ui, vb0 = 32 * TV + 2 * vi;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {  // the tile's read-modify-write targets -> L1
+    const int u = ub0 + 16 * (i >> 1) + (i & 1);
+    if (u < kd && (vi & 1) == 0)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(D + static_cast<long long>(u) * kd + 32 * TV + 8 * vi));
+  }
+  double acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+#pragma unroll 2
+  for (int c = 0; c < nbk; ++c) {
+    const double* zc = Z + c * kdp;
+    double a[4], b[8];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double2 x = *reinterpret_cast<const double2*>(zc + ub0 + 16 * q);
+      a[2 * q] = x.x, a[2 * q + 1] = x.y;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 y = *reinterpret_cast<const double2*>(zc + vb0 + 8 * q);
+      b[2 * q] = y.x, b[2 * q + 1] = y.y;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int u = ub0 + 16 * (i >> 1) + (i & 1);
+    if (u >= kd || (u >= k0 && u < k1)) continue;
+    double* rowp = D + static_cast<long long>(u) * kd;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int v = vb0 + 8 * (j >> 1) + (j & 1);
+      if (v <= u && (v < k0 || v >= k1)) rowp[v] -= acc[i][j];
+    }
+  }
+}
+
 // In-place inversion of the SPD line matrix D (kd x kd row-major in global scratch, lower
 // triangle used) by the blocked symmetric sweep; leaves -D^{-1} in the lower triangle.
+// The next step's pivot block is factored by warp 0 while the other 15 warps write the
+// current step's A_RK and A_KK (tile updates from a dynamic queue).
+// Shared memory: P (NB x NB+1), Li[2] (double-buffered), ir (NB), the tile counter, Z.
 template <int NB>
-__device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P, double* Li,
-                             double* pan, double* dinv4, double* Z, int& first_bad,
-                             int bad_base) {
+__device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P, double* Li2,
+                             double* ir, int* cnt, double* Z, int& first_bad, int bad_base,
+                             int la) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int LS = NB * (NB + 1);
   PROF_DECL
-  for (int k0 = 0; k0 < kd; k0 += NB) {
+  if (tid == 0) cnt[0] = 0;
+  if (warp == 0) pivot_warp<NB>(D, kd, 0, min(NB, kd), P, Li2, ir, first_bad, bad_base);
+  const int nt = (kd + 31) / 32;
+  const int ntiles = nt * (nt + 1) / 2;
+  int step = 0;
+  for (int k0 = 0; k0 < kd; k0 += NB, ++step) {
     const int nbk = min(NB, kd - k0);
     const int k1 = k0 + nbk;
-    // ---- pivot block: Cholesky blocked by 4 columns, Li = inv(L) blocked by 4 rows
-    for (int e = tid; e < NB * NB; e += kFT) {
-      const int a = e / NB, b = e - a * NB;
-      P[a * (NB + 1) + b] =
-          (a < nbk && b <= a) ? D[static_cast<long long>(k0 + a) * kd + k0 + b] : 0.0;
-      Li[a * (NB + 1) + b] = 0.0;
-    }
+    const double* Li = Li2 + (step & 1) * LS;
+    double* Lnext = Li2 + ((step + 1) & 1) * LS;
     __syncthreads();
-    PROF_MARK(5);
-#pragma unroll 1
-    for (int kb = 0; kb < nbk; kb += 4) {
-      const int w4 = min(4, nbk - kb);
-      double l4[4][4], i4[4][4];
-      chol4(P + kb * (NB + 1) + kb, NB + 1, w4, l4, i4, first_bad, bad_base + k0 + kb, tid);
-      // panel of L below the 4-block
-      for (int r = kb + w4 + tid; r < nbk; r += kFT) {
-        double p[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) p[t] = t < w4 ? P[r * (NB + 1) + kb + t] : 0.0;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          double acc = 0.0;
-#pragma unroll
-          for (int t2 = 0; t2 <= t; ++t2) acc += p[t2] * i4[t][t2];
-          pan[r * 4 + t] = acc;
-        }
-      }
-      // block row kb of Li (rows kb.. of L left of the block are final):
-      //   Li[kb+a][c] = -sum_t i4[a][t] sum_{k=c}^{kb-1} L[kb+t][k] Li[k][c],  c < kb
-      for (int c = tid; c < kb; c += kFT) {
-        double sv[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          double acc = 0.0;
-          if (t < w4)
-            for (int k = c; k < kb; ++k) acc += P[(kb + t) * (NB + 1) + k] * Li[k * (NB + 1) + c];
-          sv[t] = acc;
-        }
-#pragma unroll
-        for (int a2 = 0; a2 < 4; ++a2) {
-          double v = 0.0;
-#pragma unroll
-          for (int t = 0; t <= a2; ++t) v -= i4[a2][t] * sv[t];
-          if (a2 < w4) Li[(kb + a2) * (NB + 1) + c] = v;
-        }
-      }
-      if (tid < 16) {  // diagonal blocks of L and Li (static register indices only)
-#pragma unroll
-        for (int a2 = 0; a2 < 4; ++a2)
-#pragma unroll
-          for (int b2 = 0; b2 < 4; ++b2)
-            if (tid == a2 * 4 + b2 && a2 < w4 && b2 <= a2) Li[(kb + a2) * (NB + 1) + kb + b2] = i4[a2][b2];
-      }
-      __syncthreads();
-      const int m = nbk - kb - w4;
-      for (int e = tid; e < m * m; e += kFT) {
-        const int rr = e / m, cc = e - rr * m;
-        if (cc > rr) continue;
-        const int r = kb + w4 + rr, c = kb + w4 + cc;
-        double acc = 0.0;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) acc += pan[r * 4 + t] * pan[c * 4 + t];
-        P[r * (NB + 1) + c] -= acc;
-      }
-      for (int e = tid; e < nbk * 4; e += kFT) {
-        const int r = e >> 2, t = e & 3;
-        if (t < w4 && r >= kb + w4) P[r * (NB + 1) + kb + t] = pan[r * 4 + t];
-      }
-      if (tid < 16) {
-#pragma unroll
-        for (int a2 = 0; a2 < 4; ++a2)
-#pragma unroll
-          for (int b2 = 0; b2 < 4; ++b2)
-            if (tid == a2 * 4 + b2 && a2 < w4 && b2 <= a2) P[(kb + a2) * (NB + 1) + kb + b2] = l4[a2][b2];
-      }
-      __syncthreads();
-    }
-    PROF_MARK(6);
+    if (tid == 0) cnt[(step + 1) & 1] = 0;  // the queue of the next step (idle since the sync)
     PROF_MARK(1);
     // ---- Z = A_RK Li^T, thread per row: all loads issued first, 32 independent chains
     for (int i = tid; i < kdp; i += kFT) {
@@ -323,93 +253,65 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
     }
     __syncthreads();
     PROF_MARK(2);
-    // ---- A_RR -= Z Z^T over the lower triangle (K excluded): 32x32 warp tiles, 4x8 thread
-    // tiles (rows ub0+16q+2ui+{0,1}, columns vb0+8q+2vi+{0,1}: conflict-free double2 reads)
-    {
-      const int ui = lane & 7, vi = lane >> 3;
-      const int nt = (kd + 31) / 32;
-      int TU = 0, TV = 0;
-      auto advance = [&](int steps) {
-        while (steps-- > 0) {
-          if (++TV > TU) TV = 0, ++TU;
-        }
-      };
-      advance(warp);
-      for (; TU < nt; advance(kFW)) {
-        const int ub0 = 32 * TU + 2 * ui, vb0 = 32 * TV + 2 * vi;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {  // the tile's read-modify-write targets -> L1
-          const int u = ub0 + 16 * (i >> 1) + (i & 1);
-          if (u < kd && (vi & 1) == 0)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(D + static_cast<long long>(u) * kd + 32 * TV + 8 * vi));
-        }
-        double acc[4][8];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-#pragma unroll 2
-        for (int c = 0; c < nbk; ++c) {
-          const double* zc = Z + c * kdp;
-          double a[4], b[8];
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const double2 x = *reinterpret_cast<const double2*>(zc + ub0 + 16 * q);
-            a[2 * q] = x.x, a[2 * q + 1] = x.y;
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const double2 y = *reinterpret_cast<const double2*>(zc + vb0 + 8 * q);
-            b[2 * q] = y.x, b[2 * q + 1] = y.y;
-          }
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int u = ub0 + 16 * (i >> 1) + (i & 1);
-          if (u >= kd || (u >= k0 && u < k1)) continue;
-          double* rowp = D + static_cast<long long>(u) * kd;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int v = vb0 + 8 * (j >> 1) + (j & 1);
-            if (v <= u && (v < k0 || v >= k1)) rowp[v] -= acc[i][j];
-          }
-        }
-      }
+    // ---- A_RR -= Z Z^T, 32x32 tiles from a shared queue. Look-ahead (la): warp 0 first
+    // finishes the tile holding the next pivot block and factors that block meanwhile.
+    const int nx = (la && k1 < kd) ? k1 / 32 : -1;
+    const int special = nx >= 0 ? nx * (nx + 1) / 2 + nx : -1;
+    if (warp == 0 && special >= 0) {
+      rupd_tile(D, kd, kdp, Z, nbk, k0, k1, nx, nx, lane);
+      __syncwarp();
+      pivot_warp<NB>(D, kd, k1, min(NB, kd - k1), P, Lnext, ir, first_bad, bad_base);
+      PROF_MARK(5);
     }
-    PROF_MARK(3);
-    // ---- A_RK <- Z Li ; A_KK <- -Li^T Li   (entries disjoint from the update above)
-    for (int i = tid; i < kd; i += kFT) {
-      if (i >= k0 && i < k1) continue;
-      double z[NB];
-#pragma unroll
-      for (int c = 0; c < NB; ++c) z[c] = Z[c * kdp + i];
-#pragma unroll
-      for (int c = 0; c < NB; ++c) {
-        if (c < nbk) {
-          double acc = 0.0;
-#pragma unroll
-          for (int c2 = c; c2 < NB; ++c2) acc = fma(z[c2], Li[c2 * (NB + 1) + c], acc);
-          if (i > k0)
-            D[static_cast<long long>(i) * kd + k0 + c] = acc;
-          else
-            D[static_cast<long long>(k0 + c) * kd + i] = acc;
-        }
-      }
-    }
-    for (int e = tid; e < nbk * nbk; e += kFT) {
-      const int a = e / nbk, b = e - a * nbk;
-      if (b > a) continue;
-      double acc = 0.0;
-      for (int mm = a; mm < nbk; ++mm) acc += Li[mm * (NB + 1) + a] * Li[mm * (NB + 1) + b];
-      D[static_cast<long long>(k0 + a) * kd + k0 + b] = -acc;
+    for (;;) {
+      int idx = 0;
+      if (lane == 0) idx = atomicAdd(cnt + (step & 1), 1);
+      idx = __shfl_sync(~0u, idx, 0);
+      if (idx >= ntiles) break;
+      if (idx == special) continue;
+      int TU = static_cast<int>((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
+      while (TU * (TU + 1) / 2 > idx) --TU;
+      while ((TU + 1) * (TU + 2) / 2 <= idx) ++TU;
+      rupd_tile(D, kd, kdp, Z, nbk, k0, k1, TU, idx - TU * (TU + 1) / 2, lane);
     }
     __syncthreads();
+    PROF_MARK(3);
+    if (!la && warp == 0) {
+      // the next pivot block is final now: factor it while the other warps write A_RK, A_KK
+      if (k1 < kd) pivot_warp<NB>(D, kd, k1, min(NB, kd - k1), P, Lnext, ir, first_bad, bad_base);
+      PROF_MARK(5);
+    } else {
+      // ---- A_RK <- Z Li ; A_KK <- -Li^T Li
+      const int t0 = la ? 0 : 32, t2 = tid - t0, nth = kFT - t0;
+      for (int i = t2; i < kd; i += nth) {
+        if (i >= k0 && i < k1) continue;
+        double z[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) z[c] = Z[c * kdp + i];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          if (c < nbk) {
+            double acc = 0.0;
+#pragma unroll
+            for (int c2 = c; c2 < NB; ++c2) acc = fma(z[c2], Li[c2 * (NB + 1) + c], acc);
+            if (i > k0)
+              D[static_cast<long long>(i) * kd + k0 + c] = acc;
+            else
+              D[static_cast<long long>(k0 + c) * kd + i] = acc;
+          }
+        }
+      }
+      for (int e = t2; e < nbk * nbk; e += nth) {
+        const int a = e / nbk, b = e - a * nbk;
+        if (b > a) continue;
+        double acc = 0.0;
+        for (int mm = a; mm < nbk; ++mm) acc += Li[mm * (NB + 1) + a] * Li[mm * (NB + 1) + b];
+        D[static_cast<long long>(k0 + a) * kd + k0 + b] = -acc;
+      }
+    }
     PROF_MARK(4);
   }
+  __syncthreads();
   PROF_FLUSH(32);
 }
 
@@ -456,7 +358,7 @@ __global__ void __launch_bounds__(kFT, 1)
     k_line_factor(const SubInfo* __restrict__ subs, const double* __restrict__ coef, size_t N,
                   int W, int nc, double* __restrict__ fac, double* __restrict__ scratch,
                   long long scratch_stride, int kdp, int mid, int* __restrict__ bad,
-                  const int2* __restrict__ changed) {
+                  const int2* __restrict__ changed, int la) {
   const int sub = mid ? blockIdx.x : blockIdx.x >> 1;
   const int chain = mid ? 0 : blockIdx.x & 1;
   const SubInfo s = subs[sub];
@@ -471,17 +373,17 @@ __global__ void __launch_bounds__(kFT, 1)
   double* F = fac + s.fac_off;
   extern __shared__ __align__(16) double fsm[];
   double* P = fsm;                    // NB x (NB+1)
-  double* Li = P + NB * (NB + 1);     // NB x (NB+1)
-  double* pan = Li + NB * (NB + 1);   // 4 x NB
-  double* dinv4 = pan + 4 * NB;       // NB/4 x 16
-  double* Z = dinv4 + 4 * NB;         // NB x kdp
+  double* Li = P + NB * (NB + 1);     // 2 x NB x (NB+1)
+  double* ir = Li + 2 * NB * (NB + 1);  // NB
+  int* cnt = reinterpret_cast<int*>(ir + NB);
+  double* Z = ir + 2 * NB;            // NB x kdp
   for (int e = tid; e < NB * kdp; e += kFT) Z[e] = 0.0;
   int first_bad = 0x7fffffff;
   PROF_DECL
   if (mid) {
     build_line(s, coef, N, W, nc, m, m > 0 ? m - 1 : -1, m, m < L - 1 ? m + 1 : -1, m + 1, F, D);
     PROF_MARK(0);
-    sweep_invert<NB>(D, kd, kdp, fsm, Li, pan, dinv4, Z, first_bad, m * kd);
+    sweep_invert<NB>(D, kd, kdp, P, Li, ir, cnt, Z, first_bad, m * kd, la);
     pack_line(s, m, D, F);
   } else {
     const int nlines = chain == 0 ? m : L - 1 - m;
@@ -492,7 +394,7 @@ __global__ void __launch_bounds__(kFT, 1)
       const int bl = chain == 0 ? l : l + 1;  // coupling between l and prev
       build_line(s, coef, N, W, nc, l, prev, bl, -1, 0, F, D);
       PROF_MARK(0);
-      sweep_invert<NB>(D, kd, kdp, fsm, Li, pan, dinv4, Z, first_bad, l * kd);
+      sweep_invert<NB>(D, kd, kdp, P, Li, ir, cnt, Z, first_bad, l * kd, la);
       pack_line(s, l, D, F);
       PROF_MARK(5);
     }
@@ -1138,7 +1040,11 @@ void line_factor(const SubInfo* d_subs, int nsub, int /*C*/, int nb, int kd_max,
                  const double* coef, size_t N, int W, int nc, double* fac, double* scratch,
                  long long scratch_stride, int* d_bad, cudaStream_t st, const int2* changed) {
   const int kdp = (kd_max + 31) / 32 * 32;
-  const size_t smem = (2 * nb * (nb + 1) + 8 * nb + static_cast<size_t>(nb) * kdp) * sizeof(double);
+  static const int la = [] {
+    const char* e = std::getenv("FFB_LOOKAHEAD");
+    return e ? std::atoi(e) : 1;
+  }();
+  const size_t smem = (3 * nb * (nb + 1) + 2 * nb + static_cast<size_t>(nb) * kdp) * sizeof(double);
   if (smem > 227 * 1024) fail("linsolve.cholesky: subdomain line too wide for shared memory");
   for (int mid = 0; mid <= 1; ++mid) {
     const int grid = mid ? nsub : 2 * nsub;
@@ -1146,12 +1052,12 @@ void line_factor(const SubInfo* d_subs, int nsub, int /*C*/, int nb, int kd_max,
       FFB_CUDA(cudaFuncSetAttribute(k_line_factor<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
       k_line_factor<32><<<grid, kFT, smem, st>>>(d_subs, coef, N, W, nc, fac, scratch,
-                                                 scratch_stride, kdp, mid, d_bad, changed);
+                                                 scratch_stride, kdp, mid, d_bad, changed, la);
     } else if (nb == 16) {
       FFB_CUDA(cudaFuncSetAttribute(k_line_factor<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
       k_line_factor<16><<<grid, kFT, smem, st>>>(d_subs, coef, N, W, nc, fac, scratch,
-                                                 scratch_stride, kdp, mid, d_bad, changed);
+                                                 scratch_stride, kdp, mid, d_bad, changed, la);
     } else {
       fail("internal: unsupported pivot block size");
     }

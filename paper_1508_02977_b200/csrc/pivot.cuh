@@ -1,0 +1,74 @@
+// Pivot block of the factor kernel's blocked symmetric sweep (band.cu, K5): the Cholesky
+// factor L of the nbk x nbk diagonal block A_KK and its inverse Li = L^-1, by one warp.
+//
+// Lane j owns column j in registers. The columns rotate down one row per elimination step
+// (c[t] holds row k + t at step k), so every register index is static while the k loop stays
+// rolled — a few hundred instructions, which matters because the pivot runs beside the other
+// warps' work once per sweep step and must not evict their code. Column k of L is broadcast
+// through shared memory, stored rotated (LR[k][t] = L[k + t][k]) so that every lane reads it
+// with aligned 16-byte broadcast loads; shuffles would cost two SHFL per double on the
+// (shared) MIO pipe. The forward substitution for Li reuses the same rows.
+#pragma once
+
+namespace ffb {
+
+template <int NB>
+__device__ __noinline__ void pivot_warp(const double* __restrict__ D, int kd, int k0, int nbk,
+                                        double* LR, double* Li, double* ir, int& first_bad,
+                                        int bad_base) {
+  static_assert(NB % 2 == 0 && NB <= 32, "pivot block");
+  const int lane = threadIdx.x & 31;
+  double c[NB];
+#pragma unroll
+  for (int t = 0; t < NB; ++t) {
+    const int a = max(t, lane), b = min(t, lane);
+    c[t] = (lane < nbk && t < nbk) ? D[static_cast<long long>(k0 + a) * kd + k0 + b]
+                                   : (t == lane ? 1.0 : 0.0);
+  }
+  int fb = first_bad;
+#pragma unroll 1
+  for (int k = 0; k < NB; ++k) {
+    double dkk = __shfl_sync(~0u, c[0], k);
+    if (!(dkk > 0.0) || !isfinite(dkk)) {
+      if (k < nbk) fb = min(fb, bad_base + k0 + k);
+      dkk = 1.0;
+    }
+    const double r = rsqrt(dkk);
+    const double l = (lane == k) ? dkk * r : c[0] * r;  // L[lane][k] for lane >= k
+    double* row = LR + k * NB;                           // row[t] = L[k + t][k]
+    if (lane >= k && lane < NB) row[lane - k] = l;
+    if (lane == k) ir[k] = r;
+    __syncwarp();
+    // trailing update of column `lane`, rotated: c[t-1] = c[t] - L[k+t][k] L[lane][k]
+    // (rows k + t >= NB read stale entries of `row`: they only ever feed rows >= NB)
+    c[0] = c[1] - row[1] * l;
+#pragma unroll
+    for (int t = 2; t < NB; t += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(row + t);
+      c[t - 1] = c[t] - v.x * l;
+      c[t] = c[t + 1] - v.y * l;
+    }
+    c[NB - 1] = 0.0;
+  }
+  first_bad = fb;
+  // column `lane` of L^-1: y_k = cur_k / L[k][k], cur_i -= L[i][k] y_k (i > k), rotated
+#pragma unroll
+  for (int t = 0; t < NB; ++t) c[t] = (t == lane) ? 1.0 : 0.0;
+#pragma unroll 1
+  for (int k = 0; k < NB; ++k) {
+    const double y = c[0] * ir[k];
+    if (lane < NB) Li[k * (NB + 1) + lane] = y;
+    const double* row = LR + k * NB;
+    c[0] = c[1] - row[1] * y;
+#pragma unroll
+    for (int t = 2; t < NB; t += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(row + t);
+      c[t - 1] = c[t] - v.x * y;
+      c[t] = c[t + 1] - v.y * y;
+    }
+    c[NB - 1] = 0.0;
+  }
+  __syncwarp();
+}
+
+}  // namespace ffb
