@@ -112,6 +112,31 @@ long ffb_build_partition(int W, int H, int px, int py, int ov, int* buf, long ca
 /* assign_workers (schwarz.hpp:56, schwarz.cpp:46-52) */
 int ffb_assign_workers(int n_workers, int n_parts, int* out);
 
+/* ---- linsolve boundary: include/flowfem/linsolve.hpp ---------------
+ * An explicit SparseSystem in CSR form (assembly.hpp:43-53): n scalar unknowns, both
+ * triangles stored, row_ptr[n+1] / cols[nnz] / vals[nnz], free vertex major, component minor.
+ * Host buffers in and out; the arithmetic runs on the device. */
+#define FFB_SOLVE_CHOLESKY 0 /* SolveMethod::DirectCholesky (linsolve.hpp:10) */
+#define FFB_SOLVE_CG 1       /* SolveMethod::ConjugateGradient */
+/* y = A x in CSR order (spmv, assembly.hpp:76, assembly.cpp:240-249); bitwise */
+int ffb_csr_spmv(ffb_ctx* ctx, int n, const int* row_ptr, const int* cols, const double* vals,
+                 const double* x, double* y);
+/* rcm_order (linsolve.hpp:22-24, linsolve.cpp:37-83): perm[new] = old; bit-exact */
+int ffb_rcm_order(int n, int components, const int* row_ptr, const int* cols, int* perm);
+/* cg_solve (linsolve.hpp:53-56, linsolve.cpp:298-361): Jacobi-PCG, det_dot reductions,
+ * true-residual stop at tol, max_iters 0 -> 10 n, optional warm start; bitwise equal to the
+ * reference's iterates, iteration count and residual. Errors: "linsolve.cg: ..." */
+int ffb_csr_cg_solve(ffb_ctx* ctx, int n, const int* row_ptr, const int* cols,
+                     const double* vals, const double* rhs, double tol, int max_iters,
+                     const double* warm, double* x, int* iters, double* res);
+/* solve (linsolve.hpp:58-62, linsolve.cpp:363-399): zero right-hand side -> zero vector;
+ * FFB_SOLVE_CG -> cg_solve; FFB_SOLVE_CHOLESKY -> band Cholesky of the RCM-ordered matrix
+ * on the device, one step of iterative refinement, res = ||b - A x|| / ||b||.
+ * Errors: "linsolve.cholesky: breakdown at pivot k (unknown u): ..." */
+int ffb_csr_solve(ffb_ctx* ctx, int n, int components, const int* row_ptr, const int* cols,
+                  const double* vals, const double* rhs, int method, double tol, int max_iters,
+                  const double* warm, double* x, int* iters, double* res);
+
 /* ---- operator: include/flowfem/assembly.hpp --------------------------------------- */
 /* y = A x and b of the unconstrained global system: assemble (assembly.hpp:59-61,
  * assembly.cpp:32-166) followed by spmv (assembly.hpp:76, assembly.cpp:240-249), computed

@@ -592,6 +592,154 @@ int fp_cg_solve(int W, int H, const double* t10, const double* alpha, const doub
   return rc;
 }
 
+/* ------------------------------------------------------------- CSR path */
+
+/* y = A x, row-sequential sums in CSR order (spmv, assembly.cpp:240-249) */
+int fp_csr_spmv(int n, const int* row_ptr, const int* cols, const double* vals, const double* x,
+                double* y) {
+#pragma omp parallel for schedule(static)
+  for (int r = 0; r < n; ++r) {
+    double s = 0.0;
+    for (int q = row_ptr[r]; q < row_ptr[r + 1]; ++q) s += vals[q] * x[cols[q]];
+    y[r] = s;
+  }
+  return 0;
+}
+
+/* Jacobi PCG on an explicit CSR system (cg_solve, linsolve.cpp:298-361): diagonal = last
+ * stored entry of column r in row r, det_dot chunks, true-residual stop, warm start */
+int fp_csr_cg_solve(int n, const int* row_ptr, const int* cols, const double* vals,
+                    const double* b, double tol, int max_iters_cfg, const double* warm,
+                    double* x, int* iters_out, double* res_out) {
+  double* diag = (double*)malloc((n ? n : 1) * sizeof(double));
+  double* r = (double*)malloc((n ? n : 1) * sizeof(double));
+  double* z = (double*)malloc((n ? n : 1) * sizeof(double));
+  double* p = (double*)malloc((n ? n : 1) * sizeof(double));
+  double* Ap = (double*)malloc((n ? n : 1) * sizeof(double));
+  int rc = 0;
+  for (int i = 0; i < n; ++i) {
+    double d = 0.0;
+    for (int q = row_ptr[i]; q < row_ptr[i + 1]; ++q)
+      if (cols[q] == i) d = vals[q];
+    diag[i] = d;
+  }
+  for (int i = 0; i < n; ++i)
+    if (!(diag[i] > 0.0)) {
+      rc = fail("linsolve.cg: non-positive diagonal at row %d", i);
+      goto out;
+    }
+  {
+    const double normb = sqrt(det_dot(b, b, n));
+    if (warm)
+      memcpy(x, warm, n * sizeof(double));
+    else
+      memset(x, 0, n * sizeof(double));
+    if (normb == 0.0) {
+      memset(x, 0, n * sizeof(double));
+      if (iters_out) *iters_out = 0;
+      if (res_out) *res_out = 0.0;
+      goto out;
+    }
+    fp_csr_spmv(n, row_ptr, cols, vals, x, Ap);
+    for (int i = 0; i < n; ++i) {
+      r[i] = b[i] - Ap[i];
+      z[i] = r[i] / diag[i];
+      p[i] = z[i];
+    }
+    double rz = det_dot(r, z, n);
+    double res = sqrt(det_dot(r, r, n)) / normb;
+    const long max_iters = max_iters_cfg > 0 ? max_iters_cfg : 10L * n;
+    long it = 0;
+    while (res > tol && it < max_iters) {
+      ++it;
+      fp_csr_spmv(n, row_ptr, cols, vals, p, Ap);
+      const double pAp = det_dot(p, Ap, n);
+      if (pAp <= 0.0) {
+        rc = fail("linsolve.cg: indefinite matrix detected at iteration %ld", it);
+        goto out;
+      }
+      const double alpha = rz / pAp;
+      for (int i = 0; i < n; ++i) {
+        x[i] += alpha * p[i];
+        r[i] -= alpha * Ap[i];
+      }
+      res = sqrt(det_dot(r, r, n)) / normb;
+      if (res <= tol) break;
+      for (int i = 0; i < n; ++i) z[i] = r[i] / diag[i];
+      const double rz_new = det_dot(r, z, n);
+      const double beta = rz_new / rz;
+      rz = rz_new;
+      for (int i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+    }
+    if (iters_out) *iters_out = (int)it;
+    if (res_out) *res_out = res;
+    if (res > tol)
+      rc = fail("linsolve.cg: no convergence after %ld iterations, relative residual %f", it, res);
+  }
+out:
+  free(diag), free(r), free(z), free(p), free(Ap);
+  return rc;
+}
+
+/* RCM of the free-vertex graph expanded to scalar unknowns (rcm_order, linsolve.cpp:37-83):
+ * block adjacency from each vertex's first-component row (:20-33), start = unvisited vertex
+ * of minimum degree (smallest id on ties), BFS with neighbours by (degree, id), reversed */
+static const int* g_rcm_degree;
+static int rcm_cmp(const void* pa, const void* pb) {
+  const int a = *(const int*)pa, b = *(const int*)pb;
+  if (g_rcm_degree[a] != g_rcm_degree[b]) return g_rcm_degree[a] < g_rcm_degree[b] ? -1 : 1;
+  return a < b ? -1 : (a > b ? 1 : 0);
+}
+
+int fp_rcm_order(int n, int nc, const int* row_ptr, const int* cols, int* perm) {
+  if (nc <= 0 || n % nc != 0) return fail("linsolve.rcm_order: system size not a multiple of components");
+  const int nb = n / nc;
+  int* adj_ptr = (int*)calloc(nb + 1, sizeof(int));
+  int* adj = (int*)malloc(((size_t)row_ptr[n] + 1) * sizeof(int));
+  for (int b = 0; b < nb; ++b) {
+    const int row = b * nc;
+    int last = -1, cnt = 0;
+    adj_ptr[b + 1] = adj_ptr[b];
+    for (int q = row_ptr[row]; q < row_ptr[row + 1]; ++q) {
+      const int k = cols[q] / nc;
+      if (k != b && k != last) adj[adj_ptr[b] + cnt++] = k;
+      last = k;
+    }
+    adj_ptr[b + 1] = adj_ptr[b] + cnt;
+  }
+  int* degree = (int*)malloc((nb ? nb : 1) * sizeof(int));
+  for (int b = 0; b < nb; ++b) degree[b] = adj_ptr[b + 1] - adj_ptr[b];
+  char* visited = (char*)calloc(nb ? nb : 1, 1);
+  int* order = (int*)malloc((nb ? nb : 1) * sizeof(int));
+  int* nbrs = (int*)malloc((nb ? nb : 1) * sizeof(int));
+  int norder = 0, scanned = 0;
+  g_rcm_degree = degree;
+  while (norder < nb) {
+    int start = -1;
+    for (int b = scanned; b < nb; ++b)
+      if (!visited[b] && (start < 0 || degree[b] < degree[start])) start = b;
+    while (scanned < nb && visited[scanned]) ++scanned;
+    visited[start] = 1;
+    int head = norder;
+    order[norder++] = start;
+    while (head < norder) {
+      const int v = order[head++];
+      int m = 0;
+      for (int q = adj_ptr[v]; q < adj_ptr[v + 1]; ++q)
+        if (!visited[adj[q]]) nbrs[m++] = adj[q];
+      qsort(nbrs, m, sizeof(int), rcm_cmp);
+      for (int i = 0; i < m; ++i) {
+        visited[nbrs[i]] = 1;
+        order[norder++] = nbrs[i];
+      }
+    }
+  }
+  for (int i = 0; i < nb; ++i)
+    for (int c = 0; c < nc; ++c) perm[i * nc + c] = order[nb - 1 - i] * nc + c;
+  free(adj_ptr), free(adj), free(degree), free(visited), free(order), free(nbrs);
+  return 0;
+}
+
 /* ---------------------------------------------------------------- adapt */
 
 /* constant P1 gradients (p1_gradients, mesh.cpp:172-186) for the two triangle

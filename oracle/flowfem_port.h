@@ -36,6 +36,12 @@ int fp_assemble_apply(int W, int H, const double* t10, const double* alpha,
 int fp_cg_solve(int W, int H, const double* t10, const double* alpha, const double* lambda,
                 int nc, double tol, int max_iters, const double* warm3, double* out3,
                 int* iters, double* res);
+int fp_csr_spmv(int n, const int* row_ptr, const int* cols, const double* vals, const double* x,
+                double* y);
+int fp_csr_cg_solve(int n, const int* row_ptr, const int* cols, const double* vals,
+                    const double* b, double tol, int max_iters, const double* warm, double* x,
+                    int* iters, double* res);
+int fp_rcm_order(int n, int nc, const int* row_ptr, const int* cols, int* perm);
 int fp_error_indicator(int W, int H, const double* t10, const double* alpha,
                        const double* lambda, const double* u3, int nc, double* eta,
                        double* eta_max);

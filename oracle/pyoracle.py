@@ -180,6 +180,94 @@ class Oracle:
         return dict(u3=out, alpha=alpha, eta_max=em[:n_passes], iters=iters, seconds=sec.value)
 
 
+class CsrSystem:
+    """A SparseSystem in CSR form (proj/include/flowfem/assembly.hpp:43-53): both triangles
+    stored, free vertex major / component minor."""
+
+    def __init__(self, row_ptr, cols, vals, rhs, components=3):
+        self.row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int32)
+        self.cols = np.ascontiguousarray(cols, dtype=np.int32)
+        self.vals = _f64(vals)
+        self.rhs = _f64(rhs)
+        self.components = int(components)
+        self.n = len(self.row_ptr) - 1
+
+    def dense(self):
+        A = np.zeros((self.n, self.n))
+        for r in range(self.n):
+            for q in range(self.row_ptr[r], self.row_ptr[r + 1]):
+                A[r, self.cols[q]] = self.vals[q]
+        return A
+
+
+def ref_assemble_system(terms, alpha, lam, nc=3, dir_vertices=None, dir_values=None):
+    """The reference's assemble() (assembly.cpp:32-166) as a CsrSystem, optionally with a
+    Dirichlet set (dir_values: len(dir_vertices) x nc)."""
+    if REF is None:
+        raise OracleError("reference oracle not built")
+    terms = _f64(terms)
+    _, H, W = terms.shape
+    alpha, lam = _f64(alpha), _f64(lam)
+    dv = np.ascontiguousarray(dir_vertices if dir_vertices is not None else [], dtype=np.int32)
+    dval = _f64(dir_values if dir_values is not None else np.zeros((0, nc)))
+    n, nnz = C.c_int(), C.c_long()
+    args = [W, H, _ptr(terms), _ptr(alpha), _ptr(lam), nc, len(dv), _ptr(dv), _ptr(dval)]
+    REF._call("assemble_system", *args, C.byref(n), C.byref(nnz), None, None, None, None)
+    rp = np.zeros(n.value + 1, dtype=np.int32)
+    cols = np.zeros(nnz.value, dtype=np.int32)
+    vals = np.zeros(nnz.value)
+    rhs = np.zeros(n.value)
+    REF._call("assemble_system", *args, C.byref(n), C.byref(nnz), _ptr(rp), _ptr(cols),
+              _ptr(vals), _ptr(rhs))
+    return CsrSystem(rp, cols, vals, rhs, nc)
+
+
+def csr_cg_solve(oracle, sys: CsrSystem, tol=1e-10, max_iters=0, warm=None):
+    """cg_solve (linsolve.cpp:298-361) of the port or the reference on a CsrSystem;
+    returns (x, iterations, residual)."""
+    x = np.zeros(sys.n)
+    it, res = C.c_int(), C.c_double()
+    w = None if warm is None else _f64(warm)
+    if oracle.prefix == "ref_":
+        oracle._call("csr_cg_solve", sys.n, sys.components, _ptr(sys.row_ptr), _ptr(sys.cols),
+                     _ptr(sys.vals), _ptr(sys.rhs), C.c_double(tol), int(max_iters), _ptr(w),
+                     _ptr(x), C.byref(it), C.byref(res))
+    else:
+        oracle._call("csr_cg_solve", sys.n, _ptr(sys.row_ptr), _ptr(sys.cols), _ptr(sys.vals),
+                     _ptr(sys.rhs), C.c_double(tol), int(max_iters), _ptr(w), _ptr(x),
+                     C.byref(it), C.byref(res))
+    return x, it.value, res.value
+
+
+def ref_csr_solve(sys: CsrSystem, method=1, tol=1e-10, max_iters=0, warm=None):
+    """The reference's solve() (linsolve.cpp:363-399); method 1 Cholesky, 0 CG."""
+    x = np.zeros(sys.n)
+    it, res = C.c_int(), C.c_double()
+    w = None if warm is None else _f64(warm)
+    REF._call("csr_solve", sys.n, sys.components, _ptr(sys.row_ptr), _ptr(sys.cols),
+              _ptr(sys.vals), _ptr(sys.rhs), int(method), C.c_double(tol), int(max_iters),
+              _ptr(w), _ptr(x), C.byref(it), C.byref(res))
+    return x, it.value, res.value
+
+
+def csr_spmv(oracle, sys: CsrSystem, x):
+    y = np.zeros(sys.n)
+    oracle._call("csr_spmv", sys.n, _ptr(sys.row_ptr), _ptr(sys.cols), _ptr(sys.vals),
+                 _ptr(_f64(x)), _ptr(y))
+    return y
+
+
+def rcm_order(oracle, sys: CsrSystem):
+    perm = np.zeros(sys.n, dtype=np.int32)
+    if oracle.prefix == "ref_":
+        oracle._call("rcm_order", sys.n, sys.components, _ptr(sys.row_ptr), _ptr(sys.cols),
+                     _ptr(perm))
+    else:
+        oracle._call("rcm_order", sys.n, sys.components, _ptr(sys.row_ptr), _ptr(sys.cols),
+                     _ptr(perm))
+    return perm
+
+
 def _load(sub, name, prefix, kind):
     p = os.path.join(HERE, sub, name)
     return Oracle(p, prefix, kind) if os.path.exists(p) else None

@@ -259,6 +259,107 @@ int ref_solve_monolithic(int W, int H, const double* t10, const double* alpha,
   });
 }
 
+// ----------------------------------------------------------------- CSR linsolve boundary
+// The reference's SparseSystem from assemble() (optional Dirichlet set: n_dir vertices,
+// nc values each). Call with row_ptr == nullptr to get n and nnz, then with arrays sized
+// n+1 / nnz / nnz / n.
+int ref_assemble_system(int W, int H, const double* t10, const double* alpha,
+                        const double* lambda, int nc, int n_dir, const int* dir_vertices,
+                        const double* dir_values, int* n_out, long* nnz_out, int* row_ptr,
+                        int* cols, double* vals, double* rhs) {
+  return guard([&] {
+    const TriMesh m = build_pixel_mesh(W, H);
+    const DataTerms dt = to_terms(W, H, t10);
+    const RegField reg = to_reg(m.n_triangles, alpha, lambda);
+    DirichletSet ds;
+    for (int k = 0; k < n_dir; ++k) {
+      ds.vertices.push_back(dir_vertices[k]);
+      for (int c = 0; c < nc; ++c) ds.values.push_back(dir_values[k * nc + c]);
+    }
+    const SparseSystem sys = assemble(m, dt, reg, nc, n_dir > 0 ? &ds : nullptr);
+    *n_out = sys.n;
+    *nnz_out = static_cast<long>(sys.cols.size());
+    if (!row_ptr) return;
+    std::copy(sys.row_ptr.begin(), sys.row_ptr.end(), row_ptr);
+    std::copy(sys.cols.begin(), sys.cols.end(), cols);
+    std::copy(sys.vals.begin(), sys.vals.end(), vals);
+    std::copy(sys.rhs.begin(), sys.rhs.end(), rhs);
+  });
+}
+
+namespace {
+SparseSystem csr_system(int n, int nc, const int* row_ptr, const int* cols, const double* vals,
+                        const double* rhs) {
+  SparseSystem sys;
+  sys.n = n;
+  sys.components = nc;
+  sys.row_ptr.assign(row_ptr, row_ptr + n + 1);
+  sys.cols.assign(cols, cols + row_ptr[n]);
+  sys.vals.assign(vals, vals + row_ptr[n]);
+  if (rhs) sys.rhs.assign(rhs, rhs + n);
+  return sys;
+}
+}  // namespace
+
+// solve() (linsolve.cpp:363-399) on an explicit CSR system; method 0 CG, 1 Cholesky
+int ref_csr_solve(int n, int nc, const int* row_ptr, const int* cols, const double* vals,
+                  const double* rhs, int method, double tol, int max_iters, const double* warm,
+                  double* x, int* iters, double* res) {
+  return guard([&] {
+    const SparseSystem sys = csr_system(n, nc, row_ptr, cols, vals, rhs);
+    SolverConfig cfg;
+    cfg.method = method == 1 ? SolveMethod::DirectCholesky : SolveMethod::ConjugateGradient;
+    cfg.cg_tolerance = tol;
+    cfg.cg_max_iters = max_iters;
+    std::vector<double> w;
+    if (warm) w.assign(warm, warm + n);
+    SolveReport rep;
+    const std::vector<double> out = solve(sys, cfg, &rep, warm ? &w : nullptr);
+    std::copy(out.begin(), out.end(), x);
+    if (iters) *iters = rep.iterations;
+    if (res) *res = rep.residual;
+  });
+}
+
+// cg_solve (linsolve.cpp:298-361) itself (no zero-rhs shortcut of solve())
+int ref_csr_cg_solve(int n, int nc, const int* row_ptr, const int* cols, const double* vals,
+                     const double* rhs, double tol, int max_iters, const double* warm,
+                     double* x, int* iters, double* res) {
+  return guard([&] {
+    const SparseSystem sys = csr_system(n, nc, row_ptr, cols, vals, rhs);
+    SolverConfig cfg;
+    cfg.method = SolveMethod::ConjugateGradient;
+    cfg.cg_tolerance = tol;
+    cfg.cg_max_iters = max_iters;
+    std::vector<double> w;
+    if (warm) w.assign(warm, warm + n);
+    SolveReport rep;
+    const std::vector<double> out = cg_solve(sys, cfg, warm ? &w : nullptr, &rep);
+    std::copy(out.begin(), out.end(), x);
+    if (iters) *iters = rep.iterations;
+    if (res) *res = rep.residual;
+  });
+}
+
+int ref_csr_spmv(int n, const int* row_ptr, const int* cols, const double* vals,
+                 const double* x, double* y) {
+  return guard([&] {
+    const SparseSystem sys = csr_system(n, 1, row_ptr, cols, vals, nullptr);
+    std::vector<double> xv(x, x + n), yv;
+    spmv(sys, xv, yv);
+    std::copy(yv.begin(), yv.end(), y);
+  });
+}
+
+int ref_rcm_order(int n, int nc, const int* row_ptr, const int* cols, int* perm) {
+  return guard([&] {
+    std::vector<double> vals(row_ptr[n], 0.0);
+    const SparseSystem sys = csr_system(n, nc, row_ptr, cols, vals.data(), nullptr);
+    const std::vector<int> p = rcm_order(sys);
+    std::copy(p.begin(), p.end(), perm);
+  });
+}
+
 int ref_error_indicator(int W, int H, const double* t10, const double* alpha,
                         const double* lambda, const double* u3, int nc, double* eta,
                         double* eta_max) {

@@ -11,7 +11,8 @@ from .flowfem import (AdaptConfig, Context, DataTerms, DerivativeField, FlowfemE
                       build_data_terms, build_partition, choose_split, compute_derivatives,
                       default_context, enumerate_splits, error_indicator, frames_to_terms,
                       gaussian_smooth, kernel_launches, run_on_frames, run_on_frames_device,
-                      schwarz_solve,
+                      schwarz_solve, SolveMethod, SolverConfig, SolveReport, SparseSystem,
+                      spmv, rcm_order, cg_solve, solve,
                       uniform_reg, update_alpha)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

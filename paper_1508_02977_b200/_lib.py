@@ -51,6 +51,10 @@ SIGNATURES = {
     "ffb_frames_to_terms": (_i, [_vp, _i, _i, _vp, _vp, _d, _d, _vp]),
     "ffb_enumerate_splits": (_i, [_i, _i, _i, _vp, _vp, _vp, _i]),
     "ffb_choose_split": (_i, [_i, _i, _i, _vp, _vp, _vp]),
+    "ffb_csr_spmv": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp]),
+    "ffb_rcm_order": (_i, [_i, _i, _vp, _vp, _vp]),
+    "ffb_csr_cg_solve": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp]),
+    "ffb_csr_solve": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _i, _d, _i, _vp, _vp, _vp, _vp]),
     "ffb_build_partition": (C.c_long, [_i, _i, _i, _i, _i, _vp, C.c_long]),
     "ffb_assign_workers": (_i, [_i, _i, _vp]),
     "ffb_assemble_apply": (_i, [_vp, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp]),

@@ -30,8 +30,9 @@ CU = {
     "band.cu": ["-Xptxas", "-v"] if os.environ.get("FFB_PTXAS_V") else [],
     "pcg.cu": [],
     "ras.cu": ["--fmad=false"],
+    "linsolve.cu": ["--fmad=false"],
 }
-CPP = ["capi.cpp", "partition.cpp"]
+CPP = ["capi.cpp", "partition.cpp", "rcm.cpp"]
 HEADERS = ["ffb_internal.cuh", "partition.hpp"]
 
 

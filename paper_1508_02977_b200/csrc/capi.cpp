@@ -113,6 +113,10 @@ struct ffb_ctx {
   DBuf<AxisMap> d_col, d_row;
   DBuf<double> fac, dscratch, ylocal, zlocal, rlocal, xlocal, G0, G1, incs;
   DBuf<int> own_col, own_row;
+  // linsolve boundary on an explicit CSR system (ffb_csr_*)
+  DBuf<int> csr_rp, csr_ci, csr_perm, csr_iperm, csr_bad;
+  DBuf<double> csr_v, csr_b, csr_x, csr_r, csr_z, csr_p, csr_Ap, csr_diag, csr_part, csr_AB;
+  DBuf<CgCtl> cgctl;
   DBuf<double> alpha_fact;  // alpha of the resident factorisation (incremental refactor)
   DBuf<int2> d_changed;
   long long fact_key_t_full = -1;  // terms version / partition of the last full factorisation
@@ -1132,6 +1136,197 @@ int ffb_run_on_frames_dev(ffb_ctx* c, int W, int H, const double* d_f0, const do
   return guard([&] {
     check_ctx(c);
     run_dev(c, W, H, d_f0, d_f1, cfg, d_u3, stats);
+  });
+}
+
+/* ---- linsolve boundary on an explicit CSR SparseSystem (linsolve.hpp:26-62) ---------- */
+}  // extern "C"
+
+namespace {
+
+CsrDev upload_csr(ffb_ctx* c, int n, const int* row_ptr, const int* cols, const double* vals) {
+  if (n < 0) fail("linsolve: negative system size");
+  if (n > 0 && (!row_ptr || !cols || !vals)) fail("linsolve: null CSR array");
+  const long long nnz = n > 0 ? row_ptr[n] : 0;
+  int* rp = c->csr_rp.ensure(n + 1);
+  int* ci = c->csr_ci.ensure(nnz);
+  double* v = c->csr_v.ensure(nnz);
+  FFB_CUDA(cudaMemcpyAsync(rp, row_ptr, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, c->st));
+  if (nnz) {
+    FFB_CUDA(cudaMemcpyAsync(ci, cols, nnz * sizeof(int), cudaMemcpyHostToDevice, c->st));
+    upload(v, vals, nnz, c->st);
+  }
+  return CsrDev{n, rp, ci, v};
+}
+
+// cg_solve (linsolve.cpp:298-361) on the device, bit for bit; b, x device vectors of A.n
+void run_cg(ffb_ctx* c, const CsrDev& A, const double* b, const double* warm_h, double tol,
+            int max_iters, double* x, int* iters, double* res) {
+  const int n = A.n;
+  double* diag = c->csr_diag.ensure(n);
+  int* bad = c->csr_bad.ensure(1);
+  FFB_CUDA(cudaMemsetAsync(bad, 0x7f, sizeof(int), c->st));
+  csr_diag(A, diag, bad, c->st);
+  int bad_h = 0;
+  FFB_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  if (bad_h != 0x7f7f7f7f) fail("linsolve.cg: non-positive diagonal at row " + std::to_string(bad_h));
+  CgCtl h{};
+  h.tol = tol;
+  h.max_iters = max_iters > 0 ? max_iters : 10LL * n;
+  CgCtl* ctl = c->cgctl.ensure(1);
+  FFB_CUDA(cudaMemcpyAsync(ctl, &h, sizeof(CgCtl), cudaMemcpyHostToDevice, c->st));
+  double* part = c->csr_part.ensure(dot_chunks(n));
+  double *r = c->csr_r.ensure(n), *z = c->csr_z.ensure(n), *p = c->csr_p.ensure(n),
+         *Ap = c->csr_Ap.ensure(n);
+  det_dot(b, b, n, part, ctl, c->st);
+  cg_scalar(part, n, cg_stage_normb(), ctl, c->st);
+  if (warm_h)
+    upload(x, warm_h, n, c->st);
+  else
+    FFB_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), c->st));
+  csr_spmv(A, x, Ap, ctl, c->st);
+  cg_init(n, b, Ap, diag, r, z, p, ctl, c->st);
+  det_dot(r, z, n, part, ctl, c->st);
+  cg_scalar(part, n, cg_stage_init_rz(), ctl, c->st);
+  det_dot(r, r, n, part, ctl, c->st);
+  cg_scalar(part, n, cg_stage_init_res(), ctl, c->st);
+  for (;;) {
+    FFB_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(CgCtl), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    if (h.done) break;
+    for (int k = 0; k < 16; ++k) cg_iteration(A, x, r, z, p, Ap, diag, part, ctl, c->st);
+  }
+  if (h.zero) {
+    FFB_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), c->st));
+    h.it = 0, h.res = 0.0;
+  }
+  if (iters) *iters = static_cast<int>(h.it);
+  if (res) *res = h.res;
+  if (h.err == 2)
+    fail("linsolve.cg: indefinite matrix detected at iteration " + std::to_string(h.it));
+  if (!h.zero && h.res > tol)
+    fail("linsolve.cg: no convergence after " + std::to_string(h.it) +
+         " iterations, relative residual " + std::to_string(h.res));
+}
+
+}  // namespace
+
+extern "C" {
+
+int ffb_csr_spmv(ffb_ctx* c, int n, const int* row_ptr, const int* cols, const double* vals,
+                 const double* x, double* y) {
+  return guard([&] {
+    check_ctx(c);
+    const CsrDev A = upload_csr(c, n, row_ptr, cols, vals);
+    if (n == 0) return;
+    double* xd = c->csr_x.ensure(n);
+    double* yd = c->csr_r.ensure(n);
+    upload(xd, x, n, c->st);
+    csr_spmv(A, xd, yd, nullptr, c->st);
+    download(y, yd, n, c->st);
+    sync(c);
+  });
+}
+
+int ffb_rcm_order(int n, int components, const int* row_ptr, const int* cols, int* perm) {
+  return guard([&] {
+    if (n < 0 || !row_ptr || (n > 0 && (!cols || !perm))) fail("linsolve.rcm_order: bad arguments");
+    const std::vector<int> p = rcm_order(n, components, row_ptr, cols);
+    std::copy(p.begin(), p.end(), perm);
+  });
+}
+
+int ffb_csr_cg_solve(ffb_ctx* c, int n, const int* row_ptr, const int* cols, const double* vals,
+                     const double* rhs, double tol, int max_iters, const double* warm, double* x,
+                     int* iters, double* res) {
+  return guard([&] {
+    check_ctx(c);
+    const CsrDev A = upload_csr(c, n, row_ptr, cols, vals);
+    if (n == 0) {
+      if (iters) *iters = 0;
+      if (res) *res = 0.0;
+      return;
+    }
+    double* b = c->csr_b.ensure(n);
+    double* xd = c->csr_x.ensure(n);
+    upload(b, rhs, n, c->st);
+    run_cg(c, A, b, warm, tol, max_iters, xd, iters, res);
+    download(x, xd, n, c->st);
+    sync(c);
+  });
+}
+
+int ffb_csr_solve(ffb_ctx* c, int n, int components, const int* row_ptr, const int* cols,
+                  const double* vals, const double* rhs, int method, double tol, int max_iters,
+                  const double* warm, double* x, int* iters, double* res) {
+  return guard([&] {
+    check_ctx(c);
+    if (method != FFB_SOLVE_CHOLESKY && method != FFB_SOLVE_CG) fail("linsolve.solve: unknown method");
+    bool all_zero = true;
+    for (int i = 0; i < n && all_zero; ++i) all_zero = rhs[i] == 0.0;
+    if (all_zero) {  // linsolve.cpp:365-372
+      std::fill(x, x + n, 0.0);
+      if (iters) *iters = 0;
+      if (res) *res = 0.0;
+      return;
+    }
+    const CsrDev A = upload_csr(c, n, row_ptr, cols, vals);
+    double* b = c->csr_b.ensure(n);
+    double* xd = c->csr_x.ensure(n);
+    upload(b, rhs, n, c->st);
+    if (method == FFB_SOLVE_CG) {
+      run_cg(c, A, b, warm, tol, max_iters, xd, iters, res);
+      download(x, xd, n, c->st);
+      sync(c);
+      return;
+    }
+    // direct: RCM (bit-exact with the reference's analyse) -> band Cholesky -> solve,
+    // one refinement step, residual report (linsolve.cpp:377-397)
+    const std::vector<int> perm = rcm_order(n, components, row_ptr, cols);
+    std::vector<int> iperm(n);
+    for (int k = 0; k < n; ++k) iperm[perm[k]] = k;
+    int bw = 0;
+    for (int r = 0; r < n; ++r)
+      for (int q = row_ptr[r]; q < row_ptr[r + 1]; ++q)
+        bw = std::max(bw, std::abs(iperm[r] - iperm[cols[q]]));
+    int* dperm = c->csr_perm.ensure(n);
+    int* diperm = c->csr_iperm.ensure(n);
+    FFB_CUDA(cudaMemcpyAsync(dperm, perm.data(), n * sizeof(int), cudaMemcpyHostToDevice, c->st));
+    FFB_CUDA(cudaMemcpyAsync(diperm, iperm.data(), n * sizeof(int), cudaMemcpyHostToDevice, c->st));
+    const size_t nab = static_cast<size_t>(n) * (bw + 1);
+    double* AB = c->csr_AB.ensure(nab);
+    FFB_CUDA(cudaMemsetAsync(AB, 0, nab * sizeof(double), c->st));
+    band_scatter(A, diperm, bw, AB, c->st);
+    int* bad = c->csr_bad.ensure(1);
+    FFB_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(int), c->st));
+    band_cholesky(n, bw, AB, bad, c->st);
+    int bad_h = -1;
+    FFB_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    if (bad_h >= 0)
+      fail("linsolve.cholesky: breakdown at pivot " + std::to_string(bad_h) + " (unknown " +
+           std::to_string(perm[bad_h]) + "): matrix is not positive definite");
+    double* t = c->csr_z.ensure(n);
+    double* Ax = c->csr_Ap.ensure(n);
+    double* r = c->csr_r.ensure(n);
+    gather(n, dperm, b, t, c->st);
+    band_solve(n, bw, AB, t, c->st);
+    scatter(n, dperm, t, xd, false, c->st);
+    csr_spmv(A, xd, Ax, nullptr, c->st);
+    vec_sub(n, b, Ax, r, c->st);
+    gather(n, dperm, r, t, c->st);
+    band_solve(n, bw, AB, t, c->st);
+    scatter(n, dperm, t, xd, true, c->st);
+    if (res) {
+      csr_spmv(A, xd, Ax, nullptr, c->st);
+      double* rep = c->csr_part.ensure(1);
+      residual_report(n, b, Ax, rep, c->st);
+      download(res, rep, 1, c->st);
+    }
+    if (iters) *iters = 0;
+    download(x, xd, n, c->st);
+    sync(c);
   });
 }
 

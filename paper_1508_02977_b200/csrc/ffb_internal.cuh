@@ -147,4 +147,38 @@ void update_alpha(double* alpha_out, const double* alpha, const double* eta,
 constexpr int kRedBlocks = 592;  // 4 x 148 SMs
 constexpr int kRedThreads = 256;
 
+// ---- linsolve boundary on an explicit CSR system (linsolve.cu) ----------------------
+struct CsrDev {
+  int n;
+  const int* rp;
+  const int* ci;
+  const double* v;
+};
+// device-side state of cg_solve (linsolve.cpp:298-361)
+struct CgCtl {
+  double tol, normb, rz, res, alpha, beta;
+  long long it, max_iters;
+  int done, zero, err;  // err 2: indefinite (pAp <= 0)
+};
+void csr_spmv(const CsrDev& A, const double* x, double* y, const CgCtl* ctl, cudaStream_t st);
+void csr_diag(const CsrDev& A, double* diag, int* bad_row, cudaStream_t st);
+int dot_chunks(long long n);
+void det_dot(const double* a, const double* b, long long n, double* partial, const CgCtl* ctl,
+             cudaStream_t st);
+void cg_scalar(const double* partial, long long n, int stage, CgCtl* ctl, cudaStream_t st);
+int cg_stage_normb();
+int cg_stage_init_rz();
+int cg_stage_init_res();
+void cg_init(int n, const double* b, const double* Ap, const double* diag, double* r, double* z,
+             double* p, const CgCtl* c, cudaStream_t st);
+void cg_iteration(const CsrDev& A, double* x, double* r, double* z, double* p, double* Ap,
+                  const double* diag, double* partial, CgCtl* c, cudaStream_t st);
+void band_scatter(const CsrDev& A, const int* iperm, int bw, double* AB, cudaStream_t st);
+void band_cholesky(int n, int bw, double* AB, int* bad, cudaStream_t st);
+void band_solve(int n, int bw, const double* AB, double* x, cudaStream_t st);
+void gather(int n, const int* idx, const double* src, double* dst, cudaStream_t st);
+void scatter(int n, const int* idx, const double* src, double* dst, bool add, cudaStream_t st);
+void vec_sub(int n, const double* b, const double* y, double* r, cudaStream_t st);
+void residual_report(int n, const double* b, const double* Ax, double* out, cudaStream_t st);
+
 }  // namespace ffb

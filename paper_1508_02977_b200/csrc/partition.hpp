@@ -35,6 +35,8 @@ struct Partition {
 
 std::vector<Split> enumerate_splits(int W, int H, int n_parts);
 Split choose_split(int W, int H, int n_parts);
+// rcm_order (linsolve.cpp:37-83) of a CSR system with nc components per vertex (rcm.cpp)
+std::vector<int> rcm_order(int n, int nc, const int* row_ptr, const int* cols);
 std::vector<int> assign_workers(int n_workers, int n_parts);
 Partition build_partition(int W, int H, int px, int py, int ov);
 std::vector<int> flatten(const Partition& P);

@@ -328,6 +328,111 @@ def assemble_apply(terms: DataTerms, reg: RegField, components: int, x: FlowStat
     return FlowState.from_planes(y3), FlowState.from_planes(b3)
 
 
+# ---------------------------------------------------------------- linsolve boundary
+class SolveMethod:
+    """linsolve.hpp:10 (enum class SolveMethod)."""
+    DirectCholesky = 0
+    ConjugateGradient = 1
+
+
+@dataclass
+class SolverConfig:
+    """linsolve.hpp:12-17."""
+    method: int = SolveMethod.DirectCholesky
+    cg_tolerance: float = 1e-10
+    cg_max_iters: int = 0
+    factor_workers: int = 1  # accepted for API parity; the factor runs on the device
+
+
+@dataclass
+class SolveReport:
+    """linsolve.hpp:19-22."""
+    iterations: int = 0
+    residual: float = 0.0
+
+
+@dataclass
+class SparseSystem:
+    """assembly.hpp:43-53: n scalar unknowns, CSR with both triangles, free vertex major /
+    component minor (the Dirichlet bookkeeping of the reference is not needed here)."""
+    row_ptr: np.ndarray
+    cols: np.ndarray
+    vals: np.ndarray
+    rhs: np.ndarray
+    components: int = 3
+
+    def __post_init__(self):
+        self.row_ptr = np.ascontiguousarray(self.row_ptr, dtype=np.int32)
+        self.cols = np.ascontiguousarray(self.cols, dtype=np.int32)
+        self.vals = _f64(self.vals)
+        self.rhs = _f64(self.rhs)
+        if len(self.rhs) != self.n:
+            raise FlowfemError("linsolve: rhs length does not match the system size")
+
+    @property
+    def n(self) -> int:
+        return len(self.row_ptr) - 1
+
+
+def _ip(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def spmv(sys: SparseSystem, x, ctx: Context | None = None) -> np.ndarray:
+    """y = A x (assembly.hpp:76, assembly.cpp:240-249), on the device, bitwise."""
+    ctx = ctx or default_context()
+    x = _f64(x)
+    y = np.zeros(sys.n)
+    _check(ctx.lib.ffb_csr_spmv(ctx.handle, sys.n, _ip(sys.row_ptr), _ip(sys.cols),
+                                _p(sys.vals), _p(x), _p(y)))
+    return y
+
+
+def rcm_order(sys: SparseSystem) -> np.ndarray:
+    """linsolve.hpp:22-24 / linsolve.cpp:37-83 (host integer work, bit-exact)."""
+    lib = _lib.load()
+    perm = np.zeros(sys.n, dtype=np.int32)
+    _check(lib.ffb_rcm_order(sys.n, sys.components, _ip(sys.row_ptr), _ip(sys.cols), _ip(perm)))
+    return perm
+
+
+def cg_solve(sys: SparseSystem, cfg: SolverConfig = SolverConfig(), warm_start=None,
+             report: SolveReport | None = None, ctx: Context | None = None) -> np.ndarray:
+    """linsolve.hpp:53-56 / linsolve.cpp:298-361 on the device (bitwise the reference's)."""
+    ctx = ctx or default_context()
+    x = np.zeros(sys.n)
+    it, res = C.c_int(), C.c_double()
+    w = _f64(warm_start) if warm_start is not None and len(warm_start) == sys.n else None
+    rc = ctx.lib.ffb_csr_cg_solve(ctx.handle, sys.n, _ip(sys.row_ptr), _ip(sys.cols),
+                                  _p(sys.vals), _p(sys.rhs), float(cfg.cg_tolerance),
+                                  int(cfg.cg_max_iters), _p(w) if w is not None else None,
+                                  _p(x), C.byref(it), C.byref(res))
+    if report is not None:
+        report.iterations, report.residual = it.value, res.value
+    _check(rc)
+    return x
+
+
+def solve(sys: SparseSystem, cfg: SolverConfig = SolverConfig(),
+          report: SolveReport | None = None, warm_start=None,
+          ctx: Context | None = None) -> np.ndarray:
+    """linsolve.hpp:58-62 / linsolve.cpp:363-399: zero rhs -> 0; CG or the direct solve
+    (band Cholesky of the RCM-ordered matrix on the device + one refinement step)."""
+    ctx = ctx or default_context()
+    x = np.zeros(sys.n)
+    it, res = C.c_int(), C.c_double()
+    w = _f64(warm_start) if warm_start is not None and len(warm_start) == sys.n else None
+    rc = ctx.lib.ffb_csr_solve(ctx.handle, sys.n, sys.components, _ip(sys.row_ptr),
+                               _ip(sys.cols), _p(sys.vals), _p(sys.rhs), int(cfg.method),
+                               float(cfg.cg_tolerance), int(cfg.cg_max_iters),
+                               _p(w) if w is not None else None, _p(x), C.byref(it),
+                               C.byref(res))
+    if report is not None:
+        report.iterations, report.residual = it.value, res.value
+    _check(rc)
+    return x
+
+
 @dataclass
 class IndicatorField:
     eta: np.ndarray

@@ -11,6 +11,11 @@ Fixtures (the reference ships no golden files):
                      eta_max, iterations
   partitions.json    SHA-256 of the reference's flat Partition for every configured split
                      plus the split choices
+  linsolve.npz       the linsolve boundary: SparseSystems from the
+                     reference's assemble() (random frames/alpha, optional Dirichlet row,
+                     as test_linsolve.cpp:16-33 builds them), the reference's rcm_order,
+                     cg_solve (x, iterations, residual) and direct solve() on each, and
+                     the outcome on an indefinite system
 """
 import hashlib
 import json
@@ -77,11 +82,72 @@ def partitions(R):
         json.dump(out, fh, indent=1, sort_keys=True)
 
 
+LINSOLVE_CASES = [  # (W, H, components, seed, dirichlet)
+    (7, 6, 2, 1, False), (7, 6, 3, 5, True), (10, 9, 3, 3, False), (24, 18, 3, 11, True),
+    (40, 30, 2, 4, False), (33, 21, 3, 8, False)]
+
+
+def linsolve_system(R, W, H, nc, seed, dirichlet):
+    rng = np.random.default_rng(seed)
+    f0 = rng.uniform(0, 255, (H, W))
+    f1 = np.clip(np.roll(f0, 1, axis=1) + rng.normal(0, 6, (H, W)), 0, 255)
+    terms = R.frames_to_terms(f0, f1, 1.0, 2.5)
+    nt = 2 * (W - 1) * (H - 1)
+    alpha = rng.uniform(5.0, 150.0, nt)
+    lam = np.full(nt, 35.0)
+    dv = dval = None
+    if dirichlet:
+        dv = np.arange(W)  # bottom row, test_linsolve.cpp:25-30
+        dval = rng.uniform(-1.0, 1.0, (W, nc))
+    return po.ref_assemble_system(terms, alpha, lam, nc, dv, dval)
+
+
+def linsolve(R):
+    out = {}
+    for k, (W, H, nc, seed, dirichlet) in enumerate(LINSOLVE_CASES):
+        s = linsolve_system(R, W, H, nc, seed, dirichlet)
+        xc, it, res = po.csr_cg_solve(R, s, 1e-12)
+        xd, _, resd = po.ref_csr_solve(s, 1)
+        out.update({f"{k}_row_ptr": s.row_ptr, f"{k}_cols": s.cols, f"{k}_vals": s.vals,
+                    f"{k}_rhs": s.rhs, f"{k}_nc": nc, f"{k}_perm": po.rcm_order(R, s),
+                    f"{k}_cg_x": xc, f"{k}_cg_iters": it, f"{k}_cg_res": res,
+                    f"{k}_direct_x": xd, f"{k}_direct_res": resd})
+        print("linsolve case", k, "n", s.n, "cg iters", it)
+    # an indefinite system: one neighbour coupling made larger than the geometric mean of
+    # its diagonals (both triangles)
+    s = linsolve_system(R, 9, 8, 3, 21, False)
+    vals = s.vals.copy()
+    r = 40
+    q = next(q for q in range(s.row_ptr[r], s.row_ptr[r + 1]) if s.cols[q] == r + 3)
+    c = s.cols[q]
+    dr = vals[next(q2 for q2 in range(s.row_ptr[r], s.row_ptr[r + 1]) if s.cols[q2] == r)]
+    dc = vals[next(q2 for q2 in range(s.row_ptr[c], s.row_ptr[c + 1]) if s.cols[q2] == c)]
+    v = 3.0 * np.sqrt(dr * dc)
+    vals[q] = v
+    vals[next(q2 for q2 in range(s.row_ptr[c], s.row_ptr[c + 1]) if s.cols[q2] == r)] = v
+    bad = po.CsrSystem(s.row_ptr, s.cols, vals, s.rhs, 3)
+    msgs = []
+    for method in (1, 0):
+        try:
+            po.ref_csr_solve(bad, method, 1e-12)
+            msgs.append("")
+        except po.OracleError as e:
+            msgs.append(str(e))
+    out.update({"bad_row_ptr": bad.row_ptr, "bad_cols": bad.cols, "bad_vals": bad.vals,
+                "bad_rhs": bad.rhs, "bad_msg_cholesky": msgs[0], "bad_msg_cg": msgs[1]})
+    print("indefinite:", msgs)
+    np.savez_compressed(os.path.join(OUT, "linsolve.npz"), **out)
+
+
 if __name__ == "__main__":
     R = po.REF
     if R is None:
         raise SystemExit("build the reference oracle first: make -C oracle")
     R.set_threads(os.cpu_count())
+    if len(sys.argv) > 1 and sys.argv[1] == "linsolve":
+        linsolve(R)
+        raise SystemExit(0)
     small_stages(R)
     partitions(R)
     c1_chain(R)
+    linsolve(R)

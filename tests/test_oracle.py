@@ -64,3 +64,43 @@ def test_oracle_solution_is_converged(port, golden):
     lam = np.full_like(g["alpha"], cfg.lambda0)
     y3, b3 = port.assemble_apply(t, g["alpha"], lam, 3, g["u3"])
     assert rel_l2(y3, b3) < 1e-11
+
+
+# ------------------------------------------------------------------ linsolve boundary (§8f-2)
+def _csr_case(golden, k):
+    import pyoracle as po
+    g = golden("linsolve.npz")
+    return g, po.CsrSystem(g[f"{k}_row_ptr"], g[f"{k}_cols"], g[f"{k}_vals"], g[f"{k}_rhs"],
+                           int(g[f"{k}_nc"]))
+
+
+@pytest.mark.parametrize("k", range(6))
+def test_port_csr_cg_and_rcm_pinned_to_reference(port, golden, k):
+    """The port's CSR cg_solve and rcm_order equal the reference's (golden) bit for bit."""
+    import pyoracle as po
+    g, s = _csr_case(golden, k)
+    x, it, res = po.csr_cg_solve(port, s, 1e-12)
+    assert np.array_equal(x, g[f"{k}_cg_x"])
+    assert it == int(g[f"{k}_cg_iters"]) and res == float(g[f"{k}_cg_res"])
+    assert np.array_equal(po.rcm_order(port, s), g[f"{k}_perm"])
+
+
+def test_port_cg_indefinite_message(port, golden):
+    import pyoracle as po
+    g = golden("linsolve.npz")
+    bad = po.CsrSystem(g["bad_row_ptr"], g["bad_cols"], g["bad_vals"], g["bad_rhs"], 3)
+    with pytest.raises(po.OracleError) as e:
+        po.csr_cg_solve(port, bad, 1e-12)
+    assert str(e.value) == str(g["bad_msg_cg"])
+
+
+def test_library_rcm_order_bitwise(golden):
+    """ffb_rcm_order is host integer work: checked here without a GPU."""
+    from paper_1508_02977_b200 import flowfem as ff
+    for k in range(6):
+        g, s = _csr_case(golden, k)
+        fs = ff.SparseSystem(s.row_ptr, s.cols, s.vals, s.rhs, s.components)
+        assert np.array_equal(ff.rcm_order(fs), g[f"{k}_perm"])
+    with pytest.raises(ff.FlowfemError, match="linsolve.rcm_order: system size not a multiple"):
+        g, s = _csr_case(golden, 0)
+        ff.rcm_order(ff.SparseSystem(s.row_ptr, s.cols, s.vals, s.rhs, 5))
