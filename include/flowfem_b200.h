@@ -137,6 +137,23 @@ int ffb_csr_solve(ffb_ctx* ctx, int n, int components, const int* row_ptr, const
                   const double* vals, const double* rhs, int method, double tol, int max_iters,
                   const double* warm, double* x, int* iters, double* res);
 
+/* ---- I/O and evaluation: include/flowfem/imaging.hpp, metrics.hpp ---
+ * load_image (imaging.hpp, image_io.cpp:136-145): binary PGM (8/16 bit) or non-interlaced
+ * PNG, normalised to [0,1] (RGB -> 0.299 R + 0.587 G + 0.114 B). Call with out == NULL to
+ * get W, H; then with *W, *H set and out of W*H doubles. */
+int ffb_load_image(const char* path, int* W, int* H, double* out);
+/* save_pgm (image_io.cpp:147-160): clamp to [0,1], 8-bit */
+int ffb_save_pgm(const char* path, int W, int H, const double* img);
+/* read_flo / write_flo (metrics.hpp:28-29, metrics.cpp:22-64): Middlebury .flo, float32
+ * u, v planes of W*H; read with u == v == NULL for the size first */
+int ffb_read_flo(const char* path, int* W, int* H, float* u, float* v);
+int ffb_write_flo(const char* path, int W, int H, const float* u, const float* v);
+/* compute_metrics (metrics.hpp:41, metrics.cpp:75-100) as a device reduction: average
+ * angular error [deg] and endpoint error over pixels with valid truth (|u|,|v| <= 1e9) */
+int ffb_compute_metrics(ffb_ctx* ctx, int W, int H, const double* u1, const double* u2,
+                        const float* tu, const float* tv, double* aae_deg, double* ee,
+                        long long* valid);
+
 /* ---- operator: include/flowfem/assembly.hpp --------------------------------------- */
 /* y = A x and b of the unconstrained global system: assemble (assembly.hpp:59-61,
  * assembly.cpp:32-166) followed by spmv (assembly.hpp:76, assembly.cpp:240-249), computed

@@ -268,6 +268,34 @@ def rcm_order(oracle, sys: CsrSystem):
     return perm
 
 
+def ref_compute_metrics(flow3, tu, tv):
+    """The reference's compute_metrics (metrics.cpp:75-100): (aae_deg, ee, valid)."""
+    flow3 = _f64(flow3)
+    _, H, W = flow3.shape
+    tu = np.ascontiguousarray(tu, dtype=np.float32)
+    tv = np.ascontiguousarray(tv, dtype=np.float32)
+    a, e, k = C.c_double(), C.c_double(), C.c_long()
+    REF._call("compute_metrics", W, H, _ptr(flow3), _ptr(tu), _ptr(tv), C.byref(a), C.byref(e),
+              C.byref(k))
+    return a.value, e.value, k.value
+
+
+def ref_write_flo(path, tu, tv):
+    tu = np.ascontiguousarray(tu, dtype=np.float32)
+    tv = np.ascontiguousarray(tv, dtype=np.float32)
+    H, W = tu.shape
+    REF._call("write_flo", path.encode(), W, H, _ptr(tu), _ptr(tv))
+
+
+def ref_to_flo(flow3):
+    flow3 = _f64(flow3)
+    _, H, W = flow3.shape
+    u = np.zeros((H, W), np.float32)
+    v = np.zeros((H, W), np.float32)
+    REF._call("to_flo", W, H, _ptr(flow3), _ptr(u), _ptr(v))
+    return u, v
+
+
 def _load(sub, name, prefix, kind):
     p = os.path.join(HERE, sub, name)
     return Oracle(p, prefix, kind) if os.path.exists(p) else None

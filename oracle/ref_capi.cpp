@@ -28,6 +28,7 @@
 #include "flowfem/assembly.hpp"
 #include "flowfem/imaging.hpp"
 #include "flowfem/linsolve.hpp"
+#include "flowfem/metrics.hpp"
 #include "flowfem/mesh.hpp"
 #include "flowfem/pipeline.hpp"
 #include "flowfem/schwarz.hpp"
@@ -357,6 +358,38 @@ int ref_rcm_order(int n, int nc, const int* row_ptr, const int* cols, int* perm)
     const SparseSystem sys = csr_system(n, nc, row_ptr, cols, vals.data(), nullptr);
     const std::vector<int> p = rcm_order(sys);
     std::copy(p.begin(), p.end(), perm);
+  });
+}
+
+// ----------------------------------------------------------------- evaluation (metrics.cpp)
+// compute_metrics (metrics.cpp:75-100) of planes3 flow against float truth planes
+int ref_compute_metrics(int W, int H, const double* flow3, const float* tu, const float* tv,
+                        double* aae, double* ee, long* valid) {
+  return guard([&] {
+    const FlowState st = to_state(W, H, flow3);
+    FloField f(W, H);
+    std::memcpy(f.u.data(), tu, sizeof(float) * W * H);
+    std::memcpy(f.v.data(), tv, sizeof(float) * W * H);
+    const FlowMetrics m = compute_metrics(st, f);
+    *aae = m.aae_deg, *ee = m.ee, *valid = m.valid;
+  });
+}
+
+int ref_write_flo(const char* path, int W, int H, const float* u, const float* v) {
+  return guard([&] {
+    FloField f(W, H);
+    std::memcpy(f.u.data(), u, sizeof(float) * W * H);
+    std::memcpy(f.v.data(), v, sizeof(float) * W * H);
+    write_flo(path, f);
+  });
+}
+
+// to_flo (metrics.cpp:66-73) of planes3
+int ref_to_flo(int W, int H, const double* flow3, float* u, float* v) {
+  return guard([&] {
+    const FloField f = to_flo(to_state(W, H, flow3));
+    std::memcpy(u, f.u.data(), sizeof(float) * W * H);
+    std::memcpy(v, f.v.data(), sizeof(float) * W * H);
   });
 }
 

@@ -12,7 +12,8 @@ from .flowfem import (AdaptConfig, Context, DataTerms, DerivativeField, FlowfemE
                       default_context, enumerate_splits, error_indicator, frames_to_terms,
                       gaussian_smooth, kernel_launches, run_on_frames, run_on_frames_device,
                       schwarz_solve, SolveMethod, SolverConfig, SolveReport, SparseSystem,
-                      spmv, rcm_order, cg_solve, solve,
+                      spmv, rcm_order, cg_solve, solve, load_image, save_pgm, FloField,
+                      read_flo, write_flo, to_flo, FlowMetrics, compute_metrics,
                       uniform_reg, update_alpha)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -52,6 +52,11 @@ SIGNATURES = {
     "ffb_enumerate_splits": (_i, [_i, _i, _i, _vp, _vp, _vp, _i]),
     "ffb_choose_split": (_i, [_i, _i, _i, _vp, _vp, _vp]),
     "ffb_csr_spmv": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp]),
+    "ffb_load_image": (_i, [C.c_char_p, _vp, _vp, _vp]),
+    "ffb_save_pgm": (_i, [C.c_char_p, _i, _i, _vp]),
+    "ffb_read_flo": (_i, [C.c_char_p, _vp, _vp, _vp, _vp]),
+    "ffb_write_flo": (_i, [C.c_char_p, _i, _i, _vp, _vp]),
+    "ffb_compute_metrics": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ffb_rcm_order": (_i, [_i, _i, _vp, _vp, _vp]),
     "ffb_csr_cg_solve": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp]),
     "ffb_csr_solve": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _i, _d, _i, _vp, _vp, _vp, _vp]),

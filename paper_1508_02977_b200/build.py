@@ -31,8 +31,9 @@ CU = {
     "pcg.cu": [],
     "ras.cu": ["--fmad=false"],
     "linsolve.cu": ["--fmad=false"],
+    "metrics.cu": ["--fmad=false"],
 }
-CPP = ["capi.cpp", "partition.cpp", "rcm.cpp"]
+CPP = ["capi.cpp", "partition.cpp", "rcm.cpp", "io.cpp"]
 HEADERS = ["ffb_internal.cuh", "partition.hpp"]
 
 
@@ -69,7 +70,7 @@ def build(verbose: bool = False) -> str:
             print(f"[{src}] {log}", file=sys.stderr)
     if _newer(objs, LIB):
         cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static", "-lrt", "-ldl",
-                                                             "-lpthread"]
+                                                             "-lpthread", "-lz"]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"link failed:\n{p.stdout}\n{p.stderr}")

@@ -1330,4 +1330,78 @@ int ffb_csr_solve(ffb_ctx* c, int n, int components, const int* row_ptr, const i
   });
 }
 
+/* ---- I/O and evaluation (image_io.cpp, metrics.cpp) ---------------------------------- */
+int ffb_load_image(const char* path, int* W, int* H, double* out) {
+  return guard([&] {
+    if (!path || !W || !H) fail("imaging.load_image: null argument");
+    int w = 0, h = 0;
+    const std::vector<double> img = load_image(path, w, h);
+    if (out) {
+      if (*W != w || *H != h) fail("imaging.load_image: output buffer size does not match " + std::string(path));
+      std::copy(img.begin(), img.end(), out);
+    }
+    *W = w, *H = h;
+  });
+}
+
+int ffb_save_pgm(const char* path, int W, int H, const double* img) {
+  return guard([&] {
+    if (!path || !img || W <= 0 || H <= 0) fail("imaging.save_pgm: bad arguments");
+    save_pgm(path, W, H, img);
+  });
+}
+
+int ffb_read_flo(const char* path, int* W, int* H, float* u, float* v) {
+  return guard([&] {
+    if (!path || !W || !H) fail("metrics.read_flo: null argument");
+    int w = 0, h = 0;
+    std::vector<float> uu, vv;
+    read_flo(path, w, h, uu, vv);
+    if (u && v) {
+      if (*W != w || *H != h) fail("metrics.read_flo: output buffer size does not match " + std::string(path));
+      std::copy(uu.begin(), uu.end(), u);
+      std::copy(vv.begin(), vv.end(), v);
+    }
+    *W = w, *H = h;
+  });
+}
+
+int ffb_write_flo(const char* path, int W, int H, const float* u, const float* v) {
+  return guard([&] {
+    if (!path || !u || !v || W <= 0 || H <= 0) fail("metrics.write_flo: bad arguments");
+    write_flo(path, W, H, u, v);
+  });
+}
+
+int ffb_compute_metrics(ffb_ctx* c, int W, int H, const double* u1, const double* u2,
+                        const float* tu, const float* tv, double* aae_deg, double* ee,
+                        long long* valid) {
+  return guard([&] {
+    check_ctx(c);
+    check_dims(W, H, "metrics.compute_metrics");
+    const size_t n = static_cast<size_t>(W) * H;
+    double* d = c->work.ensure(2 * n + 2 * ((n + 1) / 2) + 3 * kRedBlocks + 4);
+    double* du1 = d;
+    double* du2 = d + n;
+    float* dtu = reinterpret_cast<float*>(d + 2 * n);
+    float* dtv = dtu + n;
+    double* part = d + 2 * n + 2 * ((n + 1) / 2);
+    double* out = part + 3 * kRedBlocks;
+    unsigned* counter = c->counter.ensure(1);
+    upload(du1, u1, n, c->st);
+    upload(du2, u2, n, c->st);
+    FFB_CUDA(cudaMemcpyAsync(dtu, tu, n * sizeof(float), cudaMemcpyHostToDevice, c->st));
+    FFB_CUDA(cudaMemcpyAsync(dtv, tv, n * sizeof(float), cudaMemcpyHostToDevice, c->st));
+    FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
+    flow_metrics(du1, du2, dtu, dtv, static_cast<long long>(n), part, counter, out, c->st);
+    double h[3];
+    download(h, out, 3, c->st);
+    sync(c);
+    const long long k = static_cast<long long>(h[2]);
+    *valid = k;
+    *aae_deg = k > 0 ? h[0] / static_cast<double>(k) * 180.0 / M_PI : 0.0;
+    *ee = k > 0 ? h[1] / static_cast<double>(k) : 0.0;
+  });
+}
+
 }  // extern "C"

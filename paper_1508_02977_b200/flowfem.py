@@ -328,6 +328,91 @@ def assemble_apply(terms: DataTerms, reg: RegField, components: int, x: FlowStat
     return FlowState.from_planes(y3), FlowState.from_planes(b3)
 
 
+# ---------------------------------------------------------------- I/O and evaluation
+def load_image(path: str) -> np.ndarray:
+    """imaging.hpp load_image (image_io.cpp:136-145): binary PGM or PNG -> H x W float64 in
+    [0,1]."""
+    lib = _lib.load()
+    W, H = C.c_int(), C.c_int()
+    _check(lib.ffb_load_image(os.fsencode(path), C.byref(W), C.byref(H), None))
+    img = np.zeros((H.value, W.value))
+    _check(lib.ffb_load_image(os.fsencode(path), C.byref(W), C.byref(H), _p(img)))
+    return img
+
+
+def save_pgm(path: str, img) -> None:
+    """image_io.cpp:147-160 (clamped to [0,1], 8 bit)."""
+    img = _f64(img)
+    H, W = img.shape
+    _check(_lib.load().ffb_save_pgm(os.fsencode(path), W, H, _p(img)))
+
+
+@dataclass
+class FloField:
+    """metrics.hpp:13-23: float32 flow planes (H x W); |component| > 1e9 marks invalid."""
+    u: np.ndarray
+    v: np.ndarray
+
+    @property
+    def width(self) -> int:
+        return self.u.shape[1]
+
+    @property
+    def height(self) -> int:
+        return self.u.shape[0]
+
+
+def read_flo(path: str) -> FloField:
+    """metrics.cpp:22-45."""
+    lib = _lib.load()
+    W, H = C.c_int(), C.c_int()
+    _check(lib.ffb_read_flo(os.fsencode(path), C.byref(W), C.byref(H), None, None))
+    u = np.zeros((H.value, W.value), np.float32)
+    v = np.zeros((H.value, W.value), np.float32)
+    _check(lib.ffb_read_flo(os.fsencode(path), C.byref(W), C.byref(H), _p(u), _p(v)))
+    return FloField(u, v)
+
+
+def write_flo(path: str, f: FloField) -> None:
+    """metrics.cpp:47-64."""
+    u = np.ascontiguousarray(f.u, dtype=np.float32)
+    v = np.ascontiguousarray(f.v, dtype=np.float32)
+    H, W = u.shape
+    _check(_lib.load().ffb_write_flo(os.fsencode(path), W, H, _p(u), _p(v)))
+
+
+def to_flo(state: "FlowState") -> FloField:
+    """metrics.cpp:66-73: (u1, u2) rounded to float32."""
+    p = state.planes()
+    return FloField(p[0].astype(np.float32), p[1].astype(np.float32))
+
+
+@dataclass
+class FlowMetrics:
+    """metrics.hpp:33-37."""
+    aae_deg: float = 0.0
+    ee: float = 0.0
+    valid: int = 0
+
+
+def compute_metrics(flow: "FlowState", truth: FloField, ctx: Context | None = None) -> FlowMetrics:
+    """metrics.cpp:75-100 as a device reduction: average angular error (degrees, (u, v, 1)
+    normalisation) and endpoint error over pixels with valid truth."""
+    ctx = ctx or default_context()
+    p = flow.planes()
+    if p.shape[1:] != truth.u.shape:
+        raise FlowfemError("metrics.compute_metrics: flow and ground truth sizes differ")
+    H, W = truth.u.shape
+    u1 = np.ascontiguousarray(p[0])
+    u2 = np.ascontiguousarray(p[1])
+    tu = np.ascontiguousarray(truth.u, dtype=np.float32)
+    tv = np.ascontiguousarray(truth.v, dtype=np.float32)
+    a, e, k = C.c_double(), C.c_double(), C.c_longlong()
+    _check(ctx.lib.ffb_compute_metrics(ctx.handle, W, H, _p(u1), _p(u2), _p(tu), _p(tv),
+                                       C.byref(a), C.byref(e), C.byref(k)))
+    return FlowMetrics(a.value, e.value, k.value)
+
+
 # ---------------------------------------------------------------- linsolve boundary
 class SolveMethod:
     """linsolve.hpp:10 (enum class SolveMethod)."""
