@@ -14,6 +14,7 @@ from .flowfem import (AdaptConfig, Context, DataTerms, DerivativeField, FlowfemE
                       schwarz_solve, SolveMethod, SolverConfig, SolveReport, SparseSystem,
                       spmv, rcm_order, cg_solve, solve, load_image, save_pgm, FloField,
                       read_flo, write_flo, to_flo, FlowMetrics, compute_metrics,
+                      PipelineConfig, PipelineResult, run_pipeline,
                       uniform_reg, update_alpha)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

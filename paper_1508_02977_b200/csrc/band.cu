@@ -217,7 +217,7 @@ __device__ __forceinline__ void rupd_tile(double* __restrict__ D, int kd, int kd
 template <int NB>
 __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P, double* Li2,
                              double* ir, int* cnt, double* Z, int& first_bad, int bad_base,
-                             int la) {
+                             int la, int q, int C) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int LS = NB * (NB + 1);
   PROF_DECL
@@ -253,8 +253,9 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
     }
     __syncthreads();
     PROF_MARK(2);
-    // ---- A_RR -= Z Z^T, 32x32 tiles from a shared queue. Look-ahead (la): warp 0 first
-    // finishes the tile holding the next pivot block and factors that block meanwhile.
+    // ---- A_RR -= Z Z^T, 32x32 tiles from a shared queue (tiles q, q + C, ... of the
+    // cluster's CTA q). Look-ahead (la, single CTA): warp 0 first finishes the tile holding
+    // the next pivot block and factors that block meanwhile.
     const int nx = (la && k1 < kd) ? k1 / 32 : -1;
     const int special = nx >= 0 ? nx * (nx + 1) / 2 + nx : -1;
     if (warp == 0 && special >= 0) {
@@ -265,7 +266,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
     }
     for (;;) {
       int idx = 0;
-      if (lane == 0) idx = atomicAdd(cnt + (step & 1), 1);
+      if (lane == 0) idx = q + C * atomicAdd(cnt + (step & 1), 1);
       idx = __shfl_sync(~0u, idx, 0);
       if (idx >= ntiles) break;
       if (idx == special) continue;
@@ -274,7 +275,8 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       while ((TU + 1) * (TU + 2) / 2 <= idx) ++TU;
       rupd_tile(D, kd, kdp, Z, nbk, k0, k1, TU, idx - TU * (TU + 1) / 2, lane);
     }
-    __syncthreads();
+    // all tile updates (and, across the cluster, all reads of A_RK for Z) are done
+    if (C > 1) cl_sync(); else __syncthreads();
     PROF_MARK(3);
     if (!la && warp == 0) {
       // the next pivot block is final now: factor it while the other warps write A_RK, A_KK
@@ -283,7 +285,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
     } else {
       // ---- A_RK <- Z Li ; A_KK <- -Li^T Li
       const int t0 = la ? 0 : 32, t2 = tid - t0, nth = kFT - t0;
-      for (int i = t2; i < kd; i += nth) {
+      for (int i = t2 + nth * q; i < kd; i += nth * C) {
         if (i >= k0 && i < k1) continue;
         double z[NB];
 #pragma unroll
@@ -301,7 +303,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
           }
         }
       }
-      for (int e = t2; e < nbk * nbk; e += nth) {
+      for (int e = q == 0 ? t2 : nbk * nbk; e < nbk * nbk; e += nth) {
         const int a = e / nbk, b = e - a * nbk;
         if (b > a) continue;
         double acc = 0.0;
@@ -309,6 +311,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
         D[static_cast<long long>(k0 + a) * kd + k0 + b] = -acc;
       }
     }
+    if (C > 1) cl_sync();  // A_RK, A_KK written cluster-wide before the next Z / pack
     PROF_MARK(4);
   }
   __syncthreads();
@@ -318,12 +321,15 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
 // D <- A_ll - sum over the given neighbour lines of B (inv_nb) B  (lower triangle)
 __device__ void build_line(const SubInfo& s, const double* __restrict__ coef, size_t N, int W,
                            int nc, int l, int nb0, int bl0, int nb1, int bl1,
-                           const double* __restrict__ F, double* __restrict__ D) {
+                           const double* __restrict__ F, double* __restrict__ D, int q,
+                           int C) {
   // neighbour nbX (line index or -1) with coupling taken at line blX (bcoef(blX): between
-  // lines blX and blX-1)
+  // lines blX and blX-1). CTA q of the cluster builds rows kFW q + (kFW C) k + warp, which
+  // read only the same rows of the neighbour inverses (packed by this CTA: pack_line uses
+  // the same split).
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kd = s.kd;
-  for (int i = warp; i < kd; i += kFW) {
+  for (int i = warp + kFW * q; i < kd; i += kFW * C) {
     const double b0i = nb0 >= 0 ? bcoef(s, coef, N, W, nc, bl0, i) : 0.0;
     const double b1i = nb1 >= 0 ? bcoef(s, coef, N, W, nc, bl1, i) : 0.0;
     const long long oi = prow_off(i);
@@ -339,11 +345,12 @@ __device__ void build_line(const SubInfo& s, const double* __restrict__ coef, si
   __syncthreads();
 }
 
-__device__ void pack_line(const SubInfo& s, int l, const double* __restrict__ D, double* F) {
+__device__ void pack_line(const SubInfo& s, int l, const double* __restrict__ D, double* F,
+                          int q, int C) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kd = s.kd;
   double* Fl = F + static_cast<long long>(l) * s.line_sz;
-  for (int i = warp; i < kd; i += kFW) {
+  for (int i = warp + kFW * q; i < kd; i += kFW * C) {
     const long long o = prow_off(i);
     for (int j = lane; j <= i; j += 32) Fl[o + j] = -D[static_cast<long long>(i) * kd + j];
     if ((i & 1) == 0 && lane == 0) Fl[o + i + 1] = 0.0;  // pad of even rows
@@ -351,16 +358,21 @@ __device__ void pack_line(const SubInfo& s, int l, const double* __restrict__ D,
   __syncthreads();
 }
 
-// one CTA per (subdomain, chain): chain 0 lines 0..m-1 downward, chain 1 lines L-1..m+1
-// upward; mid = 1 launches one CTA per subdomain for the middle line
+// one thread-block cluster of C CTAs per (subdomain, chain): chain 0 lines 0..m-1 downward,
+// chain 1 lines L-1..m+1 upward; mid = 1 launches one cluster per subdomain for the middle
+// line. The CTAs of a cluster share the line matrix D (global scratch, L2-resident): each
+// builds and packs its share of the rows, takes every C-th tile of the trailing updates and
+// its share of the A_RK rows, and factors the pivot blocks redundantly (no exchange).
 template <int NB>
 __global__ void __launch_bounds__(kFT, 1)
     k_line_factor(const SubInfo* __restrict__ subs, const double* __restrict__ coef, size_t N,
                   int W, int nc, double* __restrict__ fac, double* __restrict__ scratch,
                   long long scratch_stride, int kdp, int mid, int* __restrict__ bad,
                   const int2* __restrict__ changed, int la) {
-  const int sub = mid ? blockIdx.x : blockIdx.x >> 1;
-  const int chain = mid ? 0 : blockIdx.x & 1;
+  const int C = static_cast<int>(cl_size()), q = static_cast<int>(cl_rank());
+  const int cid = blockIdx.x / C;
+  const int sub = mid ? cid : cid >> 1;
+  const int chain = mid ? 0 : cid & 1;
   const SubInfo s = subs[sub];
   const int tid = threadIdx.x;
   const int kd = s.kd, L = s.L, m = mid_line(L);
@@ -369,7 +381,7 @@ __global__ void __launch_bounds__(kFT, 1)
   // untouched prefix of each chain keeps its inverses (D_l depends on lines <= l only)
   const int2 chg = changed ? changed[sub] : make_int2(0, L - 1);
   if (chg.x > chg.y) return;  // nothing changed in this subdomain
-  double* D = scratch + (mid ? sub : blockIdx.x) * scratch_stride;
+  double* D = scratch + (mid ? sub : cid) * scratch_stride;
   double* F = fac + s.fac_off;
   extern __shared__ __align__(16) double fsm[];
   double* P = fsm;                    // NB x (NB+1)
@@ -381,10 +393,12 @@ __global__ void __launch_bounds__(kFT, 1)
   int first_bad = 0x7fffffff;
   PROF_DECL
   if (mid) {
-    build_line(s, coef, N, W, nc, m, m > 0 ? m - 1 : -1, m, m < L - 1 ? m + 1 : -1, m + 1, F, D);
+    build_line(s, coef, N, W, nc, m, m > 0 ? m - 1 : -1, m, m < L - 1 ? m + 1 : -1, m + 1, F, D,
+               q, C);
+    if (C > 1) cl_sync();
     PROF_MARK(0);
-    sweep_invert<NB>(D, kd, kdp, P, Li, ir, cnt, Z, first_bad, m * kd, la);
-    pack_line(s, m, D, F);
+    sweep_invert<NB>(D, kd, kdp, P, Li, ir, cnt, Z, first_bad, m * kd, la, q, C);
+    pack_line(s, m, D, F, q, C);
   } else {
     const int nlines = chain == 0 ? m : L - 1 - m;
     const int t0 = chain == 0 ? chg.x : L - 1 - chg.y;
@@ -392,15 +406,16 @@ __global__ void __launch_bounds__(kFT, 1)
       const int l = chain == 0 ? t : L - 1 - t;
       const int prev = t == 0 ? -1 : (chain == 0 ? l - 1 : l + 1);
       const int bl = chain == 0 ? l : l + 1;  // coupling between l and prev
-      build_line(s, coef, N, W, nc, l, prev, bl, -1, 0, F, D);
+      build_line(s, coef, N, W, nc, l, prev, bl, -1, 0, F, D, q, C);
+      if (C > 1) cl_sync();
       PROF_MARK(0);
-      sweep_invert<NB>(D, kd, kdp, P, Li, ir, cnt, Z, first_bad, l * kd, la);
-      pack_line(s, l, D, F);
+      sweep_invert<NB>(D, kd, kdp, P, Li, ir, cnt, Z, first_bad, l * kd, la, q, C);
+      pack_line(s, l, D, F, q, C);
       PROF_MARK(5);
     }
   }
   PROF_FLUSH(0);
-  if (tid == 0 && first_bad != 0x7fffffff) atomicMin(bad + sub, first_bad);
+  if (tid == 0 && q == 0 && first_bad != 0x7fffffff) atomicMin(bad + sub, first_bad);
 }
 
 // ----------------------------------------------------------------- K6 solve
@@ -1036,7 +1051,7 @@ void changed_lines(const SubInfo* d_subs, int nsub, const double* alpha, const d
   FFB_LAUNCHED();
 }
 
-void line_factor(const SubInfo* d_subs, int nsub, int /*C*/, int nb, int kd_max,
+void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
                  const double* coef, size_t N, int W, int nc, double* fac, double* scratch,
                  long long scratch_stride, int* d_bad, cudaStream_t st, const int2* changed) {
   const int kdp = (kd_max + 31) / 32 * 32;
@@ -1046,18 +1061,19 @@ void line_factor(const SubInfo* d_subs, int nsub, int /*C*/, int nb, int kd_max,
   }();
   const size_t smem = (3 * nb * (nb + 1) + 2 * nb + static_cast<size_t>(nb) * kdp) * sizeof(double);
   if (smem > 227 * 1024) fail("linsolve.cholesky: subdomain line too wide for shared memory");
+  if (const char* e = std::getenv("FFB_FCLUSTER")) {
+    const int v = std::atoi(e);
+    if (v == 1 || v == 2 || v == 4 || v == 8) C = v;
+  }
+  const int lac = C > 1 ? 0 : la;  // the look-ahead pivot is a single-CTA schedule
   for (int mid = 0; mid <= 1; ++mid) {
-    const int grid = mid ? nsub : 2 * nsub;
+    const int grid = (mid ? nsub : 2 * nsub) * C;
     if (nb == 32) {
-      FFB_CUDA(cudaFuncSetAttribute(k_line_factor<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-      k_line_factor<32><<<grid, kFT, smem, st>>>(d_subs, coef, N, W, nc, fac, scratch,
-                                                 scratch_stride, kdp, mid, d_bad, changed, la);
+      launch_cluster(k_line_factor<32>, grid, kFT, smem, C, st, d_subs, coef, N, W, nc, fac,
+                     scratch, scratch_stride, kdp, mid, d_bad, changed, lac);
     } else if (nb == 16) {
-      FFB_CUDA(cudaFuncSetAttribute(k_line_factor<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-      k_line_factor<16><<<grid, kFT, smem, st>>>(d_subs, coef, N, W, nc, fac, scratch,
-                                                 scratch_stride, kdp, mid, d_bad, changed, la);
+      launch_cluster(k_line_factor<16>, grid, kFT, smem, C, st, d_subs, coef, N, W, nc, fac,
+                     scratch, scratch_stride, kdp, mid, d_bad, changed, lac);
     } else {
       fail("internal: unsupported pivot block size");
     }
@@ -1070,7 +1086,8 @@ SolvePlan solve_plan(int kd_max, int C) {
   pl.C = C;
   const size_t fixed =
       128 + (static_cast<size_t>(kCW) * kd_max + 3 * kd_max + 8 * kd_max) * sizeof(double);
-  const size_t budget = 227 * 1024 - 1024;
+  size_t budget = 227 * 1024 - 1024;
+  if (const char* e = std::getenv("FFB_SOLVE_SMEM_KB")) budget = static_cast<size_t>(std::atoi(e)) * 1024;
   if (kd_max > 2 * kCT || fixed + 2 * 1024 * sizeof(double) > budget)
     fail("linsolve.cholesky: subdomain line too wide for the solve kernel");
   const size_t avail = budget - fixed;

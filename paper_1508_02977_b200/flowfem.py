@@ -739,6 +739,51 @@ def run_on_frames(f0, f1, cfg: RunConfig, ctx: Context | None = None) -> RunResu
                      RunStats.from_c(st, cfg.adapt_iters), W, H)
 
 
+@dataclass
+class PipelineConfig:
+    """The file-level fields of pipeline.hpp:15-33 used by run_pipeline; the solver fields
+    are a RunConfig. Visualisations (out_png, dump_alpha, dump_mt) are out of scope."""
+    frame0: str = ""
+    frame1: str = ""
+    ground_truth: str = ""
+    out_flo: str = ""
+    out_metrics: str = ""
+    run: RunConfig = field(default_factory=RunConfig)
+    scale_255: bool = False  # multiply the [0,1] images by 255 (SURVEY D3 frames)
+
+
+@dataclass
+class PipelineResult:
+    result: RunResult
+    metrics: Optional[FlowMetrics]
+
+
+def run_pipeline(cfg: PipelineConfig, ctx: Context | None = None) -> PipelineResult:
+    """run_pipeline (pipeline.cpp:110-120): load both frames, run_on_frames, compute_metrics
+    against the ground truth if given, write the .flo and the metrics CSV (pipeline.cpp:82-98)."""
+    if not cfg.frame0 or not cfg.frame1:
+        raise FlowfemError("cli.run: both frames are required")
+    f0, f1 = load_image(cfg.frame0), load_image(cfg.frame1)
+    if cfg.scale_255:
+        f0, f1 = f0 * 255.0, f1 * 255.0
+    res = run_on_frames(f0, f1, cfg.run, ctx)
+    metrics = None
+    if cfg.ground_truth:
+        metrics = compute_metrics(res.flow, read_flo(cfg.ground_truth), ctx)
+    if cfg.out_flo:
+        write_flo(cfg.out_flo, to_flo(res.flow))
+    if cfg.out_metrics:
+        try:
+            with open(cfg.out_metrics, "w") as fh:
+                fh.write("mode,aae_deg,ee,valid_pixels\n")
+                if metrics is not None:
+                    fh.write(f"{'illum_on' if cfg.run.illumination else 'illum_off'},"
+                             f"{metrics.aae_deg:g},{metrics.ee:g},{metrics.valid}\n")
+        except OSError:
+            raise FlowfemError("cli.out_metrics: cannot open " + cfg.out_metrics)
+    return PipelineResult(res, metrics)
+
+
 def run_on_frames_device(f0_ptr: int, f1_ptr: int, W: int, H: int, u3_ptr: int, cfg: RunConfig,
                          ctx: Context | None = None) -> RunStats:
     """Same with device pointers (e.g. torch CUDA tensors' data_ptr()); inputs stay in HBM."""

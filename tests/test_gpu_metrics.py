@@ -31,3 +31,27 @@ def test_metrics_no_valid_and_size_mismatch(ctx):
     assert (m.aae_deg, m.ee, m.valid) == (0.0, 0.0, 0)
     with pytest.raises(ff.FlowfemError, match="metrics.compute_metrics: flow and ground truth sizes differ"):
         ff.compute_metrics(flow, ff.FloField(np.zeros((5, 4), np.float32), np.zeros((5, 4), np.float32)), ctx=ctx)
+
+
+def test_run_pipeline_files_end_to_end(ctx, tmp_path):
+    """pipeline.cpp:110-120: PGM frames in, .flo + metrics CSV out; the metrics equal
+    compute_metrics of the returned flow against the written truth."""
+    from paper_1508_02977_b200 import synth
+    f0, f1, flow, cfg = synth.make("c1")
+    ff.save_pgm(str(tmp_path / "f0.pgm"), f0 / 255.0)
+    ff.save_pgm(str(tmp_path / "f1.pgm"), f1 / 255.0)
+    ff.write_flo(str(tmp_path / "gt.flo"), ff.FloField(flow[0].astype(np.float32),
+                                                       flow[1].astype(np.float32)))
+    pc = ff.PipelineConfig(str(tmp_path / "f0.pgm"), str(tmp_path / "f1.pgm"),
+                           str(tmp_path / "gt.flo"), str(tmp_path / "out.flo"),
+                           str(tmp_path / "m.csv"),
+                           ff.RunConfig(sigma=cfg.sigma, parts=cfg.parts, overlap=cfg.overlap,
+                                        adapt_iters=cfg.n_passes), scale_255=True)
+    r = ff.run_pipeline(pc, ctx=ctx)
+    out = ff.read_flo(str(tmp_path / "out.flo"))
+    assert np.array_equal(out.u, r.result.flow.u1.astype(np.float32))
+    m = ff.compute_metrics(r.result.flow, ff.read_flo(str(tmp_path / "gt.flo")), ctx=ctx)
+    assert (m.aae_deg, m.ee, m.valid) == (r.metrics.aae_deg, r.metrics.ee, r.metrics.valid)
+    assert r.metrics.valid == f0.size and r.metrics.ee < 1.0  # the rotation is recovered
+    lines = (tmp_path / "m.csv").read_text().splitlines()
+    assert lines[0] == "mode,aae_deg,ee,valid_pixels" and lines[1].startswith("illum_on,")
