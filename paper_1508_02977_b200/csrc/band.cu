@@ -72,6 +72,12 @@ __host__ __device__ __forceinline__ long long prow_off(int r) {
   return (r & 1) ? 2 * m * (m + 1) + 2 * m + 2 : 2 * m * (m + 1);
 }
 
+// the same offset in 32-bit arithmetic (a line holds < 2^31 entries)
+__device__ __forceinline__ int prow_off32(int r) {
+  const int m = r >> 1;
+  return 2 * m * (m + 1) + (r & 1) * (2 * m + 2);
+}
+
 // global interleaved index of local unknown j of line l
 __device__ __forceinline__ long long gidx(const SubInfo& s, int l, int j, int W, int nc) {
   const int a = j / nc, c = j - a * nc;
@@ -209,6 +215,47 @@ __device__ __forceinline__ void rupd_tile(double* __restrict__ D, int kd, int kd
   }
 }
 
+// P (stride NB+1, lower) <- A_K'K' - Z_K' Z_K'^T for the next pivot block K' = [k1, k1+nb1)
+// (k1 a multiple of 32): the 32x32 tile of rupd_tile, read from D but written to P only.
+// Split over 4 warps (part = warp 0..3): rows 8 part .. 8 part + 7, lane -> 2 rows x 4 cols.
+template <int NB>
+__device__ __forceinline__ void kk_update(const double* __restrict__ D, int kd, int kdp,
+                                          const double* __restrict__ Z, int nbk, int k1,
+                                          int nb1, double* P, int lane, int part) {
+  const int ui = lane & 3, vi = lane >> 2;
+  const int u0 = 8 * part + 2 * ui, v0 = 4 * vi;
+  double acc[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  if (v0 <= u0 + 1) {
+#pragma unroll 4
+    for (int c = 0; c < nbk; ++c) {
+      const double* zc = Z + c * kdp + k1;
+      const double2 a = *reinterpret_cast<const double2*>(zc + u0);
+      const double2 b0 = *reinterpret_cast<const double2*>(zc + v0);
+      const double2 b1 = *reinterpret_cast<const double2*>(zc + v0 + 2);
+      const double b[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[0][j] = fma(a.x, b[j], acc[0][j]);
+        acc[1][j] = fma(a.y, b[j], acc[1][j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int u = u0 + i;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int v = v0 + j;
+      if (v <= u && u < nb1)
+        P[u * (NB + 1) + v] = D[static_cast<long long>(k1 + u) * kd + k1 + v] - acc[i][j];
+    }
+  }
+}
+
 // In-place inversion of the SPD line matrix D (kd x kd row-major in global scratch, lower
 // triangle used) by the blocked symmetric sweep; leaves -D^{-1} in the lower triangle.
 // The next step's pivot block is factored by warp 0 while the other 15 warps write the
@@ -223,6 +270,9 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
   PROF_DECL
   if (tid == 0) cnt[0] = 0;
   if (warp == 0) pivot_warp<NB>(D, kd, 0, min(NB, kd), P, Li2, ir, first_bad, bad_base);
+  const bool la_reg = NB == 32 && la;  // look-ahead on a private copy of the next pivot block
+  int pv_tag = 0;                      // pivot_pair progress tags (same on every warp)
+  if (tid == 0) cnt[2] = 0;
   const int nt = (kd + 31) / 32;
   const int ntiles = nt * (nt + 1) / 2;
   int step = 0;
@@ -258,10 +308,26 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
     // the next pivot block and factors that block meanwhile.
     const int nx = (la && k1 < kd) ? k1 / 32 : -1;
     const int special = nx >= 0 ? nx * (nx + 1) / 2 + nx : -1;
-    if (warp == 0 && special >= 0) {
-      rupd_tile(D, kd, kdp, Z, nbk, k0, k1, nx, nx, lane);
-      __syncwarp();
-      pivot_warp<NB>(D, kd, k1, min(NB, kd - k1), P, Lnext, ir, first_bad, bad_base);
+    if (la_reg && warp < 4 && special >= 0) {
+      // NB = 32: tile (nx, nx) is exactly the next pivot block K', needed by nothing but the
+      // pivot (A_KK is overwritten at its own step). Every CTA of the cluster updates a
+      // private copy in P (warps 0-3) and factors it (warp 0); nobody writes the tile back,
+      // so there is no ordering against the other CTAs' updates.
+      kk_update<NB>(D, kd, kdp, Z, nbk, k1, min(NB, kd - k1), P, lane, warp);
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (warp < 2)
+        pivot_pair<NB>(P, NB + 1, k1, min(NB, kd - k1), P, Lnext, ir, first_bad, bad_base,
+                       cnt + 2, ++pv_tag);
+      else
+        ++pv_tag;
+      PROF_MARK(5);
+    } else if (warp == 0 && special >= 0) {
+      {
+        rupd_tile(D, kd, kdp, Z, nbk, k0, k1, nx, nx, lane);
+        __syncwarp();
+        pivot_warp<NB>(D + static_cast<long long>(k1) * kd + k1, kd, k1, min(NB, kd - k1), P,
+                       Lnext, ir, first_bad, bad_base);
+      }
       PROF_MARK(5);
     }
     for (;;) {
@@ -280,12 +346,14 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
     PROF_MARK(3);
     if (!la && warp == 0) {
       // the next pivot block is final now: factor it while the other warps write A_RK, A_KK
-      if (k1 < kd) pivot_warp<NB>(D, kd, k1, min(NB, kd - k1), P, Lnext, ir, first_bad, bad_base);
+      if (k1 < kd)
+        pivot_warp<NB>(D + static_cast<long long>(k1) * kd + k1, kd, k1, min(NB, kd - k1), P,
+                       Lnext, ir, first_bad, bad_base);
       PROF_MARK(5);
     } else {
       // ---- A_RK <- Z Li ; A_KK <- -Li^T Li
       const int t0 = la ? 0 : 32, t2 = tid - t0, nth = kFT - t0;
-      for (int i = t2 + nth * q; i < kd; i += nth * C) {
+      for (int i = q + C * t2; i < kd; i += nth * C) {  // rows q, q + C, ...
         if (i >= k0 && i < k1) continue;
         double z[NB];
 #pragma unroll
@@ -311,6 +379,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
         D[static_cast<long long>(k0 + a) * kd + k0 + b] = -acc;
       }
     }
+    PROF_MARK(7);
     if (C > 1) cl_sync();  // A_RK, A_KK written cluster-wide before the next Z / pack
     PROF_MARK(4);
   }
@@ -457,7 +526,49 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+__device__ __forceinline__ double2 lds_f64x2(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
+// R per-lane partial sums (R = 4 or 8 rows) -> lane ends with the warp total of row
+// lane / (32 / R): halving exchanges (16, 8[, 4]) then a butterfly over the rest
+template <int R>
+__device__ __forceinline__ double transpose_reduce(double (&acc)[R], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8;
+#pragma unroll
+  for (int k = 0; k < R / 2; ++k) {
+    const double send = b4 ? acc[k] : acc[k + R / 2];
+    const double keep = b4 ? acc[k + R / 2] : acc[k];
+    acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int k = 0; k < R / 4; ++k) {
+    const double send = b3 ? acc[k] : acc[k + R / 4];
+    const double keep = b3 ? acc[k + R / 4] : acc[k];
+    acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  double t = acc[0];
+  if (R == 8) {
+    const bool b2 = lane & 4;
+    const double send = b2 ? acc[0] : acc[1];
+    const double keep = b2 ? acc[1] : acc[0];
+    t = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  } else {
+    t += __shfl_xor_sync(0xffffffffu, t, 4);
+  }
+  t += __shfl_xor_sync(0xffffffffu, t, 2);
+  t += __shfl_xor_sync(0xffffffffu, t, 1);
+  return t;
+}
+
 constexpr int kSW = 16;  // solve warps per CTA: 15 compute + 1 producer
+constexpr int kSolveHdr = 1024;  // mbarriers (0..255) and the chunk table (256..1023)
+constexpr int kMaxChunks = 191;  // chunks of one line per CTA
+// development probe (FFB_SOLVE_DBG): 1 skip the row arithmetic, 2 skip the line exchange,
+// 4 skip the bulk copies. Results are wrong with any bit set; timing decomposition only.
+__device__ int g_solve_dbg = 0;
 constexpr int kST = kSW * 32;
 constexpr int kCW = kSW - 1;
 constexpr int kCT = kCW * 32;
@@ -491,6 +602,25 @@ __device__ __forceinline__ int chain_line(int phase, int chain, int L, int t) {
   return chain == 0 ? m - t : m + t;
 }
 
+// wait with cluster-scope acquire: pairs with remote release-arrivals from the other CTAs
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// arrive (release, cluster scope: covers this CTA's prior shared-memory stores ordered before
+// it by a CTA barrier) on the mbarrier at the same offset in CTA `rank`
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, unsigned rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -525,12 +655,16 @@ __global__ void __launch_bounds__(kST, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + 8;
-  double* stage0 = reinterpret_cast<double*>(smem_raw + 128);
+  const int dbg = g_solve_dbg;
+  uint64_t* red_bar = empty + 8;  // [2]: partial sums for my rows have arrived (line parity)
+  uint64_t* x_bar = red_bar + 2;  // [2]: the other CTAs' x of the line have arrived
+  double* stage0 = reinterpret_cast<double*>(smem_raw + kSolveHdr);
   double* colpart = stage0 + static_cast<size_t>(stages) * cap;  // kCW x kd_max
   double* wv = colpart + static_cast<size_t>(kCW) * kd_max;      // kd_max
   double* yrow = wv + kd_max;                                    // kd_max (own rows)
-  double* xprev = yrow + kd_max;                                 // kd_max
-  double* red = xprev + kd_max;                                  // 8 x kd_max reduce slots
+  double* xbuf = yrow + kd_max;                                  // 2 x kd_max (line parity)
+  double* red = xbuf + 2 * kd_max;                               // 2 x C x kd_max slots
+  double* dcorr = red + 2 * static_cast<size_t>(C) * kd_max;     // kd_max: D_ii w_i
   double* yl = ylocal + s.vec_off;
   double* zl = zlocal + s.vec_off;
   const double* rl = rlocal ? rlocal + s.vec_off : nullptr;  // per-subdomain rhs (RAS mode)
@@ -541,21 +675,32 @@ __global__ void __launch_bounds__(kST, 1)
       mbar_init(&full[q], 1);
       mbar_init(&empty[q], kCW);
     }
+    // point-to-point line exchange between the cluster's CTAs (no cluster-wide barriers):
+    // CTA o receives partial sums from CTAs o+1..C-1 and x from all others
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&red_bar[q], static_cast<uint32_t>(max(C - 1 - crank, 1)));
+      mbar_init(&x_bar[q], static_cast<uint32_t>(max(C - 1, 1)));
+    }
     fence_barrier_init();
   }
-  for (int j = tid; j < kd_max; j += kST) xprev[j] = 0.0;
-  __syncthreads();
+  // chunk boundaries of this CTA's rows, the same for every line: cb[0] = rlo < ... <
+  // cb[nch] = rhi, each chunk's packed rows fitting one ring stage
+  int* cb = reinterpret_cast<int*>(smem_raw + 256);
+  if (tid == 0) {
+    int n = 0, r = rlo;
+    cb[0] = rlo;
+    while (r < rhi && n < kMaxChunks) cb[++n] = r = chunk_end(r, rhi, cap);
+    if (r < rhi) __trap();  // ring stages too small for this line width
+    cb[kMaxChunks] = n;
+  }
+  for (int j = tid; j < 2 * kd_max; j += kST) xbuf[j] = 0.0;
+  if (C > 1) cl_sync(); else __syncthreads();  // barriers initialised cluster-wide
+  const int nch = cb[kMaxChunks];
 
   // ------------------------------------------------------------------ producer warp
   if (warp == kCW) {
-    if (rlo >= rhi) {  // no rows here: still take part in the cluster barriers
-      for (int t = 0; t < nl && C > 1; ++t) {
-        cl_sync();
-        cl_sync();
-      }
-      return;
-    }
-    int q = 0, t_i = 0, r_i = rlo;
+    if (rlo >= rhi) return;
+    int q = 0, t_i = 0, r_i = 0;  // r_i: chunk index within the line
     int line_of[8];  // line of the chunk last placed in each stage
 #pragma unroll
     for (int k = 0; k < 8; ++k) line_of[k] = -1;
@@ -572,32 +717,26 @@ __global__ void __launch_bounds__(kST, 1)
         if (C > 1 && prev_line > t_sync) break;
         if (q >= stages) mbar_wait(&empty[st], ((q / stages) - 1) & 1);
         const int l = chain_line(phase, chain, L, t_i);
-        const int r1 = chunk_end(r_i, rhi, cap);
-        const long long o0 = prow_off(r_i), o1 = prow_off(r1);
+        const int o0 = prow_off32(cb[r_i]), o1 = prow_off32(cb[r_i + 1]);
         if (lane == 0) {
-          fence_proxy_async();
-          mbar_expect_tx(&full[st], static_cast<uint32_t>((o1 - o0) * sizeof(double)));
-          bulk_g2s(stage0 + static_cast<size_t>(st) * cap, F + static_cast<long long>(l) * s.line_sz + o0,
-                   static_cast<uint32_t>((o1 - o0) * sizeof(double)), &full[st]);
+          if (dbg & 4) {
+            mbar_arrive(&full[st]);
+          } else {
+            fence_proxy_async();
+            mbar_expect_tx(&full[st], static_cast<uint32_t>((o1 - o0) * sizeof(double)));
+            bulk_g2s(stage0 + static_cast<size_t>(st) * cap, F + static_cast<long long>(l) * s.line_sz + o0,
+                     static_cast<uint32_t>((o1 - o0) * sizeof(double)), &full[st]);
+          }
         }
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           if (k == st) line_of[k] = t_i;
         ++q;
-        r_i = r1;
-        if (r_i >= rhi) r_i = rlo, ++t_i;
+        if (++r_i == nch) r_i = 0, ++t_i;
       }
     };
-    if (C == 1) {
-      issue_until(1 << 30);
-    } else {
-      for (int t = 0; t < nl; ++t) {
-        issue_until(t);
-        cl_sync();
-        cl_sync();
-      }
-    }
+    issue_until(1 << 30);  // gated by the empty barriers only
     return;
   }
 
@@ -638,7 +777,10 @@ __global__ void __launch_bounds__(kST, 1)
   int c_seq = 0;
   for (int t = 0; t < nl; ++t) {
     const int l = chain_line(phase, chain, L, t);
+    const int par = t & 1;
     const bool subtract = phase == 1 && t > 0;  // x_l = y_l - Dinv_l w
+    const double* xprev = xbuf + (par ^ 1) * kd_max;  // x of line t-1 (zeros at t = 0)
+    if (C > 1 && t > 0 && !(dbg & 2)) mbar_wait_cluster(&x_bar[par ^ 1], ((t - 1) >> 1) & 1);
     double cur_y[PS];
 #pragma unroll
     for (int q = 0; q < PS; ++q) {
@@ -654,6 +796,8 @@ __global__ void __launch_bounds__(kST, 1)
     // lane owns the column pairs j = 64 mm + 2 lane + {0, 1}: operand in registers for the
     // whole line, rows read as 16-byte pairs (row starts are 16-byte aligned)
     constexpr int M2 = (MAXM + 1) / 2;
+    constexpr int RB = M2 <= 4 ? 8 : 4;  // rows per batch (register budget)
+    constexpr bool WREG = M2 <= 7;        // operand pairs in registers, else read per step
     double2 wreg[M2], cacc[M2];
 #pragma unroll
     for (int mm = 0; mm < M2; ++mm) {
@@ -662,69 +806,74 @@ __global__ void __launch_bounds__(kST, 1)
       wreg[mm].y = j + 1 < kd ? wv[j + 1] : 0.0;
       cacc[mm].x = cacc[mm].y = 0.0;
     }
-    int r0 = rlo;
-    while (r0 < rhi) {
-      const int r1 = chunk_end(r0, rhi, cap);
+    for (int ci = 0; ci < nch; ++ci) {
+      const int r0 = cb[ci], r1 = cb[ci + 1];
       const int st = c_seq % stages;
       mbar_wait(&full[st], (c_seq / stages) & 1);
       PROF_MARK(1);
-      const double* Sb = stage0 + static_cast<size_t>(st) * cap - prow_off(r0);
-      // batches of 8 rows per warp: 8 independent accumulation chains, one transpose
-      // reduction (9 shuffles) per batch instead of 5 per row
-      for (int i0 = r0 + warp; i0 < r1; i0 += 8 * kCW) {
-        double racc[8];
+      const double* Sb = stage0 + static_cast<size_t>(st) * cap - prow_off32(r0);
+      // batches of R rows per warp (rows i0 + k kCW): R independent accumulation chains and
+      // one transpose reduction per batch. Row i is read as its padded pairs (the pad is 0):
+      // every lane loads unconditionally and masks by selection, so the R loads of a column
+      // step issue back to back; the diagonal enters both the row dot and the column sums
+      // and is taken out once through dcorr.
+      const uint32_t sbase = smem_u32(Sb) + 16u * lane;
+      for (int i0 = r0 + warp; i0 < r1 && !(dbg & 1); i0 += RB * kCW) {
+        uint32_t ra[RB];
+        double wi[RB], racc[RB];
+        int np[RB];
+        int npmax = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < RB; ++k) {
+          const int i = i0 + k * kCW;
+          const bool ok = i < r1;
+          ra[k] = sbase + 8u * static_cast<uint32_t>(prow_off32(ok ? i : r0));
+          wi[k] = ok ? wv[i] : 0.0;
+          np[k] = ok ? (i + 2) >> 1 : 0;  // pairs in the padded row
+          npmax = max(npmax, np[k]);
           racc[k] = 0.0;
-          const int i = i0 + k * kCW;
-          if (i >= r1) continue;
-          const double* Si = Sb + prow_off(i);
-          const double wi = wv[i];
-#pragma unroll
-          for (int mm = 0; mm < M2; ++mm) {
-            const int j = 64 * mm + 2 * lane;
-            if (64 * mm > i) break;
-            if (j <= i) {
-              const double2 v = *reinterpret_cast<const double2*>(Si + j);
-              const double vy = j + 1 <= i ? v.y : 0.0;
-              racc[k] = fma(v.x, wreg[mm].x, racc[k]);
-              racc[k] = fma(vy, wreg[mm].y, racc[k]);
-              if (j < i) cacc[mm].x = fma(v.x, wi, cacc[mm].x);
-              if (j + 1 < i) cacc[mm].y = fma(v.y, wi, cacc[mm].y);
-            }
-          }
         }
-        {  // transpose reduction: lane ends with the total of row k(lane)
-          const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const double send = b4 ? racc[k] : racc[k + 4];
-            const double keep = b4 ? racc[k + 4] : racc[k];
-            racc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-          }
+        for (int mm = 0; mm < M2; ++mm) {
+          if (32 * mm >= npmax) break;
+          const int pidx = 32 * mm + lane;
+          double2 v[RB];
 #pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const double send = b3 ? racc[k] : racc[k + 2];
-            const double keep = b3 ? racc[k + 2] : racc[k];
-            racc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+          for (int k = 0; k < RB; ++k) v[k] = lds_f64x2(ra[k] + 512u * mm);
+          const double2 w2 = WREG ? wreg[mm] : *reinterpret_cast<const double2*>(wv + 64 * mm + 2 * lane);
+#pragma unroll
+          for (int k = 0; k < RB; ++k) {
+            const bool in = pidx < np[k];
+            v[k].x = in ? v[k].x : 0.0;
+            v[k].y = in ? v[k].y : 0.0;
+            racc[k] = fma(v[k].x, w2.x, racc[k]);
+            racc[k] = fma(v[k].y, w2.y, racc[k]);
           }
-          {
-            const double send = b2 ? racc[0] : racc[1];
-            const double keep = b2 ? racc[1] : racc[0];
-            racc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+          double cx = cacc[mm].x, cy = cacc[mm].y, dx = 0.0, dy = 0.0;
+#pragma unroll
+          for (int k = 0; k < RB; k += 2) {
+            cx = fma(v[k].x, wi[k], cx);
+            cy = fma(v[k].y, wi[k], cy);
+            dx = fma(v[k + 1].x, wi[k + 1], dx);
+            dy = fma(v[k + 1].y, wi[k + 1], dy);
           }
-          racc[0] += __shfl_xor_sync(0xffffffffu, racc[0], 2);
-          racc[0] += __shfl_xor_sync(0xffffffffu, racc[0], 1);
-          const int k = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
-          const int i = i0 + k * kCW;
-          if ((lane & 3) == 0 && i < r1) yrow[i] = racc[0];
+          cacc[mm].x = cx + dx;
+          cacc[mm].y = cy + dy;
         }
+        if (lane < RB) {  // D_ii w_i of row k = lane
+          const int i = i0 + lane * kCW;
+          if (i < r1) dcorr[i] = Sb[prow_off32(i) + i] * wv[i];
+        }
+        // transpose reduction: lane ends with the total of row k(lane)
+        const double tot = transpose_reduce<RB>(racc, lane);
+        const int kk = lane / (32 / RB);
+        const int i = i0 + kk * kCW;
+        if ((lane & (32 / RB - 1)) == 0 && i < r1) yrow[i] = tot;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
       PROF_MARK(2);
       ++c_seq;
-      r0 = r1;
     }
 #pragma unroll
     for (int mm = 0; mm < M2; ++mm) {
@@ -738,27 +887,29 @@ __global__ void __launch_bounds__(kST, 1)
     // scattered to the CTA that owns each row
     int owner = 0;
     for (int j = tid; j < rhi; j += kCT) {
-      double tv = (j >= rlo) ? yrow[j] : 0.0;
+      double tv = (j >= rlo) ? yrow[j] - dcorr[j] : 0.0;
 #pragma unroll 5
       for (int w = 0; w < kCW; ++w) tv += colpart[w * kd_max + j];
       while (owner + 1 < C && row_lo(owner + 1, C, kd) <= j) ++owner;
-      if (C == 1)
-        red[j] = tv;
+      double* slot = red + static_cast<size_t>(par * C + crank) * kd_max;
+      if (owner == crank || (dbg & 2))
+        slot[j] = tv;
       else
-        cl_map(red, static_cast<unsigned>(owner))[crank * kd_max + j] = tv;
+        cl_map(slot, static_cast<unsigned>(owner))[j] = tv;
     }
-    if (C == 1) compute_bar(); else cl_sync();
+    compute_bar();
+    if (C > 1 && !(dbg & 2)) {
+      if (tid == 0)
+        for (int o = 0; o < crank; ++o) mbar_arrive_remote(&red_bar[par], static_cast<unsigned>(o));
+      if (crank < C - 1) mbar_wait_cluster(&red_bar[par], (t >> 1) & 1);
+    }
     PROF_MARK(4);
 #pragma unroll
     for (int q = 0; q < PS; ++q) {
       const int j = rlo + tid + kCT * q;
       if (j >= rhi) continue;
       double tv = 0.0;
-      if (C == 1) {
-        tv = red[j];
-      } else {
-        for (int c = crank; c < C; ++c) tv += red[c * kd_max + j];
-      }
+      for (int c = crank; c < C; ++c) tv += red[static_cast<size_t>(par * C + c) * kd_max + j];
       const long long k = static_cast<long long>(l) * kd + j;
       double v;
       if (!subtract) {
@@ -773,15 +924,21 @@ __global__ void __launch_bounds__(kST, 1)
         v = cur_y[q] - tv;
         zl[k] = v;
       }
-      if (C == 1) {
-        xprev[j] = v;
-      } else {
-        for (int c = 0; c < C; ++c) cl_map(xprev, static_cast<unsigned>(c))[j] = v;
-      }
+      double* xo = xbuf + par * kd_max;
+      xo[j] = v;
+      for (int c = 0; c < C && !(dbg & 2); ++c)
+        if (c != crank) cl_map(xo, static_cast<unsigned>(c))[j] = v;
     }
-    if (C == 1) compute_bar(); else cl_sync();
+    compute_bar();
+    if (C > 1 && tid == 0 && !(dbg & 2))
+      for (int c = 0; c < C; ++c)
+        if (c != crank) mbar_arrive_remote(&x_bar[par], static_cast<unsigned>(c));
     PROF_MARK(5);
   }
+  // every CTA receives x from all others at every line: waiting for the last line's
+  // arrivals means no remote store into this CTA's shared memory is still in flight
+  if (C > 1 && !(dbg & 2)) mbar_wait_cluster(&x_bar[(nl - 1) & 1], ((nl - 1) >> 1) & 1);
+  if (C > 1 && (dbg & 2)) cl_sync();
   PROF_FLUSH(16);
 }
 
@@ -1065,7 +1222,8 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
     const int v = std::atoi(e);
     if (v == 1 || v == 2 || v == 4 || v == 8) C = v;
   }
-  const int lac = C > 1 ? 0 : la;  // the look-ahead pivot is a single-CTA schedule
+  // the look-ahead through D is a single-CTA schedule; the NB = 32 one works in clusters
+  const int lac = (C > 1 && nb != 32) ? 0 : la;
   for (int mid = 0; mid <= 1; ++mid) {
     const int grid = (mid ? nsub : 2 * nsub) * C;
     if (nb == 32) {
@@ -1081,11 +1239,13 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
   }
 }
 
+void set_solve_dbg(int v) { FFB_CUDA(cudaMemcpyToSymbol(g_solve_dbg, &v, sizeof(int))); }
+
 SolvePlan solve_plan(int kd_max, int C) {
   SolvePlan pl{};
   pl.C = C;
-  const size_t fixed =
-      128 + (static_cast<size_t>(kCW) * kd_max + 3 * kd_max + 8 * kd_max) * sizeof(double);
+  const size_t fixed = kSolveHdr + (static_cast<size_t>(kCW) * kd_max + 5 * kd_max +
+                                    2 * static_cast<size_t>(C) * kd_max) * sizeof(double);
   size_t budget = 227 * 1024 - 1024;
   if (const char* e = std::getenv("FFB_SOLVE_SMEM_KB")) budget = static_cast<size_t>(std::atoi(e)) * 1024;
   if (kd_max > 2 * kCT || fixed + 2 * 1024 * sizeof(double) > budget)
@@ -1112,6 +1272,7 @@ SolvePlan solve_plan(int kd_max, int C) {
   pl.kd_max = kd_max;
   pl.ldg = 0;
   if (const char* e = std::getenv("FFB_SOLVE")) pl.ldg = std::string(e) == "ldg";
+
   return pl;
 }
 

@@ -603,6 +603,30 @@ int ffb_debug_prof(unsigned long long* out64, int reset) {
   return guard([&] { debug_prof(out64, reset != 0); });
 }
 
+// development probe: average time of `n` applications of the Schwarz preconditioner with
+// the context's resident factorisation (after a solve), on the current residual vector
+int ffb_debug_time_asm(ffb_ctx* c, int nc, int n, int dbg, double* ms) {
+  return guard([&] {
+    check_ctx(c);
+    if (!c->have_part || !c->r.p) fail("ffb_debug_time_asm: no resident factorisation");
+    cudaEvent_t a, b;
+    FFB_CUDA(cudaEventCreate(&a));
+    FFB_CUDA(cudaEventCreate(&b));
+    set_solve_dbg(dbg);
+    launch_asm(c, nc, c->r.p, nullptr);
+    FFB_CUDA(cudaEventRecord(a, c->st));
+    for (int i = 0; i < n; ++i) launch_asm(c, nc, c->r.p, nullptr);
+    FFB_CUDA(cudaEventRecord(b, c->st));
+    FFB_CUDA(cudaEventSynchronize(b));
+    float t = 0;
+    FFB_CUDA(cudaEventElapsedTime(&t, a, b));
+    *ms = t / n;
+    set_solve_dbg(0);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  });
+}
+
 int ffb_set_stream(ffb_ctx* c, void* stream, int own) {
   return guard([&] {
     check_ctx(c);

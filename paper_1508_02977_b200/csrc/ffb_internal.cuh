@@ -147,6 +147,8 @@ void update_alpha(double* alpha_out, const double* alpha, const double* eta,
 constexpr int kRedBlocks = 592;  // 4 x 148 SMs
 constexpr int kRedThreads = 256;
 
+void set_solve_dbg(int v);  // development probe flags of the solve kernel (band.cu)
+
 // ---- flow metrics (metrics.cu): out = (sum angular error, sum endpoint error, valid);
 // part >= 3 * kRedBlocks doubles, counter zero-initialised (reset by the kernel)
 void flow_metrics(const double* u1, const double* u2, const float* tu, const float* tv,

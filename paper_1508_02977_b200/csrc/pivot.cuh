@@ -12,8 +12,10 @@
 
 namespace ffb {
 
+// src: the block's lower triangle with leading dimension ld (global D or a shared tile,
+// which may alias LR); k0: its first row, for the breakdown index.
 template <int NB>
-__device__ __noinline__ void pivot_warp(const double* __restrict__ D, int kd, int k0, int nbk,
+__device__ __noinline__ void pivot_warp(const double* src, long long ld, int k0, int nbk,
                                         double* LR, double* Li, double* ir, int& first_bad,
                                         int bad_base) {
   static_assert(NB % 2 == 0 && NB <= 32, "pivot block");
@@ -22,9 +24,9 @@ __device__ __noinline__ void pivot_warp(const double* __restrict__ D, int kd, in
 #pragma unroll
   for (int t = 0; t < NB; ++t) {
     const int a = max(t, lane), b = min(t, lane);
-    c[t] = (lane < nbk && t < nbk) ? D[static_cast<long long>(k0 + a) * kd + k0 + b]
-                                   : (t == lane ? 1.0 : 0.0);
+    c[t] = (lane < nbk && t < nbk) ? src[a * ld + b] : (t == lane ? 1.0 : 0.0);
   }
+  __syncwarp();
   int fb = first_bad;
 #pragma unroll 1
   for (int k = 0; k < NB; ++k) {
@@ -67,6 +69,86 @@ __device__ __noinline__ void pivot_warp(const double* __restrict__ D, int kd, in
       c[t] = c[t + 1] - v.y * y;
     }
     c[NB - 1] = 0.0;
+  }
+  __syncwarp();
+}
+
+// The same factorisation by two warps of the CTA (called by both; role = warp & 1): the
+// Cholesky warp publishes each finished column of L through `progress` (a shared counter,
+// value tag * 64 + k + 1 once column k is in LR, unique per call so it never needs a reset)
+// and the substitution warp builds L^-1 one step behind it, so the two serial chains
+// overlap instead of running back to back.
+__device__ __forceinline__ int ld_volatile_shared(const int* p) {
+  int v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];"
+               : "=r"(v)
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+  return v;
+}
+
+template <int NB>
+__device__ __noinline__ void pivot_pair(const double* src, long long ld, int k0, int nbk,
+                                        double* LR, double* Li, double* ir, int& first_bad,
+                                        int bad_base, int* progress, int tag) {
+  static_assert(NB % 2 == 0 && NB <= 32, "pivot block");
+  const int lane = threadIdx.x & 31;
+  double c[NB];
+  if ((threadIdx.x >> 5) % 2 == 0) {  // Cholesky
+#pragma unroll
+    for (int t = 0; t < NB; ++t) {
+      const int a = max(t, lane), b = min(t, lane);
+      c[t] = (lane < nbk && t < nbk) ? src[a * ld + b] : (t == lane ? 1.0 : 0.0);
+    }
+    __syncwarp();
+    int fb = first_bad;
+#pragma unroll 1
+    for (int k = 0; k < NB; ++k) {
+      double dkk = __shfl_sync(~0u, c[0], k);
+      if (!(dkk > 0.0) || !isfinite(dkk)) {
+        if (k < nbk) fb = min(fb, bad_base + k0 + k);
+        dkk = 1.0;
+      }
+      const double r = rsqrt(dkk);
+      const double l = (lane == k) ? dkk * r : c[0] * r;
+      double* row = LR + k * NB;
+      if (lane >= k && lane < NB) row[lane - k] = l;
+      if (lane == k) ir[k] = r;
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        *reinterpret_cast<volatile int*>(progress) = tag * 64 + k + 1;
+      }
+      c[0] = c[1] - row[1] * l;
+#pragma unroll
+      for (int t = 2; t < NB; t += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(row + t);
+        c[t - 1] = c[t] - v.x * l;
+        c[t] = c[t + 1] - v.y * l;
+      }
+      c[NB - 1] = 0.0;
+    }
+    first_bad = fb;
+  } else {  // forward substitution for L^-1, one column of L behind
+#pragma unroll
+    for (int t = 0; t < NB; ++t) c[t] = (t == lane) ? 1.0 : 0.0;
+#pragma unroll 1
+    for (int k = 0; k < NB; ++k) {
+      while (ld_volatile_shared(progress) < tag * 64 + k + 1) {
+      }
+      __syncwarp();
+      __threadfence_block();
+      const double y = c[0] * ir[k];
+      if (lane < NB) Li[k * (NB + 1) + lane] = y;
+      const double* row = LR + k * NB;
+      c[0] = c[1] - row[1] * y;
+#pragma unroll
+      for (int t = 2; t < NB; t += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(row + t);
+        c[t - 1] = c[t] - v.x * y;
+        c[t] = c[t + 1] - v.y * y;
+      }
+      c[NB - 1] = 0.0;
+    }
   }
   __syncwarp();
 }
