@@ -25,4 +25,4 @@ s = r.stats
 print(f"{name}: {dt*1e3:.1f} ms wall, total {s.ms_total:.1f} ms: terms {s.ms_terms:.2f} "
       f"factor {s.ms_factor:.1f} pcg {s.ms_pcg:.1f} adapt {s.ms_adapt:.2f}; iters {s.iters}; "
       f"asm {s.ms_asm_per_iter:.3f} ms/launch = "
-      f"{16*s.factor_doubles/(s.ms_asm_per_iter*1e-3)/1e9 if s.ms_asm_per_iter else 0:.0f} GB/s")
+      f"{8*s.factor_doubles/(s.ms_asm_per_iter*1e-3)/1e9 if s.ms_asm_per_iter else 0:.0f} GB/s")
