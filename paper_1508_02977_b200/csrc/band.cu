@@ -614,12 +614,21 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "r"(parity)
       : "memory");
 }
-// arrive (release, cluster scope: covers this CTA's prior shared-memory stores ordered before
-// it by a CTA barrier) on the mbarrier at the same offset in CTA `rank`
-__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, unsigned rank) {
-  uint32_t ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(rank));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+// asynchronous store of one double into CTA `rank`'s shared memory at the offset of `dst`,
+// completing 8 transaction bytes on that CTA's mbarrier at the offset of `bar`
+__device__ __forceinline__ void st_async_remote(double* dst, double v, uint64_t* bar,
+                                                unsigned rank) {
+  uint32_t ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(dst)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(ra),
+               "d"(v), "r"(rb)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -678,14 +687,16 @@ __global__ void __launch_bounds__(kST, 1)
     // point-to-point line exchange between the cluster's CTAs (no cluster-wide barriers):
     // CTA o receives partial sums from CTAs o+1..C-1 and x from all others
     for (int q = 0; q < 2; ++q) {
-      mbar_init(&red_bar[q], static_cast<uint32_t>(max(C - 1 - crank, 1)));
-      mbar_init(&x_bar[q], static_cast<uint32_t>(max(C - 1, 1)));
+      mbar_init(&red_bar[q], 1);  // armed with the expected bytes by this CTA each use
+      mbar_init(&x_bar[q], 1);
     }
     fence_barrier_init();
   }
   // chunk boundaries of this CTA's rows, the same for every line: cb[0] = rlo < ... <
   // cb[nch] = rhi, each chunk's packed rows fitting one ring stage
   int* cb = reinterpret_cast<int*>(smem_raw + 256);
+  int* rlos = reinterpret_cast<int*>(smem_raw + 192);  // row_lo(c) for c = 0..C
+  if (tid <= C) rlos[tid] = row_lo(tid, C, kd);
   if (tid == 0) {
     int n = 0, r = rlo;
     cb[0] = rlo;
@@ -781,6 +792,13 @@ __global__ void __launch_bounds__(kST, 1)
     const bool subtract = phase == 1 && t > 0;  // x_l = y_l - Dinv_l w
     const double* xprev = xbuf + (par ^ 1) * kd_max;  // x of line t-1 (zeros at t = 0)
     if (C > 1 && t > 0 && !(dbg & 2)) mbar_wait_cluster(&x_bar[par ^ 1], ((t - 1) >> 1) & 1);
+    if (C > 1 && tid == 0 && !(dbg & 2)) {
+      // this line's incoming bytes: partial sums for my rows from CTAs crank+1..C-1, and x
+      // of every row I do not own
+      const uint32_t mine = static_cast<uint32_t>(rhi - rlo);
+      if (crank < C - 1) mbar_arrive_expect(&red_bar[par], 8u * mine * (C - 1 - crank));
+      mbar_arrive_expect(&x_bar[par], 8u * (static_cast<uint32_t>(kd) - mine));
+    }
     double cur_y[PS];
 #pragma unroll
     for (int q = 0; q < PS; ++q) {
@@ -790,7 +808,7 @@ __global__ void __launch_bounds__(kST, 1)
                              : (t == 0 ? pf_r[q] : pf_b[q] * xprev[j]);
       cur_y[q] = pf_y[q];
     }
-    prefetch(t + 1);
+    if (!(dbg & 16)) prefetch(t + 1);
     compute_bar();
     PROF_MARK(0);
     // lane owns the column pairs j = 64 mm + 2 lane + {0, 1}: operand in registers for the
@@ -886,28 +904,24 @@ __global__ void __launch_bounds__(kST, 1)
     // column partials of this CTA (+ its own row dots), reduced in a fixed warp order and
     // scattered to the CTA that owns each row
     int owner = 0;
-    for (int j = tid; j < rhi; j += kCT) {
+    for (int j = tid; j < rhi && !(dbg & 8); j += kCT) {
       double tv = (j >= rlo) ? yrow[j] - dcorr[j] : 0.0;
 #pragma unroll 5
       for (int w = 0; w < kCW; ++w) tv += colpart[w * kd_max + j];
-      while (owner + 1 < C && row_lo(owner + 1, C, kd) <= j) ++owner;
+      while (owner + 1 < C && rlos[owner + 1] <= j) ++owner;
       double* slot = red + static_cast<size_t>(par * C + crank) * kd_max;
       if (owner == crank || (dbg & 2))
         slot[j] = tv;
       else
-        cl_map(slot, static_cast<unsigned>(owner))[j] = tv;
+        st_async_remote(slot + j, tv, &red_bar[par], static_cast<unsigned>(owner));
     }
     compute_bar();
-    if (C > 1 && !(dbg & 2)) {
-      if (tid == 0)
-        for (int o = 0; o < crank; ++o) mbar_arrive_remote(&red_bar[par], static_cast<unsigned>(o));
-      if (crank < C - 1) mbar_wait_cluster(&red_bar[par], (t >> 1) & 1);
-    }
+    if (C > 1 && !(dbg & 2) && crank < C - 1) mbar_wait_cluster(&red_bar[par], (t >> 1) & 1);
     PROF_MARK(4);
 #pragma unroll
     for (int q = 0; q < PS; ++q) {
       const int j = rlo + tid + kCT * q;
-      if (j >= rhi) continue;
+      if (j >= rhi || (dbg & 8)) continue;
       double tv = 0.0;
       for (int c = crank; c < C; ++c) tv += red[static_cast<size_t>(par * C + c) * kd_max + j];
       const long long k = static_cast<long long>(l) * kd + j;
@@ -927,12 +941,9 @@ __global__ void __launch_bounds__(kST, 1)
       double* xo = xbuf + par * kd_max;
       xo[j] = v;
       for (int c = 0; c < C && !(dbg & 2); ++c)
-        if (c != crank) cl_map(xo, static_cast<unsigned>(c))[j] = v;
+        if (c != crank) st_async_remote(xo + j, v, &x_bar[par], static_cast<unsigned>(c));
     }
     compute_bar();
-    if (C > 1 && tid == 0 && !(dbg & 2))
-      for (int c = 0; c < C; ++c)
-        if (c != crank) mbar_arrive_remote(&x_bar[par], static_cast<unsigned>(c));
     PROF_MARK(5);
   }
   // every CTA receives x from all others at every line: waiting for the last line's
