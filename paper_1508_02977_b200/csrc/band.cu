@@ -256,6 +256,97 @@ __device__ __forceinline__ void kk_update(const double* __restrict__ D, int kd, 
   }
 }
 
+// A_RK <- Z L^-1 on rows r0..r0+31 (rows of K skipped): out[u][c] = sum_c2 Z[c2][u] Li[c2][c],
+// written to D[u][k0 + c] (u > k0) or its transpose D[k0 + c][u] (u < k0). Lane: 4 rows x 4
+// columns per pass, NB/16 passes (register budget of the factor kernel).
+template <int NB>
+__device__ __forceinline__ void tile_ark(double* __restrict__ D, int kd, int kdp,
+                                         const double* Z, const double* Li, int r0, int k0,
+                                         int k1, int lane) {
+  constexpr int LDL = li_stride<NB>();
+  const int ui = lane & 7, vi = lane >> 3;
+  const int nbk = k1 - k0;
+#pragma unroll 1
+  for (int pass = 0; pass < NB / 16; ++pass) {
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    const int cb = 16 * pass + 2 * vi;  // columns cb, cb+1, cb+8, cb+9
+#pragma unroll 4
+    for (int c2 = 0; c2 < NB; ++c2) {
+      double a[4], b[4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double2 x = *reinterpret_cast<const double2*>(Z + c2 * kdp + r0 + 2 * ui + 16 * h);
+        a[2 * h] = x.x, a[2 * h + 1] = x.y;
+        const double2 y = *reinterpret_cast<const double2*>(Li + c2 * LDL + cb + 8 * h);
+        b[2 * h] = y.x, b[2 * h + 1] = y.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int u = r0 + 2 * ui + 16 * (i >> 1) + (i & 1);
+      if (u >= kd || (u >= k0 && u < k1)) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = cb + 8 * (j >> 1) + (j & 1);
+        if (c >= nbk) continue;
+        if (u > k0)
+          D[static_cast<long long>(u) * kd + k0 + c] = acc[i][j];
+        else
+          D[static_cast<long long>(k0 + c) * kd + u] = acc[i][j];
+      }
+    }
+  }
+}
+
+// A_KK <- -L^-T L^-1 (lower triangle), one warp (4 rows x 4 columns per lane and pass)
+template <int NB>
+__device__ __forceinline__ void tile_akk(double* __restrict__ D, int kd, const double* Li, int k0,
+                                         int nbk, int lane) {
+  constexpr int LDL = li_stride<NB>();
+  const int ui = lane & 7, vi = lane >> 3;
+#pragma unroll 1
+  for (int pass = 0; pass < NB / 16; ++pass) {
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    const int cb = 16 * pass + 2 * vi;
+    for (int m = 0; m < nbk; ++m) {
+      double a[4], b[4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double2 x = *reinterpret_cast<const double2*>(Li + m * LDL + 2 * ui + 16 * h);
+        a[2 * h] = x.x, a[2 * h + 1] = x.y;
+        const double2 y = *reinterpret_cast<const double2*>(Li + m * LDL + cb + 8 * h);
+        b[2 * h] = y.x, b[2 * h + 1] = y.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = 2 * ui + 16 * (i >> 1) + (i & 1);
+      if (r >= nbk) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = cb + 8 * (j >> 1) + (j & 1);
+        if (c <= r) D[static_cast<long long>(k0 + r) * kd + k0 + c] = -acc[i][j];
+      }
+    }
+  }
+}
+
 // In-place inversion of the SPD line matrix D (kd x kd row-major in global scratch, lower
 // triangle used) by the blocked symmetric sweep; leaves -D^{-1} in the lower triangle.
 // The next step's pivot block is factored by warp 0 while the other 15 warps write the
@@ -266,10 +357,11 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
                              double* ir, int* cnt, double* Z, int& first_bad, int bad_base,
                              int la, int q, int C) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int LS = NB * (NB + 1);
+  constexpr int LDL = li_stride<NB>();
+  constexpr int LS = NB * LDL;
   PROF_DECL
-  if (tid == 0) cnt[0] = 0;
-  if (warp == 0) pivot_warp<NB>(D, kd, 0, min(NB, kd), P, Li2, ir, first_bad, bad_base);
+  if (tid == 0) cnt[0] = 0, cnt[3] = 0;
+  if (warp == 0) pivot_warp<NB>(D, kd, 0, min(NB, kd), P, Li2, ir, first_bad, bad_base, nullptr);
   const bool la_reg = NB == 32 && la;  // look-ahead on a private copy of the next pivot block
   int pv_tag = 0;                      // pivot_pair progress tags (same on every warp)
   if (tid == 0) cnt[2] = 0;
@@ -282,7 +374,10 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
     const double* Li = Li2 + (step & 1) * LS;
     double* Lnext = Li2 + ((step + 1) & 1) * LS;
     __syncthreads();
-    if (tid == 0) cnt[(step + 1) & 1] = 0;  // the queue of the next step (idle since the sync)
+    if (tid == 0) {  // the queues of the next step (idle since the sync)
+      cnt[(step + 1) & 1] = 0;
+      cnt[3 + ((step + 1) & 1)] = 0;
+    }
     PROF_MARK(1);
     // ---- Z = A_RK Li^T, thread per row: all loads issued first, 32 independent chains
     for (int i = tid; i < kdp; i += kFT) {
@@ -297,11 +392,13 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       for (int c = 0; c < NB; ++c) {
         double acc = 0.0;
 #pragma unroll
-        for (int c2 = 0; c2 <= c; ++c2) acc = fma(a[c2], Li[c * (NB + 1) + c2], acc);
+        for (int c2 = 0; c2 <= c; ++c2) acc = fma(a[c2], Li[c * LDL + c2], acc);
         Z[c * kdp + i] = acc;
       }
     }
-    __syncthreads();
+    // la_reg: A_RK is overwritten during this step's tile phase, so every CTA's Z must be
+    // done first (cluster barrier); otherwise a CTA barrier suffices here
+    if (la_reg && C > 1) cl_sync(); else __syncthreads();
     PROF_MARK(2);
     // ---- A_RR -= Z Z^T, 32x32 tiles from a shared queue (tiles q, q + C, ... of the
     // cluster's CTA q). Look-ahead (la, single CTA): warp 0 first finishes the tile holding
@@ -315,9 +412,10 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       // so there is no ordering against the other CTAs' updates.
       kk_update<NB>(D, kd, kdp, Z, nbk, k1, min(NB, kd - k1), P, lane, warp);
       asm volatile("bar.sync 2, 128;" ::: "memory");
+      PROF_MARK(6);
       if (warp < 2)
         pivot_pair<NB>(P, NB + 1, k1, min(NB, kd - k1), P, Lnext, ir, first_bad, bad_base,
-                       cnt + 2, ++pv_tag);
+                       cnt + 2, ++pv_tag, nullptr);
       else
         ++pv_tag;
       PROF_MARK(5);
@@ -326,9 +424,21 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
         rupd_tile(D, kd, kdp, Z, nbk, k0, k1, nx, nx, lane);
         __syncwarp();
         pivot_warp<NB>(D + static_cast<long long>(k1) * kd + k1, kd, k1, min(NB, kd - k1), P,
-                       Lnext, ir, first_bad, bad_base);
+                       Lnext, ir, first_bad, bad_base, nullptr);
       }
       PROF_MARK(5);
+    }
+    if (la_reg) {
+      // A_RK <- Z L^-1 (row tiles q, q + C, ... of the cluster) and A_KK, concurrently with the
+      // trailing updates: they touch only the columns of K, which the tiles exclude
+      if (q == C - 1 && warp == kFW - 1) tile_akk<NB>(D, kd, Li, k0, nbk, lane);
+      for (;;) {
+        int T = 0;
+        if (lane == 0) T = q + C * atomicAdd(cnt + 3 + (step & 1), 1);
+        T = __shfl_sync(~0u, T, 0);
+        if (32 * T >= kd) break;
+        tile_ark<NB>(D, kd, kdp, Z, Li, 32 * T, k0, k1, lane);
+      }
     }
     for (;;) {
       int idx = 0;
@@ -342,42 +452,25 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       rupd_tile(D, kd, kdp, Z, nbk, k0, k1, TU, idx - TU * (TU + 1) / 2, lane);
     }
     // all tile updates (and, across the cluster, all reads of A_RK for Z) are done
-    if (C > 1) cl_sync(); else __syncthreads();
+    if (!la_reg) {
+      if (C > 1) cl_sync(); else __syncthreads();
+    }
     PROF_MARK(3);
-    if (!la && warp == 0) {
+    if (la_reg) {
+      // A_RK, A_KK done in the tile phase
+    } else if (!la && warp == 0) {
       // the next pivot block is final now: factor it while the other warps write A_RK, A_KK
       if (k1 < kd)
         pivot_warp<NB>(D + static_cast<long long>(k1) * kd + k1, kd, k1, min(NB, kd - k1), P,
-                       Lnext, ir, first_bad, bad_base);
+                       Lnext, ir, first_bad, bad_base, nullptr);
       PROF_MARK(5);
     } else {
-      // ---- A_RK <- Z Li ; A_KK <- -Li^T Li
-      const int t0 = la ? 0 : 32, t2 = tid - t0, nth = kFT - t0;
-      for (int i = q + C * t2; i < kd; i += nth * C) {  // rows q, q + C, ...
-        if (i >= k0 && i < k1) continue;
-        double z[NB];
-#pragma unroll
-        for (int c = 0; c < NB; ++c) z[c] = Z[c * kdp + i];
-#pragma unroll
-        for (int c = 0; c < NB; ++c) {
-          if (c < nbk) {
-            double acc = 0.0;
-#pragma unroll
-            for (int c2 = c; c2 < NB; ++c2) acc = fma(z[c2], Li[c2 * (NB + 1) + c], acc);
-            if (i > k0)
-              D[static_cast<long long>(i) * kd + k0 + c] = acc;
-            else
-              D[static_cast<long long>(k0 + c) * kd + i] = acc;
-          }
-        }
-      }
-      for (int e = q == 0 ? t2 : nbk * nbk; e < nbk * nbk; e += nth) {
-        const int a = e / nbk, b = e - a * nbk;
-        if (b > a) continue;
-        double acc = 0.0;
-        for (int mm = a; mm < nbk; ++mm) acc += Li[mm * (NB + 1) + a] * Li[mm * (NB + 1) + b];
-        D[static_cast<long long>(k0 + a) * kd + k0 + b] = -acc;
-      }
+      // ---- A_RK <- Z Li ; A_KK <- -Li^T Li, as 32x32 tiles (4x8 per lane): row tiles
+      // q, q + C, ... of the cluster over this CTA's participating warps; A_KK by one warp
+      const int w0 = la ? 0 : 1, nw = kFW - w0, wi = warp - w0;
+      for (int T = q + C * wi; 32 * T < kd; T += C * nw)
+        tile_ark<NB>(D, kd, kdp, Z, Li, 32 * T, k0, k1, lane);
+      if (q == C - 1 && warp == kFW - 1) tile_akk<NB>(D, kd, Li, k0, nbk, lane);
     }
     PROF_MARK(7);
     if (C > 1) cl_sync();  // A_RK, A_KK written cluster-wide before the next Z / pack
@@ -453,11 +546,12 @@ __global__ void __launch_bounds__(kFT, 1)
   double* D = scratch + (mid ? sub : cid) * scratch_stride;
   double* F = fac + s.fac_off;
   extern __shared__ __align__(16) double fsm[];
-  double* P = fsm;                    // NB x (NB+1)
-  double* Li = P + NB * (NB + 1);     // 2 x NB x (NB+1)
-  double* ir = Li + 2 * NB * (NB + 1);  // NB
+  constexpr int LDL = li_stride<NB>();
+  double* P = fsm;                      // NB x (NB+1)
+  double* Li = P + NB * (NB + 1);       // 2 x NB x LDL (double-buffered L^-1)
+  double* ir = Li + 2 * NB * LDL;       // NB
   int* cnt = reinterpret_cast<int*>(ir + NB);
-  double* Z = ir + 2 * NB;            // NB x kdp
+  double* Z = ir + 2 * NB;              // NB x kdp
   for (int e = tid; e < NB * kdp; e += kFT) Z[e] = 0.0;
   int first_bad = 0x7fffffff;
   PROF_DECL
@@ -814,8 +908,12 @@ __global__ void __launch_bounds__(kST, 1)
     // lane owns the column pairs j = 64 mm + 2 lane + {0, 1}: operand in registers for the
     // whole line, rows read as 16-byte pairs (row starts are 16-byte aligned)
     constexpr int M2 = (MAXM + 1) / 2;
-    constexpr int RB = M2 <= 4 ? 8 : 4;  // rows per batch (register budget)
-    constexpr bool WREG = M2 <= 7;        // operand pairs in registers, else read per step
+#ifndef FFB_RB7
+#define FFB_RB7 4
+#endif
+    // rows per batch and operand placement within the 128-register budget
+    constexpr int RB = M2 <= 4 ? 8 : (M2 <= 7 ? FFB_RB7 : 4);
+    constexpr bool WREG = M2 <= 4 || (M2 <= 7 && RB == 4);
     double2 wreg[M2], cacc[M2];
 #pragma unroll
     for (int mm = 0; mm < M2; ++mm) {
@@ -1227,7 +1325,8 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
     const char* e = std::getenv("FFB_LOOKAHEAD");
     return e ? std::atoi(e) : 1;
   }();
-  const size_t smem = (3 * nb * (nb + 1) + 2 * nb + static_cast<size_t>(nb) * kdp) * sizeof(double);
+  const size_t smem = (nb * (nb + 1) + 2 * nb * (nb + 2) + 2 * nb + static_cast<size_t>(nb) * kdp) *
+                      sizeof(double);
   if (smem > 227 * 1024) fail("linsolve.cholesky: subdomain line too wide for shared memory");
   if (const char* e = std::getenv("FFB_FCLUSTER")) {
     const int v = std::atoi(e);
@@ -1253,6 +1352,7 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
 void set_solve_dbg(int v) { FFB_CUDA(cudaMemcpyToSymbol(g_solve_dbg, &v, sizeof(int))); }
 
 SolvePlan solve_plan(int kd_max, int C) {
+  kd_max = (kd_max + 1) & ~1;  // even: the per-line shared arrays stay 16-byte aligned
   SolvePlan pl{};
   pl.C = C;
   const size_t fixed = kSolveHdr + (static_cast<size_t>(kCW) * kd_max + 5 * kd_max +

@@ -12,12 +12,18 @@
 
 namespace ffb {
 
+// row stride of the L^-1 tiles (even: rows stay 16-byte aligned for paired loads)
+template <int NB>
+__host__ __device__ constexpr int li_stride() {
+  return NB + 2;
+}
+
 // src: the block's lower triangle with leading dimension ld (global D or a shared tile,
 // which may alias LR); k0: its first row, for the breakdown index.
 template <int NB>
 __device__ __noinline__ void pivot_warp(const double* src, long long ld, int k0, int nbk,
                                         double* LR, double* Li, double* ir, int& first_bad,
-                                        int bad_base) {
+                                        int bad_base, double* LiT) {
   static_assert(NB % 2 == 0 && NB <= 32, "pivot block");
   const int lane = threadIdx.x & 31;
   double c[NB];
@@ -59,7 +65,10 @@ __device__ __noinline__ void pivot_warp(const double* src, long long ld, int k0,
 #pragma unroll 1
   for (int k = 0; k < NB; ++k) {
     const double y = c[0] * ir[k];
-    if (lane < NB) Li[k * (NB + 1) + lane] = y;
+    if (lane < NB) {
+      Li[k * li_stride<NB>() + lane] = y;
+      if (LiT) LiT[lane * li_stride<NB>() + k] = y;
+    }
     const double* row = LR + k * NB;
     c[0] = c[1] - row[1] * y;
 #pragma unroll
@@ -78,18 +87,25 @@ __device__ __noinline__ void pivot_warp(const double* src, long long ld, int k0,
 // value tag * 64 + k + 1 once column k is in LR, unique per call so it never needs a reset)
 // and the substitution warp builds L^-1 one step behind it, so the two serial chains
 // overlap instead of running back to back.
-__device__ __forceinline__ int ld_volatile_shared(const int* p) {
+__device__ __forceinline__ int ld_acquire_shared(const int* p) {
   int v;
-  asm volatile("ld.volatile.shared.u32 %0, [%1];"
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
                : "=r"(v)
-               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p)))
+               : "memory");
   return v;
+}
+__device__ __forceinline__ void st_release_shared(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(p))),
+               "r"(v)
+               : "memory");
 }
 
 template <int NB>
 __device__ __noinline__ void pivot_pair(const double* src, long long ld, int k0, int nbk,
                                         double* LR, double* Li, double* ir, int& first_bad,
-                                        int bad_base, int* progress, int tag) {
+                                        int bad_base, int* progress, int tag, double* LiT) {
   static_assert(NB % 2 == 0 && NB <= 32, "pivot block");
   const int lane = threadIdx.x & 31;
   double c[NB];
@@ -101,23 +117,28 @@ __device__ __noinline__ void pivot_pair(const double* src, long long ld, int k0,
     }
     __syncwarp();
     int fb = first_bad;
+    // software-pipelined: the next pivot (lane k+1's updated diagonal, c[1] - l^2 with its
+    // own l) and its rsqrt are formed before this step's column update is issued
+    double dkk = __shfl_sync(~0u, c[0], 0);
+    if (!(dkk > 0.0) || !isfinite(dkk)) {
+      if (0 < nbk) fb = min(fb, bad_base + k0);
+      dkk = 1.0;
+    }
+    double r = rsqrt(dkk);
 #pragma unroll 1
     for (int k = 0; k < NB; ++k) {
-      double dkk = __shfl_sync(~0u, c[0], k);
-      if (!(dkk > 0.0) || !isfinite(dkk)) {
-        if (k < nbk) fb = min(fb, bad_base + k0 + k);
-        dkk = 1.0;
-      }
-      const double r = rsqrt(dkk);
       const double l = (lane == k) ? dkk * r : c[0] * r;
+      double dn = __shfl_sync(~0u, c[1] - l * l, (k + 1) & 31);
+      if (k + 1 < NB && (!(dn > 0.0) || !isfinite(dn))) {
+        if (k + 1 < nbk) fb = min(fb, bad_base + k0 + k + 1);
+        dn = 1.0;
+      }
+      const double rn = rsqrt(dn);
       double* row = LR + k * NB;
       if (lane >= k && lane < NB) row[lane - k] = l;
       if (lane == k) ir[k] = r;
       __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();
-        *reinterpret_cast<volatile int*>(progress) = tag * 64 + k + 1;
-      }
+      if (lane == 0) st_release_shared(progress, tag * 64 + k + 1);
       c[0] = c[1] - row[1] * l;
 #pragma unroll
       for (int t = 2; t < NB; t += 2) {
@@ -126,6 +147,8 @@ __device__ __noinline__ void pivot_pair(const double* src, long long ld, int k0,
         c[t] = c[t + 1] - v.y * l;
       }
       c[NB - 1] = 0.0;
+      dkk = dn;
+      r = rn;
     }
     first_bad = fb;
   } else {  // forward substitution for L^-1, one column of L behind
@@ -133,12 +156,14 @@ __device__ __noinline__ void pivot_pair(const double* src, long long ld, int k0,
     for (int t = 0; t < NB; ++t) c[t] = (t == lane) ? 1.0 : 0.0;
 #pragma unroll 1
     for (int k = 0; k < NB; ++k) {
-      while (ld_volatile_shared(progress) < tag * 64 + k + 1) {
+      while (ld_acquire_shared(progress) < tag * 64 + k + 1) {
       }
       __syncwarp();
-      __threadfence_block();
       const double y = c[0] * ir[k];
-      if (lane < NB) Li[k * (NB + 1) + lane] = y;
+      if (lane < NB) {
+        Li[k * li_stride<NB>() + lane] = y;
+        if (LiT) LiT[lane * li_stride<NB>() + k] = y;
+      }
       const double* row = LR + k * NB;
       c[0] = c[1] - row[1] * y;
 #pragma unroll

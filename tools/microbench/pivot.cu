@@ -6,28 +6,37 @@
 #include <cuda_runtime.h>
 #include "pivot.cuh"
 
-template <int NB>
+template <int NB, int PAIR>
 __global__ void k(const double* D, int kd, double* out, long long* cyc, int reps) {
   __shared__ __align__(16) double LR[NB * (NB + 1)];
-  __shared__ double Li[NB * (NB + 1)], ir[NB];
+  __shared__ __align__(16) double Li[NB * (NB + 2)];
+  __shared__ double ir[NB];
+  __shared__ int progress;
   int bad = 1 << 30;
-  if (threadIdx.x < 32) {
-    __syncwarp();
+  if (threadIdx.x == 0) progress = 0;
+  __syncthreads();
+  if (threadIdx.x < (PAIR ? 64 : 32)) {
     long long t0 = clock64();
-    for (int r = 0; r < reps; ++r) ffb::pivot_warp<NB>(D, kd, 0, NB, LR, Li, ir, bad, 0);
+    for (int r = 0; r < reps; ++r) {
+      if (PAIR)
+        ffb::pivot_pair<NB>(D, kd, 0, NB, LR, Li, ir, bad, 0, &progress, r + 1, nullptr);
+      else
+        ffb::pivot_warp<NB>(D, kd, 0, NB, LR, Li, ir, bad, 0, nullptr);
+      asm volatile("bar.sync 1, %0;" ::"r"(PAIR ? 64 : 32));
+    }
     long long t1 = clock64();
     if (threadIdx.x == 0) cyc[0] = (t1 - t0) / reps;
-    for (int i = threadIdx.x; i < NB * NB; i += 32) out[i] = Li[(i / NB) * (NB + 1) + i % NB];
+    for (int i = threadIdx.x; i < NB * NB; i += 32) out[i] = Li[(i / NB) * (NB + 2) + i % NB];
   }
 }
 
-template <int NB>
+template <int NB, int PAIR>
 void run(const double* D, int kd, const double* h) {
   double* out;
   long long* cyc;
   cudaMallocManaged(&out, NB * NB * 8);
   cudaMallocManaged(&cyc, 8);
-  k<NB><<<1, 512>>>(D, kd, out, cyc, 20);
+  k<NB, PAIR><<<1, 512>>>(D, kd, out, cyc, 20);
   cudaDeviceSynchronize();
   // host: L = chol(A), check Li L = I
   double L[32][32] = {};
@@ -48,7 +57,7 @@ void run(const double* D, int kd, const double* h) {
       for (int q = 0; q < NB; ++q) s += out[i * NB + q] * L[q][j];
       err = std::fmax(err, std::fabs(s - (i == j)));
     }
-  printf("NB%d pivot %lld cyc, |Li L - I| = %.2e (%s)\n", NB, *cyc, err,
+  printf("NB%d %s %lld cyc, |Li L - I| = %.2e (%s)\n", NB, PAIR ? "pivot_pair" : "pivot_warp", *cyc, err,
          cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -61,7 +70,9 @@ int main() {
   cudaMalloc(&D, sizeof(h));
   cudaMemcpy(D, h, sizeof(h), cudaMemcpyHostToDevice);
   for (int it = 0; it < 2; ++it) {
-    run<32>(D, kd, h);
-    run<16>(D, kd, h);
+    run<32, 0>(D, kd, h);
+    run<32, 1>(D, kd, h);
+    run<16, 0>(D, kd, h);
+    run<16, 1>(D, kd, h);
   }
 }

@@ -21,7 +21,7 @@ fn = ["buildD", "pivot", "Z", "Rupd", "X+sync", "line"]
 vals = [buf[0], buf[33], buf[34], buf[35], buf[36], buf[5]]
 tot = sum(vals) or 1
 print("factor CTA0 cycles:", {fn[i]: f"{vals[i]/1e6:.1f}M ({100*vals[i]/tot:.0f}%)" for i in range(6)})
-print("  warp0: special tile %.1fM pivot %.1fM (top sync %.1fM) X-work %.1fM" % (buf[37]/1e6, buf[38]/1e6, buf[33]/1e6, buf[39]/1e6))
+print("  warp0: kk tile %.1fM pivot %.1fM (top sync %.1fM) X-work %.1fM" % (buf[38]/1e6, buf[37]/1e6, buf[33]/1e6, buf[39]/1e6))
 sn = ["operand", "fullwait", "rows", "colflush", "reduce+sync", "owner+sync"]
 tot = sum(buf[16 + i] for i in range(6)) or 1
 print("solve CTA0 cycles:", {sn[i]: f"{buf[16+i]/1e6:.2f}M ({100*buf[16+i]/tot:.0f}%)" for i in range(6)})
