@@ -144,10 +144,15 @@ __device__ __forceinline__ T* cl_map(T* p, unsigned rank) {
 
 // rows [row_lo(c), row_lo(c+1)) of a packed lower triangle of size kd: equal shares of the
 // kd(kd+1)/2 entries (cumulative work ~ i^2/2)
-__device__ __forceinline__ int row_lo(int c, int C, int kd) {
+// Cost model: a row costs its entries plus rc (its batch setup and reduction share), so the
+// CTA holding the many short leading rows is not the cluster's straggler.
+__device__ __forceinline__ int row_lo(int c, int C, int kd, int rc = 0) {
   if (c <= 0) return 0;
   if (c >= C) return kd;
-  int r = static_cast<int>(kd * sqrt(static_cast<double>(c) / C) + 0.5);
+  const double a = rc + 0.5;
+  const double total = 0.5 * kd * kd + a * kd;  // F(r) = r^2/2 + a r
+  const double target = total * c / C;
+  int r = static_cast<int>(-a + sqrt(a * a + 2.0 * target) + 0.5);
   return min(max(r, c), kd - (C - c));
 }
 
@@ -743,7 +748,7 @@ __global__ void __launch_bounds__(kST, 1)
     k_line_solve(const SubInfo* __restrict__ subs, const double* __restrict__ fac,
                  const double* __restrict__ coef, size_t N, const double* __restrict__ r,
                  double* __restrict__ ylocal, double* __restrict__ zlocal, int W, int nc,
-                 int stages, int cap, int kd_max, int phase, const int* __restrict__ flags,
+                 int stages, int cap, int kd_max, int rc, int phase, const int* __restrict__ flags,
                  const double* __restrict__ rlocal) {
   if (flags && (flags[0] | flags[1])) return;  // PCG converged or failed (grid-uniform)
   const int C = static_cast<int>(cl_size()), crank = static_cast<int>(cl_rank());
@@ -753,7 +758,7 @@ __global__ void __launch_bounds__(kST, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kd = s.kd, L = s.L, m = mid_line(L);
   const int nl = chain_len(phase, chain, L);
-  const int rlo = row_lo(crank, C, kd), rhi = row_lo(crank + 1, C, kd);
+  const int rlo = row_lo(crank, C, kd, rc), rhi = row_lo(crank + 1, C, kd, rc);
   const double* F = fac + s.fac_off;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -790,7 +795,7 @@ __global__ void __launch_bounds__(kST, 1)
   // cb[nch] = rhi, each chunk's packed rows fitting one ring stage
   int* cb = reinterpret_cast<int*>(smem_raw + 256);
   int* rlos = reinterpret_cast<int*>(smem_raw + 192);  // row_lo(c) for c = 0..C
-  if (tid <= C) rlos[tid] = row_lo(tid, C, kd);
+  if (tid <= C) rlos[tid] = row_lo(tid, C, kd, rc);
   if (tid == 0) {
     int n = 0, r = rlo;
     cb[0] = rlo;
@@ -1354,6 +1359,9 @@ void set_solve_dbg(int v) { FFB_CUDA(cudaMemcpyToSymbol(g_solve_dbg, &v, sizeof(
 SolvePlan solve_plan(int kd_max, int C) {
   kd_max = (kd_max + 1) & ~1;  // even: the per-line shared arrays stay 16-byte aligned
   SolvePlan pl{};
+  // measured (tools/solve_probe.py): 16 for lines up to 512 unknowns (c2: -12%), 0 beyond
+  pl.row_cost = kd_max <= 512 ? 16 : 0;
+  if (const char* e = std::getenv("FFB_ROW_COST")) pl.row_cost = std::atoi(e);
   pl.C = C;
   const size_t fixed = kSolveHdr + (static_cast<size_t>(kCW) * kd_max + 5 * kd_max +
                                     2 * static_cast<size_t>(C) * kd_max) * sizeof(double);
@@ -1399,7 +1407,7 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
                      N, r, ylocal, zlocal, W, nc, pl.kd_max, phase, flags, rlocal);
     } else {
       launch_cluster(k_line_solve<M>, 2 * nsub * pl.C, kST, pl.smem, pl.C, st, d_subs, fac, coef,
-                     N, r, ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, phase, flags,
+                     N, r, ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, pl.row_cost, phase, flags,
                      rlocal);
     }
     FFB_LAUNCHED();
