@@ -196,6 +196,125 @@ inline double error_indicator(Context& c, const DataTerms& dt, const RegField& r
   return em;
 }
 
+// ---- linsolve: linsolve.hpp:10-62 on an explicit CSR SparseSystem -----------------------
+enum class SolveMethod { DirectCholesky = FFB_SOLVE_CHOLESKY, ConjugateGradient = FFB_SOLVE_CG };
+struct SolverConfig {
+  SolveMethod method = SolveMethod::DirectCholesky;
+  double cg_tolerance = 1e-10;
+  int cg_max_iters = 0;  // 0 -> 10 n
+};
+struct SolveReport {
+  int iterations = 0;
+  double residual = 0.0;
+};
+// the CSR part of assembly.hpp:43-53 (free vertex major, component minor, both triangles)
+struct SparseSystem {
+  int n = 0;
+  int components = 3;
+  std::vector<int> row_ptr, cols;
+  std::vector<double> vals, rhs;
+};
+
+inline std::vector<double> spmv(Context& c, const SparseSystem& s, const std::vector<double>& x) {
+  std::vector<double> y(s.n);
+  check(ffb_csr_spmv(c.get(), s.n, s.row_ptr.data(), s.cols.data(), s.vals.data(), x.data(),
+                     y.data()));
+  return y;
+}
+
+inline std::vector<int> rcm_order(const SparseSystem& s) {
+  std::vector<int> perm(s.n);
+  check(ffb_rcm_order(s.n, s.components, s.row_ptr.data(), s.cols.data(), perm.data()));
+  return perm;
+}
+
+inline std::vector<double> cg_solve(Context& c, const SparseSystem& s, const SolverConfig& cfg,
+                                    const std::vector<double>* warm_start = nullptr,
+                                    SolveReport* report = nullptr) {
+  std::vector<double> x(s.n);
+  SolveReport r;
+  const double* w = warm_start && static_cast<int>(warm_start->size()) == s.n ? warm_start->data()
+                                                                            : nullptr;
+  const int rc = ffb_csr_cg_solve(c.get(), s.n, s.row_ptr.data(), s.cols.data(), s.vals.data(),
+                                  s.rhs.data(), cfg.cg_tolerance, cfg.cg_max_iters, w, x.data(),
+                                  &r.iterations, &r.residual);
+  if (report) *report = r;
+  check(rc);
+  return x;
+}
+
+inline std::vector<double> solve(Context& c, const SparseSystem& s, const SolverConfig& cfg,
+                                 SolveReport* report = nullptr,
+                                 const std::vector<double>* warm_start = nullptr) {
+  std::vector<double> x(s.n);
+  SolveReport r;
+  const double* w = warm_start && static_cast<int>(warm_start->size()) == s.n ? warm_start->data()
+                                                                            : nullptr;
+  const int rc = ffb_csr_solve(c.get(), s.n, s.components, s.row_ptr.data(), s.cols.data(),
+                               s.vals.data(), s.rhs.data(), static_cast<int>(cfg.method),
+                               cfg.cg_tolerance, cfg.cg_max_iters, w, x.data(), &r.iterations,
+                               &r.residual);
+  if (report) *report = r;
+  check(rc);
+  return x;
+}
+
+// ---- I/O and evaluation: imaging.hpp load_image / save_pgm, metrics.hpp -----------------
+inline Image load_image(const std::string& path) {
+  Image img;
+  check(ffb_load_image(path.c_str(), &img.width, &img.height, nullptr));
+  img.data.resize(static_cast<size_t>(img.width) * img.height);
+  check(ffb_load_image(path.c_str(), &img.width, &img.height, img.data.data()));
+  return img;
+}
+
+inline void save_pgm(const std::string& path, const Image& img) {
+  check(ffb_save_pgm(path.c_str(), img.width, img.height, img.data.data()));
+}
+
+struct FloField {
+  int width = 0, height = 0;
+  std::vector<float> u, v;
+};
+
+inline FloField read_flo(const std::string& path) {
+  FloField f;
+  check(ffb_read_flo(path.c_str(), &f.width, &f.height, nullptr, nullptr));
+  f.u.resize(static_cast<size_t>(f.width) * f.height);
+  f.v.resize(f.u.size());
+  check(ffb_read_flo(path.c_str(), &f.width, &f.height, f.u.data(), f.v.data()));
+  return f;
+}
+
+inline void write_flo(const std::string& path, const FloField& f) {
+  check(ffb_write_flo(path.c_str(), f.width, f.height, f.u.data(), f.v.data()));
+}
+
+inline FloField to_flo(const FlowState& s) {
+  FloField f;
+  f.width = s.width;
+  f.height = s.height;
+  f.u.assign(s.u1.begin(), s.u1.end());
+  f.v.assign(s.u2.begin(), s.u2.end());
+  return f;
+}
+
+struct FlowMetrics {
+  double aae_deg = 0.0, ee = 0.0;
+  long valid = 0;
+};
+
+inline FlowMetrics compute_metrics(Context& c, const FlowState& flow, const FloField& truth) {
+  if (flow.width != truth.width || flow.height != truth.height)
+    throw std::runtime_error("metrics.compute_metrics: flow and ground truth sizes differ");
+  FlowMetrics m;
+  long long valid = 0;
+  check(ffb_compute_metrics(c.get(), truth.width, truth.height, flow.u1.data(), flow.u2.data(),
+                            truth.u.data(), truth.v.data(), &m.aae_deg, &m.ee, &valid));
+  m.valid = static_cast<long>(valid);
+  return m;
+}
+
 // ---- pipeline: pipeline.hpp:53 (converged-pass protocol) --------------------------------
 inline RunResult run_on_frames(Context& c, const Image& f0, const Image& f1,
                                const RunConfig& cfg) {
