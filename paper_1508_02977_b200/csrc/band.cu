@@ -352,6 +352,59 @@ __device__ __forceinline__ void tile_akk(double* __restrict__ D, int kd, const d
   }
 }
 
+// The same tile update on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64): a warp holds
+// the 32x32 tile as 4x4 accumulator blocks of 8x8 (2 doubles per lane each); per k-step of 4
+// pivot columns it loads one A fragment per row block and one B fragment per column block
+// (8 shared-memory loads for 16 MMAs = 4096 FMAs), a quarter of the operand traffic of the
+// 4x8 FFMA register tile, which is shared-memory bound on wide lines.
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void rupd_tile_mma(double* __restrict__ D, int kd, int kdp,
+                                              const double* __restrict__ Z, int nbk, int k0,
+                                              int k1, int TU, int TV, int lane) {
+  const int g = lane >> 2, t = lane & 3;  // fragment row/col group, thread in group
+  const int u0 = 32 * TU, v0 = 32 * TV;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const bool diag = TU == TV;
+#pragma unroll 2
+  for (int c0 = 0; c0 < nbk; c0 += 4) {
+    const double* zc = Z + (c0 + t) * kdp;  // A[m][k] = Z[c0+k][u0+m], B[k][n] = Z[c0+k][v0+n]
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = zc[u0 + 8 * i + g];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = diag ? a[j] : zc[v0 + 8 * j + g];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (!diag || j <= i) dmma_8x8x4(acc[i][j], a[i], b[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int u = u0 + 8 * i + g;
+    if (u >= kd || (u >= k0 && u < k1)) continue;
+    double* rowp = D + static_cast<long long>(u) * kd;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (diag && j > i) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int v = v0 + 8 * j + 2 * t + h;
+        if (v <= u && (v < k0 || v >= k1)) rowp[v] -= acc[i][j][h];
+      }
+    }
+  }
+}
+
 // In-place inversion of the SPD line matrix D (kd x kd row-major in global scratch, lower
 // triangle used) by the blocked symmetric sweep; leaves -D^{-1} in the lower triangle.
 // The next step's pivot block is factored by warp 0 while the other 15 warps write the
@@ -361,6 +414,11 @@ template <int NB>
 __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P, double* Li2,
                              double* ir, int* cnt, double* Z, int& first_bad, int bad_base,
                              int la, int q, int C) {
+  const bool use_mma = la & 2;  // tile updates on the FP64 tensor cores
+  la &= 1;
+  // Z row stride: kdp + 8 doubles puts the 4 pivot-column rows a DMMA fragment load touches
+  // on alternating 64-byte bank halves (2 wavefronts per load instead of 4)
+  const int zs = kdp + 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int LDL = li_stride<NB>();
   constexpr int LS = NB * LDL;
@@ -398,7 +456,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
         double acc = 0.0;
 #pragma unroll
         for (int c2 = 0; c2 <= c; ++c2) acc = fma(a[c2], Li[c * LDL + c2], acc);
-        Z[c * kdp + i] = acc;
+        Z[c * zs + i] = acc;
       }
     }
     // la_reg: A_RK is overwritten during this step's tile phase, so every CTA's Z must be
@@ -415,7 +473,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       // pivot (A_KK is overwritten at its own step). Every CTA of the cluster updates a
       // private copy in P (warps 0-3) and factors it (warp 0); nobody writes the tile back,
       // so there is no ordering against the other CTAs' updates.
-      kk_update<NB>(D, kd, kdp, Z, nbk, k1, min(NB, kd - k1), P, lane, warp);
+      kk_update<NB>(D, kd, zs, Z, nbk, k1, min(NB, kd - k1), P, lane, warp);
       asm volatile("bar.sync 2, 128;" ::: "memory");
       PROF_MARK(6);
       if (warp < 2)
@@ -426,7 +484,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       PROF_MARK(5);
     } else if (warp == 0 && special >= 0) {
       {
-        rupd_tile(D, kd, kdp, Z, nbk, k0, k1, nx, nx, lane);
+        rupd_tile(D, kd, zs, Z, nbk, k0, k1, nx, nx, lane);
         __syncwarp();
         pivot_warp<NB>(D + static_cast<long long>(k1) * kd + k1, kd, k1, min(NB, kd - k1), P,
                        Lnext, ir, first_bad, bad_base, nullptr);
@@ -442,7 +500,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
         if (lane == 0) T = q + C * atomicAdd(cnt + 3 + (step & 1), 1);
         T = __shfl_sync(~0u, T, 0);
         if (32 * T >= kd) break;
-        tile_ark<NB>(D, kd, kdp, Z, Li, 32 * T, k0, k1, lane);
+        tile_ark<NB>(D, kd, zs, Z, Li, 32 * T, k0, k1, lane);
       }
     }
     for (;;) {
@@ -454,7 +512,10 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       int TU = static_cast<int>((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
       while (TU * (TU + 1) / 2 > idx) --TU;
       while ((TU + 1) * (TU + 2) / 2 <= idx) ++TU;
-      rupd_tile(D, kd, kdp, Z, nbk, k0, k1, TU, idx - TU * (TU + 1) / 2, lane);
+      if (use_mma)
+        rupd_tile_mma(D, kd, zs, Z, nbk, k0, k1, TU, idx - TU * (TU + 1) / 2, lane);
+      else
+        rupd_tile(D, kd, zs, Z, nbk, k0, k1, TU, idx - TU * (TU + 1) / 2, lane);
     }
     // all tile updates (and, across the cluster, all reads of A_RK for Z) are done
     if (!la_reg) {
@@ -474,7 +535,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       // q, q + C, ... of the cluster over this CTA's participating warps; A_KK by one warp
       const int w0 = la ? 0 : 1, nw = kFW - w0, wi = warp - w0;
       for (int T = q + C * wi; 32 * T < kd; T += C * nw)
-        tile_ark<NB>(D, kd, kdp, Z, Li, 32 * T, k0, k1, lane);
+        tile_ark<NB>(D, kd, zs, Z, Li, 32 * T, k0, k1, lane);
       if (q == C - 1 && warp == kFW - 1) tile_akk<NB>(D, kd, Li, k0, nbk, lane);
     }
     PROF_MARK(7);
@@ -557,7 +618,7 @@ __global__ void __launch_bounds__(kFT, 1)
   double* ir = Li + 2 * NB * LDL;       // NB
   int* cnt = reinterpret_cast<int*>(ir + NB);
   double* Z = ir + 2 * NB;              // NB x kdp
-  for (int e = tid; e < NB * kdp; e += kFT) Z[e] = 0.0;
+  for (int e = tid; e < NB * (kdp + 8); e += kFT) Z[e] = 0.0;
   int first_bad = 0x7fffffff;
   PROF_DECL
   if (mid) {
@@ -1330,7 +1391,7 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
     const char* e = std::getenv("FFB_LOOKAHEAD");
     return e ? std::atoi(e) : 1;
   }();
-  const size_t smem = (nb * (nb + 1) + 2 * nb * (nb + 2) + 2 * nb + static_cast<size_t>(nb) * kdp) *
+  const size_t smem = (nb * (nb + 1) + 2 * nb * (nb + 2) + 2 * nb + static_cast<size_t>(nb) * (kdp + 8)) *
                       sizeof(double);
   if (smem > 227 * 1024) fail("linsolve.cholesky: subdomain line too wide for shared memory");
   if (const char* e = std::getenv("FFB_FCLUSTER")) {
@@ -1338,7 +1399,14 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
     if (v == 1 || v == 2 || v == 4 || v == 8) C = v;
   }
   // the look-ahead through D is a single-CTA schedule; the NB = 32 one works in clusters
-  const int lac = (C > 1 && nb != 32) ? 0 : la;
+  int lac = (C > 1 && nb != 32) ? 0 : la;
+  // DMMA tile updates (FFB_FACTOR_MMA=0: the FFMA register tiles): measured c2 -9%,
+  // c3 -13%, c5 -20% of the factorisation time
+  static const int mma = [] {
+    const char* e = std::getenv("FFB_FACTOR_MMA");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (mma) lac |= 2;
   for (int mid = 0; mid <= 1; ++mid) {
     const int grid = (mid ? nsub : 2 * nsub) * C;
     if (nb == 32) {
