@@ -732,6 +732,7 @@ __device__ int g_solve_dbg = 0;
 constexpr int kST = kSW * 32;
 constexpr int kCW = kSW - 1;
 constexpr int kCT = kCW * 32;
+constexpr int kCS = 8;  // column-partial slots (15 warps reduced in two rounds)
 
 // Row chunking of a CTA's rows [rlo, rhi) of one line: the longest run of rows starting at
 // r0 whose packed size fits `cap` doubles (at least one row). Identical on every thread.
@@ -809,7 +810,8 @@ __global__ void __launch_bounds__(kST, 1)
     k_line_solve(const SubInfo* __restrict__ subs, const double* __restrict__ fac,
                  const double* __restrict__ coef, size_t N, const double* __restrict__ r,
                  double* __restrict__ ylocal, double* __restrict__ zlocal, int W, int nc,
-                 int stages, int cap, int kd_max, int rc, int phase, const int* __restrict__ flags,
+                 int stages, int cap, int kd_max, int rc, int phase,
+                 const int* __restrict__ flags,
                  const double* __restrict__ rlocal) {
   if (flags && (flags[0] | flags[1])) return;  // PCG converged or failed (grid-uniform)
   const int C = static_cast<int>(cl_size()), crank = static_cast<int>(cl_rank());
@@ -828,8 +830,11 @@ __global__ void __launch_bounds__(kST, 1)
   uint64_t* red_bar = empty + 8;  // [2]: partial sums for my rows have arrived (line parity)
   uint64_t* x_bar = red_bar + 2;  // [2]: the other CTAs' x of the line have arrived
   double* stage0 = reinterpret_cast<double*>(smem_raw + kSolveHdr);
-  double* colpart = stage0 + static_cast<size_t>(stages) * cap;  // kCW x kd_max
-  double* wv = colpart + static_cast<size_t>(kCW) * kd_max;      // kd_max
+  // column-partial slots: one per compute warp, or 8 (two-round reduction) for wide lines
+  // where the 7 kd doubles buy ring capacity (must match solve_plan)
+  constexpr int ncs = MAXM >= 20 ? kCS : kCW;
+  double* colpart = stage0 + static_cast<size_t>(stages) * cap;  // ncs x kd_max
+  double* wv = colpart + static_cast<size_t>(ncs) * kd_max;      // kd_max
   double* yrow = wv + kd_max;                                    // kd_max (own rows)
   double* xbuf = yrow + kd_max;                                  // 2 x kd_max (line parity)
   double* red = xbuf + 2 * kd_max;                               // 2 x C x kd_max slots
@@ -1057,21 +1062,53 @@ __global__ void __launch_bounds__(kST, 1)
       PROF_MARK(2);
       ++c_seq;
     }
+    // column partials of the 15 warps: one slot per warp (ncs = 15), or, for wide lines,
+    // through 8 slots (fixed order): warps 8..14 hand theirs to warps 0..6, then warps 0..7
+    // publish (each reuses the slot it just read) — 7 kd doubles more for the stage ring
+    if constexpr (ncs == kCW) {
 #pragma unroll
-    for (int mm = 0; mm < M2; ++mm) {
-      const int j = 64 * mm + 2 * lane;
-      if (j < rhi) colpart[warp * kd_max + j] = cacc[mm].x;
-      if (j + 1 < rhi) colpart[warp * kd_max + j + 1] = cacc[mm].y;
+      for (int mm = 0; mm < M2; ++mm) {
+        const int j = 64 * mm + 2 * lane;
+        if (j < rhi) colpart[warp * kd_max + j] = cacc[mm].x;
+        if (j + 1 < rhi) colpart[warp * kd_max + j + 1] = cacc[mm].y;
+      }
+    } else {
+      if (warp >= kCS) {
+#pragma unroll
+        for (int mm = 0; mm < M2; ++mm) {
+          const int j = 64 * mm + 2 * lane;
+          if (j < rhi) colpart[(warp - kCS) * kd_max + j] = cacc[mm].x;
+          if (j + 1 < rhi) colpart[(warp - kCS) * kd_max + j + 1] = cacc[mm].y;
+        }
+      }
+      compute_bar();
+      if (warp < kCS) {
+#pragma unroll
+        for (int mm = 0; mm < M2; ++mm) {
+          const int j = 64 * mm + 2 * lane;
+          if (warp + kCS < kCW) {
+            if (j < rhi) cacc[mm].x += colpart[warp * kd_max + j];
+            if (j + 1 < rhi) cacc[mm].y += colpart[warp * kd_max + j + 1];
+          }
+          if (j < rhi) colpart[warp * kd_max + j] = cacc[mm].x;
+          if (j + 1 < rhi) colpart[warp * kd_max + j + 1] = cacc[mm].y;
+        }
+      }
     }
     compute_bar();
     PROF_MARK(3);
-    // column partials of this CTA (+ its own row dots), reduced in a fixed warp order and
+    // column partials of this CTA (+ its own row dots), reduced in a fixed slot order and
     // scattered to the CTA that owns each row
     int owner = 0;
     for (int j = tid; j < rhi && !(dbg & 8); j += kCT) {
       double tv = (j >= rlo) ? yrow[j] - dcorr[j] : 0.0;
+      if constexpr (ncs == kCW) {
 #pragma unroll 5
-      for (int w = 0; w < kCW; ++w) tv += colpart[w * kd_max + j];
+        for (int w = 0; w < kCW; ++w) tv += colpart[w * kd_max + j];
+      } else {
+#pragma unroll
+        for (int w = 0; w < kCS; ++w) tv += colpart[w * kd_max + j];
+      }
       while (owner + 1 < C && rlos[owner + 1] <= j) ++owner;
       double* slot = red + static_cast<size_t>(par * C + crank) * kd_max;
       if (owner == crank || (dbg & 2))
@@ -1431,7 +1468,10 @@ SolvePlan solve_plan(int kd_max, int C) {
   pl.row_cost = kd_max <= 512 ? 16 : 0;
   if (const char* e = std::getenv("FFB_ROW_COST")) pl.row_cost = std::atoi(e);
   pl.C = C;
-  const size_t fixed = kSolveHdr + (static_cast<size_t>(kCW) * kd_max + 5 * kd_max +
+  // column-partial slots: one per compute warp, or 8 (two-round reduction) for wide lines
+  // where the 7 kd doubles buy ring capacity (measured: c5 -32%, c2 +5%)
+  pl.ncs = (kd_max + 31) / 32 > 14 ? kCS : kCW;  // the kernels' MAXM >= 20 instantiations
+  const size_t fixed = kSolveHdr + (static_cast<size_t>(pl.ncs) * kd_max + 5 * kd_max +
                                     2 * static_cast<size_t>(C) * kd_max) * sizeof(double);
   size_t budget = 227 * 1024 - 1024;
   if (const char* e = std::getenv("FFB_SOLVE_SMEM_KB")) budget = static_cast<size_t>(std::atoi(e)) * 1024;
@@ -1475,7 +1515,8 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
                      N, r, ylocal, zlocal, W, nc, pl.kd_max, phase, flags, rlocal);
     } else {
       launch_cluster(k_line_solve<M>, 2 * nsub * pl.C, kST, pl.smem, pl.C, st, d_subs, fac, coef,
-                     N, r, ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, pl.row_cost, phase, flags,
+                     N, r, ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, pl.row_cost,
+                     phase, flags,
                      rlocal);
     }
     FFB_LAUNCHED();

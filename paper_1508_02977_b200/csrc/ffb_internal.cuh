@@ -90,7 +90,7 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max, con
 void changed_lines(const SubInfo* d_subs, int nsub, const double* alpha, const double* alpha_fact,
                    int W, int H, int2* changed, cudaStream_t st);
 struct SolvePlan {
-  int stages, cap, maxm, C, kd_max, ldg, row_cost;
+  int stages, cap, maxm, C, kd_max, ldg, row_cost, ncs;
   size_t smem;
 };
 SolvePlan solve_plan(int kd_max, int C);
