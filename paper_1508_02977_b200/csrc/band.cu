@@ -181,7 +181,7 @@ __device__ __forceinline__ void rupd_tile(double* __restrict__ D, int kd, int kd
   for (int i = 0; i < 4; ++i) {  // the tile's read-modify-write targets -> L1
     const int u = ub0 + 16 * (i >> 1) + (i & 1);
     if (u < kd && (vi & 1) == 0)
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(D + static_cast<long long>(u) * kd + 32 * TV + 8 * vi));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(D + prow_off32(u) + 32 * TV + 8 * vi));
   }
   double acc[4][8];
 #pragma unroll
@@ -211,7 +211,7 @@ __device__ __forceinline__ void rupd_tile(double* __restrict__ D, int kd, int kd
   for (int i = 0; i < 4; ++i) {
     const int u = ub0 + 16 * (i >> 1) + (i & 1);
     if (u >= kd || (u >= k0 && u < k1)) continue;
-    double* rowp = D + static_cast<long long>(u) * kd;
+    double* rowp = D + prow_off32(u);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int v = vb0 + 8 * (j >> 1) + (j & 1);
@@ -256,7 +256,7 @@ __device__ __forceinline__ void kk_update(const double* __restrict__ D, int kd, 
     for (int j = 0; j < 4; ++j) {
       const int v = v0 + j;
       if (v <= u && u < nb1)
-        P[u * (NB + 1) + v] = D[static_cast<long long>(k1 + u) * kd + k1 + v] - acc[i][j];
+        P[u * (NB + 1) + v] = D[prow_off32(k1 + u) + k1 + v] - acc[i][j];
     }
   }
 }
@@ -303,9 +303,9 @@ __device__ __forceinline__ void tile_ark(double* __restrict__ D, int kd, int kdp
         const int c = cb + 8 * (j >> 1) + (j & 1);
         if (c >= nbk) continue;
         if (u > k0)
-          D[static_cast<long long>(u) * kd + k0 + c] = acc[i][j];
+          D[prow_off32(u) + k0 + c] = acc[i][j];
         else
-          D[static_cast<long long>(k0 + c) * kd + u] = acc[i][j];
+          D[prow_off32(k0 + c) + u] = acc[i][j];
       }
     }
   }
@@ -346,7 +346,7 @@ __device__ __forceinline__ void tile_akk(double* __restrict__ D, int kd, const d
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int c = cb + 8 * (j >> 1) + (j & 1);
-        if (c <= r) D[static_cast<long long>(k0 + r) * kd + k0 + c] = -acc[i][j];
+        if (c <= r) D[prow_off32(k0 + r) + k0 + c] = -acc[i][j];
       }
     }
   }
@@ -392,7 +392,7 @@ __device__ __forceinline__ void rupd_tile_mma(double* __restrict__ D, int kd, in
   for (int i = 0; i < 4; ++i) {
     const int u = u0 + 8 * i + g;
     if (u >= kd || (u >= k0 && u < k1)) continue;
-    double* rowp = D + static_cast<long long>(u) * kd;
+    double* rowp = D + prow_off32(u);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (diag && j > i) continue;
@@ -405,8 +405,22 @@ __device__ __forceinline__ void rupd_tile_mma(double* __restrict__ D, int kd, in
   }
 }
 
-// In-place inversion of the SPD line matrix D (kd x kd row-major in global scratch, lower
-// triangle used) by the blocked symmetric sweep; leaves -D^{-1} in the lower triangle.
+// P (stride NB+1) <- the nbk x nbk diagonal block at (k, k) of the packed line D (lower)
+template <int NB>
+__device__ __forceinline__ void load_block(const double* __restrict__ D, int k, int nbk,
+                                           double* P, int lane) {
+  double v[NB];
+#pragma unroll
+  for (int a = 0; a < NB; ++a)  // all loads in flight before the first store
+    v[a] = (a < nbk && lane <= a) ? D[prow_off32(k + a) + k + lane] : 0.0;
+#pragma unroll
+  for (int a = 0; a < NB; ++a)
+    if (a < nbk && lane <= a) P[a * (NB + 1) + lane] = v[a];
+  __syncwarp();
+}
+
+// In-place inversion of the SPD line matrix D (its packed lower triangle, rows at prow_off, in
+// the line's own factor storage) by the blocked symmetric sweep; leaves -D^{-1} there.
 // The next step's pivot block is factored by warp 0 while the other 15 warps write the
 // current step's A_RK and A_KK (tile updates from a dynamic queue).
 // Shared memory: P (NB x NB+1), Li[2] (double-buffered), ir (NB), the tile counter, Z.
@@ -424,7 +438,10 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
   constexpr int LS = NB * LDL;
   PROF_DECL
   if (tid == 0) cnt[0] = 0, cnt[3] = 0;
-  if (warp == 0) pivot_warp<NB>(D, kd, 0, min(NB, kd), P, Li2, ir, first_bad, bad_base, nullptr);
+  if (warp == 0) {
+    load_block<NB>(D, 0, min(NB, kd), P, lane);
+    pivot_warp<NB>(P, NB + 1, 0, min(NB, kd), P, Li2, ir, first_bad, bad_base, nullptr);
+  }
   const bool la_reg = NB == 32 && la;  // look-ahead on a private copy of the next pivot block
   int pv_tag = 0;                      // pivot_pair progress tags (same on every warp)
   if (tid == 0) cnt[2] = 0;
@@ -448,8 +465,8 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       double a[NB];
 #pragma unroll
       for (int c = 0; c < NB; ++c)
-        a[c] = (live && c < nbk) ? (i > k0 ? D[static_cast<long long>(i) * kd + k0 + c]
-                                           : D[static_cast<long long>(k0 + c) * kd + i])
+        a[c] = (live && c < nbk) ? (i > k0 ? D[prow_off32(i) + k0 + c]
+                                           : D[prow_off32(k0 + c) + i])
                                  : 0.0;
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
@@ -486,8 +503,9 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       {
         rupd_tile(D, kd, zs, Z, nbk, k0, k1, nx, nx, lane);
         __syncwarp();
-        pivot_warp<NB>(D + static_cast<long long>(k1) * kd + k1, kd, k1, min(NB, kd - k1), P,
-                       Lnext, ir, first_bad, bad_base, nullptr);
+        load_block<NB>(D, k1, min(NB, kd - k1), P, lane);
+        pivot_warp<NB>(P, NB + 1, k1, min(NB, kd - k1), P, Lnext, ir, first_bad, bad_base,
+                       nullptr);
       }
       PROF_MARK(5);
     }
@@ -527,8 +545,9 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
     } else if (!la && warp == 0) {
       // the next pivot block is final now: factor it while the other warps write A_RK, A_KK
       if (k1 < kd)
-        pivot_warp<NB>(D + static_cast<long long>(k1) * kd + k1, kd, k1, min(NB, kd - k1), P,
-                       Lnext, ir, first_bad, bad_base, nullptr);
+        load_block<NB>(D, k1, min(NB, kd - k1), P, lane),
+            pivot_warp<NB>(P, NB + 1, k1, min(NB, kd - k1), P, Lnext, ir, first_bad, bad_base,
+                           nullptr);
       PROF_MARK(5);
     } else {
       // ---- A_RK <- Z Li ; A_KK <- -Li^T Li, as 32x32 tiles (4x8 per lane): row tiles
@@ -567,21 +586,21 @@ __device__ void build_line(const SubInfo& s, const double* __restrict__ coef, si
         v -= b0i * bcoef(s, coef, N, W, nc, bl0, j) * F[static_cast<long long>(nb0) * s.line_sz + oi + j];
       if (nb1 >= 0)
         v -= b1i * bcoef(s, coef, N, W, nc, bl1, j) * F[static_cast<long long>(nb1) * s.line_sz + oi + j];
-      D[static_cast<long long>(i) * kd + j] = v;
+      D[oi + j] = v;
     }
   }
   __syncthreads();
 }
 
-__device__ void pack_line(const SubInfo& s, int l, const double* __restrict__ D, double* F,
-                          int q, int C) {
+// the sweep leaves -D^-1 in place in the packed line: negate it, zero the pads of even rows
+__device__ void pack_line(const SubInfo& s, int l, double* F, int q, int C) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kd = s.kd;
   double* Fl = F + static_cast<long long>(l) * s.line_sz;
   for (int i = warp + kFW * q; i < kd; i += kFW * C) {
-    const long long o = prow_off(i);
-    for (int j = lane; j <= i; j += 32) Fl[o + j] = -D[static_cast<long long>(i) * kd + j];
-    if ((i & 1) == 0 && lane == 0) Fl[o + i + 1] = 0.0;  // pad of even rows
+    const int o = prow_off32(i);
+    for (int j = lane; j <= i; j += 32) Fl[o + j] = -Fl[o + j];
+    if ((i & 1) == 0 && lane == 0) Fl[o + i + 1] = 0.0;
   }
   __syncthreads();
 }
@@ -609,8 +628,7 @@ __global__ void __launch_bounds__(kFT, 1)
   // untouched prefix of each chain keeps its inverses (D_l depends on lines <= l only)
   const int2 chg = changed ? changed[sub] : make_int2(0, L - 1);
   if (chg.x > chg.y) return;  // nothing changed in this subdomain
-  double* D = scratch + (mid ? sub : cid) * scratch_stride;
-  double* F = fac + s.fac_off;
+  double* F = fac + s.fac_off;  // each line is built, inverted and negated in place
   extern __shared__ __align__(16) double fsm[];
   constexpr int LDL = li_stride<NB>();
   double* P = fsm;                      // NB x (NB+1)
@@ -622,12 +640,13 @@ __global__ void __launch_bounds__(kFT, 1)
   int first_bad = 0x7fffffff;
   PROF_DECL
   if (mid) {
+    double* D = F + static_cast<long long>(m) * s.line_sz;
     build_line(s, coef, N, W, nc, m, m > 0 ? m - 1 : -1, m, m < L - 1 ? m + 1 : -1, m + 1, F, D,
                q, C);
     if (C > 1) cl_sync();
     PROF_MARK(0);
     sweep_invert<NB>(D, kd, kdp, P, Li, ir, cnt, Z, first_bad, m * kd, la, q, C);
-    pack_line(s, m, D, F, q, C);
+    pack_line(s, m, F, q, C);
   } else {
     const int nlines = chain == 0 ? m : L - 1 - m;
     const int t0 = chain == 0 ? chg.x : L - 1 - chg.y;
@@ -635,11 +654,12 @@ __global__ void __launch_bounds__(kFT, 1)
       const int l = chain == 0 ? t : L - 1 - t;
       const int prev = t == 0 ? -1 : (chain == 0 ? l - 1 : l + 1);
       const int bl = chain == 0 ? l : l + 1;  // coupling between l and prev
+      double* D = F + static_cast<long long>(l) * s.line_sz;
       build_line(s, coef, N, W, nc, l, prev, bl, -1, 0, F, D, q, C);
       if (C > 1) cl_sync();
       PROF_MARK(0);
       sweep_invert<NB>(D, kd, kdp, P, Li, ir, cnt, Z, first_bad, l * kd, la, q, C);
-      pack_line(s, l, D, F, q, C);
+      pack_line(s, l, F, q, C);
       PROF_MARK(5);
     }
   }
@@ -1373,8 +1393,8 @@ static void launch_cluster(K kernel, int nblocks, int threads, size_t smem, int 
   FFB_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
 }
 
-size_t factor_scratch_doubles(int nsub, int kd_max) {
-  return static_cast<size_t>(2 * nsub) * kd_max * kd_max;
+size_t factor_scratch_doubles(int /*nsub*/, int /*kd_max*/) {
+  return 1;  // lines are factored in place in the packed factor storage
 }
 
 // changed[sub] = (first, last) local line touched by a triangle whose alpha differs from
@@ -1437,13 +1457,13 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
   }
   // the look-ahead through D is a single-CTA schedule; the NB = 32 one works in clusters
   int lac = (C > 1 && nb != 32) ? 0 : la;
-  // DMMA tile updates (FFB_FACTOR_MMA=0: the FFMA register tiles): measured c2 -9%,
-  // c3 -13%, c5 -20% of the factorisation time
+  // DMMA tile updates for NB = 32 (measured c2 -9%, c3 -13% of the factorisation time);
+  // the NB = 16 sweep (c5) is faster with the FFMA register tiles. FFB_FACTOR_MMA=0/1 forces.
   static const int mma = [] {
     const char* e = std::getenv("FFB_FACTOR_MMA");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : -1;
   }();
-  if (mma) lac |= 2;
+  if (mma == 1 || (mma < 0 && nb == 32)) lac |= 2;
   for (int mid = 0; mid <= 1; ++mid) {
     const int grid = (mid ? nsub : 2 * nsub) * C;
     if (nb == 32) {
