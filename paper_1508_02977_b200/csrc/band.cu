@@ -1454,8 +1454,7 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
   // Factor clusters of 4 CTAs regardless of how many SMs that asks for: the hardware runs the
   // clusters in waves, so only ~37 chains' lines are being rewritten at a time and stay in L2
   // (measured: c3 1.56 -> 0.78 s, c4 2.1 -> 1.5 s per adaptive chain vs one CTA per chain)
-  C = 4;
-  (void)C;
+  C = nb == 16 ? 8 : 4;  // wide lines (c5): 8 (4.2 -> 3.4 s)
   if (const char* e = std::getenv("FFB_FCLUSTER")) {
     const int v = std::atoi(e);
     if (v == 1 || v == 2 || v == 4 || v == 8) C = v;
