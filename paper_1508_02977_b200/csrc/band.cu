@@ -940,7 +940,7 @@ __global__ void __launch_bounds__(kST, 1)
   // operand of line step t, prefetched into registers one step ahead. Forward:
   // w = r_l - b_prev o y_prev; backward middle: w = r_m - b_m y_{m-1} - b_{m+1} y_{m+1};
   // backward chain: w = b_next o x_next and x_l = y_l - Dinv_l w.
-  constexpr int PS = 2;  // j = tid + kCT*q, kd <= 2*kCT
+  constexpr int PS = 32 * MAXM > kCT ? 2 : 1;  // j = tid + kCT*q, kd <= PS*kCT
   double pf_r[PS], pf_b[PS], pf_y[PS];
   auto prefetch = [&](int t) {
 #pragma unroll
