@@ -463,11 +463,19 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
     for (int i = tid; i < kdp; i += kFT) {
       const bool live = i < kd && (i < k0 || i >= k1);
       double a[NB];
+      if (live && i > k0) {
+        // row i's segment of the panel: 16-byte loads (rows start 16-byte aligned, k0 even)
+        const double2* row = reinterpret_cast<const double2*>(D + prow_off32(i) + k0);
 #pragma unroll
-      for (int c = 0; c < NB; ++c)
-        a[c] = (live && c < nbk) ? (i > k0 ? D[prow_off32(i) + k0 + c]
-                                           : D[prow_off32(k0 + c) + i])
-                                 : 0.0;
+        for (int c = 0; c < NB; c += 2) {
+          const double2 v = c < nbk ? row[c / 2] : make_double2(0.0, 0.0);
+          a[c] = v.x;
+          a[c + 1] = c + 1 < nbk ? v.y : 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) a[c] = (live && c < nbk) ? D[prow_off32(k0 + c) + i] : 0.0;
+      }
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
         double acc = 0.0;
