@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 
 namespace ffb {
@@ -52,7 +53,17 @@ __device__ unsigned long long g_prof[64];
     if (blockIdx.x == 0 && threadIdx.x == 0)                              \
       for (int i_ = 0; i_ < 16; ++i_) g_prof[(base) + i_] += prof_acc[i_]; \
   } while (0)
+// per-warp event timeline of CTA 0 for forward line steps 8..23 (tile solve kernel)
+__device__ unsigned long long g_tl[16][16][8];
+#define TL_MARK(i)                                                                   \
+  do {                                                                               \
+    if (blockIdx.x == 0 && phase == 0 && t >= 8 && t < 24 && (threadIdx.x & 31) == 0) \
+      g_tl[t - 8][threadIdx.x >> 5][i] = clock64();                                  \
+  } while (0)
 #else
+#define TL_MARK(i) \
+  do {             \
+  } while (0)
 #define PROF_DECL
 #define PROF_MARK(i) \
   do {               \
@@ -1182,24 +1193,129 @@ __global__ void __launch_bounds__(kST, 1)
   PROF_FLUSH(16);
 }
 
-// Variant without shared-memory staging: every warp streams its rows straight from global
-// memory into registers (ld.global.nc, no L1 allocation), keeping the next row's loads in
-// flight while it computes the current one — also across line boundaries, so the loads
-// overlap the per-line reductions. All 16 warps compute.
-__device__ __forceinline__ double ldg_stream(const double* p) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
+// ----------------------------------------------------------------- K6, register-tiled
+// Latency regime (lines whose packed triangle, split over the cluster, fits the register
+// file: c1, c2). A line step of the sweep is a dependent chain — the operand of line t needs
+// x of line t-1 — so what bounds it is the latency of one symmetric GEMV plus its reduction,
+// not the bytes. Here the line's lower triangle is cut into 32x32 tiles (I, J), I >= J, one
+// tile per warp across the cluster, and each warp holds its tile of the NEXT line in
+// registers (8 rows x 4 columns per lane, loaded while the current line's exchange is in
+// flight, the line after that prefetched into L2). The critical path per line is then:
+// operand -> 64 register FMAs -> 10 shuffles -> one st.async of the row and the column
+// partial to the owners of blocks I and J -> the owner sums its nt + 1 contributions in a fixed
+// order -> st.async broadcast of x to every CTA of the cluster. One CTA barrier per line.
+// Contribution k of output block I: the row partial of tile (I, k) for k <= I, the column
+// partial of tile (k - 1, I) for k > I (the diagonal tile gives both, its diagonal counted
+// once, in the row partial). Deterministic: every sum runs in a fixed order.
+constexpr int kTileWarps = 16;
+constexpr int kTileThreads = kTileWarps * 32;
+constexpr int kTileMaxNt = 16;
+constexpr int kTileMaxOwn = 2;  // blocks per dedicated owner warp
+
+__device__ __forceinline__ void st_async_to(uint32_t dst_cluster, double v, uint32_t bar_cluster) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(
+                   dst_cluster),
+               "d"(v), "r"(bar_cluster)
+               : "memory");
+}
+// mbarrier wait that fails loudly instead of hanging: traps after ~4e9 cycles (~2 s)
+__device__ __forceinline__ void mbar_wait_g(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      ".reg .s64 t0, t1;\n"
+      "mov.u64 t0, %%clock64;\n"
+      "WAITG_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONEG_%=;\n"
+      "mov.u64 t1, %%clock64;\n"
+      "sub.s64 t1, t1, t0;\n"
+      "setp.lt.s64 P1, t1, 4000000000;\n"
+      "@P1 bra WAITG_%=;\n"
+      "trap;\n"
+      "DONEG_%=:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t local, unsigned rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-template <int MAXM>
-__global__ void __launch_bounds__(kST, 1)
-    k_line_solve_ldg(const SubInfo* __restrict__ subs, const double* __restrict__ fac,
-                     const double* __restrict__ coef, size_t N, const double* __restrict__ r,
-                     double* __restrict__ ylocal, double* __restrict__ zlocal, int W, int nc,
-                     int kd_max, int phase, const int* __restrict__ flags,
-                     const double* __restrict__ rlocal) {
-  if (flags && (flags[0] | flags[1])) return;
+// ---- tile-major line layout (the register-tiled solve streams whole tiles) ----------------
+// A line's lower triangle as 32x32 tiles (I, J), I >= J, row-major; tile row I has
+// h = min(32, kd - 32 I) rows. An off-diagonal tile stores its h rows of 32 entries, a
+// diagonal tile its packed lower triangle (local row r: r + 1 entries padded to even, at
+// prow_off(r)). Same number of doubles as the packed row layout (tile_line_size == prow_off).
+__host__ __device__ __forceinline__ int tile_h(int I, int kd) { return min(32, kd - 32 * I); }
+__host__ __device__ __forceinline__ long long tile_row_off(int I, int kd) {
+  // tile rows before I are full (h = 32): I off-diagonal tiles of 1024 + one diagonal of 544
+  (void)kd;
+  return 1024LL * I * (I - 1) / 2 + 544LL * I;
+}
+__host__ __device__ __forceinline__ long long tile_off(int I, int J, int kd) {
+  return tile_row_off(I, kd) + 32LL * tile_h(I, kd) * J;
+}
+__host__ __device__ __forceinline__ int tile_size(int I, int J, int kd) {
+  const int h = tile_h(I, kd);
+  return I == J ? static_cast<int>(prow_off(h)) : 32 * h;
+}
+
+// packed rows -> tile-major, one CTA per (line, subdomain), one warp per tile row segment
+__global__ void __launch_bounds__(256) k_tile_pack(const SubInfo* __restrict__ subs,
+                                                   const double* __restrict__ fac,
+                                                   double* __restrict__ fac_t) {
+  const SubInfo s = subs[blockIdx.y];
+  const int l = blockIdx.x;
+  if (l >= s.L) return;
+  const int kd = s.kd, nt = (kd + 31) >> 5;
+  const double* src = fac + s.fac_off + static_cast<long long>(l) * s.line_sz;
+  double* dst = fac_t + s.fac_off + static_cast<long long>(l) * s.line_sz;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int T = nt * (nt + 1) / 2;
+  for (int q = warp; q < T * 32; q += 8) {  // (tile, local row)
+    const int tau = q >> 5, r = q & 31;
+    int I = static_cast<int>((sqrt(8.0 * tau + 1.0) - 1.0) * 0.5);
+    while (I * (I + 1) / 2 > tau) --I;
+    while ((I + 1) * (I + 2) / 2 <= tau) ++I;
+    const int J = tau - I * (I + 1) / 2;
+    const int h = tile_h(I, kd);
+    if (r >= h) continue;
+    const double* srow = src + prow_off(32 * I + r) + 32 * J;
+    double* drow = dst + tile_off(I, J, kd) + (I == J ? prow_off(r) : 32LL * r);
+    const int len = I == J ? ((r + 2) & ~1) : 32;  // the diagonal row with its even pad
+    if (lane < len) drow[lane] = srow[lane];
+  }
+}
+
+// ---- K6, register-tiled ---------------------------------------------------------------------
+// Placement tables (built on the host by set_tile_tables) for cluster-size index ci (C = 1,
+// 2, 4, 8) and nt tile rows:
+//  c_tile_of[ci][nt][cta][slot]  tile number (row-major over I >= J) or 255; the tiles of a
+//                                CTA fill slots (= warps) 0, 1, ... and, in that order, the
+//                                CTA's share of each line in its shared-memory stage
+//  c_nloc[ci][nt][I]             contributions to block I written by its own CTA
+//  c_owner[ci][nt][I]            warp of CTA I % C that reduces block I: the warps above the
+//                                CTA's tiles when there are any (at most kTileMaxOwn blocks
+//                                each), else warp I / C
+// A tile (I, J) goes to the CTA of block I or of block J, whichever holds fewer bytes, so at
+// least one of its two partials stays local.
+__constant__ unsigned char c_tile_of[4][kTileMaxNt + 1][8][kTileWarps];
+__constant__ unsigned char c_nloc[4][kTileMaxNt + 1][kTileMaxNt];
+__constant__ unsigned char c_owner[4][kTileMaxNt + 1][kTileMaxNt];
+
+__global__ void __launch_bounds__(kTileThreads, 1)
+    k_line_solve_tile(const SubInfo* __restrict__ subs, const double* __restrict__ fac_t,
+                      const double* __restrict__ coef, size_t N, const double* __restrict__ r,
+                      double* __restrict__ ylocal, double* __restrict__ zlocal, int W, int nc,
+                      int kdp_max, int stage_doubles, int phase, const int* __restrict__ flags,
+                      const double* __restrict__ rlocal) {
+  if (flags && (flags[0] | flags[1])) return;  // PCG converged or failed (grid-uniform)
   const int C = static_cast<int>(cl_size()), crank = static_cast<int>(cl_rank());
   const int cid = blockIdx.x / C;
   const int sub = cid >> 1, chain = cid & 1;
@@ -1207,170 +1323,362 @@ __global__ void __launch_bounds__(kST, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kd = s.kd, L = s.L, m = mid_line(L);
   const int nl = chain_len(phase, chain, L);
-  const int rlo = row_lo(crank, C, kd), rhi = row_lo(crank + 1, C, kd);
-  const double* F = fac + s.fac_off;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* colpart = reinterpret_cast<double*>(smem_raw);  // kSW x kd_max
-  double* wv = colpart + static_cast<size_t>(kSW) * kd_max;
-  double* yrow = wv + kd_max;
-  double* xprev = yrow + kd_max;
-  double* red = xprev + kd_max;
+  if (nl == 0) return;  // cluster-uniform
+  const int nt = (kd + 31) >> 5, kdp = nt * 32;
+  const int ci = C == 1 ? 0 : (C == 2 ? 1 : (C == 4 ? 2 : 3));
+  const double* F = fac_t + s.fac_off;
   double* yl = ylocal + s.vec_off;
   double* zl = zlocal + s.vec_off;
   const double* rl = rlocal ? rlocal + s.vec_off : nullptr;
-  if (nl == 0) return;
-  for (int j = tid; j < kd_max; j += kST) xprev[j] = 0.0;
+  const int dbg = g_solve_dbg;  // development probe: 4 skip the stage copies
 
-  // the warp's row stream: (line step t, row i) with i = rlo + warp + kSW*k
-  double buf[MAXM];
-  int nt = 0, ni = rlo + warp;  // next row to load
-  auto load_next = [&]() {      // issue the loads of the next row of this warp's stream
-    while (nt < nl && ni >= rhi) ++nt, ni = rlo + warp;
-    if (nt >= nl) return;
-    const int l = chain_line(phase, chain, L, nt);
-    const double* Si = F + static_cast<long long>(l) * s.line_sz + prow_off(ni);
-#pragma unroll
-    for (int mm = 0; mm < MAXM; ++mm) {
-      const int j = lane + 32 * mm;
-      buf[mm] = (32 * mm <= ni && j <= ni) ? ldg_stream(Si + j) : 0.0;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* blk_bar = reinterpret_cast<uint64_t*>(smem_raw);  // [16] one per owned block
+  // operand of line step t: wv[t & 1], landed on w_bar[t & 1]. Double-buffered: an owner whose
+  // block gets no contribution from this CTA may send the next operand while this CTA still
+  // waits for the current one.
+  uint64_t* w_bar = blk_bar + kTileWarps;                      // [2]
+  uint64_t* full = w_bar + 2;                                  // [2] line stages landed
+  double* stage = reinterpret_cast<double*>(smem_raw + 256);   // 2 x stage_doubles
+  double* wv = stage + 2 * static_cast<size_t>(stage_doubles);  // 2 x kdp_max: operands
+  long long* op_r = reinterpret_cast<long long*>(wv + 2 * kdp_max);  // kdp_max: r index, line 0
+  long long* op_b = op_r + kdp_max;  // kdp_max: coupling index (coef) at line 0
+  double* slots = reinterpret_cast<double*>(op_b + kdp_max);  // [owned block][nt + 1][32]
+  const int n_own = (nt - crank + C - 1) / C;  // blocks crank, crank + C, ... < nt
+  // this CTA's tiles: my tile's place in the line (tile-major) and in the stage (slot order),
+  // and the CTA's doubles per line
+  int my_tau = 255, my_off = 0, my_src = 0, my_sz = 0, cta_doubles = 0;
+  for (int q = 0; q < kTileWarps; ++q) {
+    const int tq = c_tile_of[ci][nt][crank][q];
+    if (tq == 255) break;
+    int I = 0;
+    while ((I + 1) * (I + 2) / 2 <= tq) ++I;
+    const int J = tq - I * (I + 1) / 2, sz = tile_size(I, J, kd);
+    if (q == warp) my_tau = tq, my_off = cta_doubles, my_src = static_cast<int>(tile_off(I, J, kd)), my_sz = sz;
+    cta_doubles += sz;
+  }
+  // contributions / operand blocks written by warps of this CTA arrive (after plain shared
+  // stores); those of other CTAs complete transaction bytes (st.async)
+  if (tid == 0) {
+    for (int q = 0; q < n_own; ++q) mbar_init(&blk_bar[q], 1 + c_nloc[ci][nt][q * C + crank]);
+    mbar_init(&w_bar[0], 1 + n_own);
+    mbar_init(&w_bar[1], 1 + n_own);
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_barrier_init();
+  }
+  const bool has_tile = my_tau != 255;
+  int TI = 0, TJ = 0;
+  if (has_tile) {
+    while ((TI + 1) * (TI + 2) / 2 <= my_tau) ++TI;
+    TJ = my_tau - TI * (TI + 1) / 2;
+  }
+  const bool diag = TI == TJ;
+  const int th = has_tile ? tile_h(TI, kd) : 0;
+  const int rg = lane >> 3, cg = lane & 7;
+  const int i0 = 32 * TI + 8 * rg;   // my rows i0 .. i0 + 7
+  const int jc0 = 32 * TJ + 2 * cg;  // my columns jc0, jc0 + 1, jc0 + 16, jc0 + 17
+  // where my two partials go: row partial -> block TI (contribution TJ, row cg of group rg),
+  // column partial -> block TJ (contribution TI + 1, column (rg & 2 ? 16 : 0) + 2 cg + (rg & 1))
+  const int orow = TI % C, ocol = TJ % C;
+  const int er = ((TI / C) * (nt + 1) + TJ) * 32 + 8 * rg + cg;
+  const int ec = ((TJ / C) * (nt + 1) + TI + 1) * 32 + (rg & 2 ? 16 : 0) + 2 * cg + (rg & 1);
+  const uint32_t slots_u = smem_u32(slots), blk_bar_u = smem_u32(blk_bar);
+  const uint32_t er_remote = mapa_u32(slots_u + 8u * er, orow);
+  const uint32_t er_bar = mapa_u32(blk_bar_u + 8u * (TI / C), orow);
+  const uint32_t ec_remote = mapa_u32(slots_u + 8u * ec, ocol);
+  const uint32_t ec_bar = mapa_u32(blk_bar_u + 8u * (TJ / C), ocol);
+  // blocks this warp reduces (ob = index among the CTA's blocks), at most two, reduced together
+  static_assert(kTileMaxOwn == 2, "owner slots are unrolled by hand");
+  int ob0 = -1, ob1 = -1;
+  for (int q = 0; q < n_own; ++q)
+    if (c_owner[ci][nt][q * C + crank] == warp) {
+      if (ob0 < 0) ob0 = q; else if (ob1 < 0) ob1 = q;
     }
+  const bool owner = ob0 >= 0;
+  const int io0 = 32 * (ob0 * C + crank) + lane, io1 = 32 * (ob1 * C + crank) + lane;  // my rows
+  uint32_t blk_tx0 = 0, blk_tx1 = 0;  // remote bytes per line into my blocks
+  if (ob0 >= 0) blk_tx0 = 256u * static_cast<uint32_t>(nt + 1 - c_nloc[ci][nt][ob0 * C + crank]);
+  if (ob1 >= 0) blk_tx1 = 256u * static_cast<uint32_t>(nt + 1 - c_nloc[ci][nt][ob1 * C + crank]);
+  const uint32_t w_tx = 256u * static_cast<uint32_t>(nt - n_own);
+  // operand addressing of unknown j: r and the slow-axis coupling are affine in the line index
+  // (gidx / bcoef with the division by nc hoisted; kept in shared memory)
+  if (tid < kd) {
+    const int a = tid / nc, c = tid - a * nc;
+    op_r[tid] = (s.xfast ? (static_cast<long long>(s.fy0) * W + s.fx0 + a)
+                         : (static_cast<long long>(s.fy0 + a) * W + s.fx0)) * nc + c;
+    const int k = c < 2 ? 0 : 1;
+    const long long v0 = s.xfast ? static_cast<long long>(s.fy0) * W + s.fx0 + a
+                                 : static_cast<long long>(s.fy0 + a) * W + s.fx0;
+    op_b[tid] = s.xfast ? (8 + k) * static_cast<long long>(N) + v0 - W
+                        : (6 + k) * static_cast<long long>(N) + v0 - 1;
+  }
+  const int r_step = s.xfast ? W * nc : nc, b_step = s.xfast ? W : 1;
+  auto r_at = [&](int l, int j) {
+    return rl ? rl[static_cast<long long>(l) * kd + j] : r[op_r[j] + static_cast<long long>(l) * r_step];
   };
-  load_next();
+  auto b_at = [&](int l, int j) { return coef[op_b[j] + static_cast<long long>(l) * b_step]; };
+  cl_sync();  // barriers and op_r / op_b initialised (cluster-wide: before any remote arrival)
 
-  constexpr int PS = 2;
-  double pf_r[PS], pf_b[PS], pf_y[PS];
-  auto prefetch = [&](int t) {
-#pragma unroll
-    for (int q = 0; q < PS; ++q) {
-      pf_r[q] = pf_b[q] = pf_y[q] = 0.0;
-      if (t >= nl) continue;
-      const int l = chain_line(phase, chain, L, t);
-      const int j = tid + kST * q;
-      if (j < kd) {
-        if (phase == 0) {
-          pf_r[q] = rl ? rl[static_cast<long long>(l) * kd + j] : r[gidx(s, l, j, W, nc)];
-          if (t > 0) pf_b[q] = bcoef(s, coef, N, W, nc, chain == 0 ? l : l + 1, j);
-        } else if (t == 0) {
-          double w = rl ? rl[static_cast<long long>(l) * kd + j] : r[gidx(s, l, j, W, nc)];
-          if (m > 0) w -= bcoef(s, coef, N, W, nc, m, j) * yl[static_cast<long long>(m - 1) * kd + j];
-          if (m < L - 1)
-            w -= bcoef(s, coef, N, W, nc, m + 1, j) * yl[static_cast<long long>(m + 1) * kd + j];
-          pf_r[q] = w;
-        } else {
-          pf_b[q] = bcoef(s, coef, N, W, nc, chain == 0 ? l + 1 : l, j);
-        }
+  // my tile of line step t -> stage t & 1 (one bulk copy per warp: the warp rewrites only its
+  // own region, after its own reads of line t - 2), line step t + 1 into L2; lane 0 only
+  auto issue_tile = [&](int t) {
+    if (!has_tile || t >= nl || (dbg & 4)) return;
+    const double* Fl = F + static_cast<long long>(chain_line(phase, chain, L, t)) * s.line_sz;
+    fence_proxy_async();
+    bulk_g2s(stage + static_cast<size_t>(t & 1) * stage_doubles + my_off, Fl + my_src,
+             static_cast<uint32_t>(my_sz) * 8u, &full[t & 1]);
+    if (t + 1 < nl)
+      bulk_prefetch_l2(F + static_cast<long long>(chain_line(phase, chain, L, t + 1)) * s.line_sz + my_src,
+                       static_cast<uint32_t>(my_sz) * 8u);
+  };
+  if (tid == 0 && !(dbg & 4)) {
+    mbar_expect_tx(&full[0], static_cast<uint32_t>(cta_doubles) * 8u);
+    if (nl > 1) mbar_expect_tx(&full[1], static_cast<uint32_t>(cta_doubles) * 8u);
+  }
+  if (lane == 0) issue_tile(0), issue_tile(1);
+  // operand of line step 0, computed locally; later operands come from the owners, who form
+  // w of line t + 1 from their x of line t:
+  //   forward   w = r_l - b o x_prev,  backward  w = b_next o x_next
+  // (the backward sweep starts at the middle line: w = r_m - b_m y_{m-1} - b_{m+1} y_{m+1})
+  if (tid < kdp) {
+    double w = 0.0;
+    if (tid < kd) {
+      const int l = chain_line(phase, chain, L, 0);
+      w = r_at(l, tid);
+      if (phase == 1) {
+        if (m > 0) w -= b_at(m, tid) * yl[static_cast<long long>(m - 1) * kd + tid];
+        if (m < L - 1) w -= b_at(m + 1, tid) * yl[static_cast<long long>(m + 1) * kd + tid];
       }
-      const int jo = rlo + tid + kST * q;
-      if (phase == 1 && t > 0 && jo < rhi) pf_y[q] = yl[static_cast<long long>(l) * kd + jo];
+    }
+    wv[tid] = w;
+  }
+  // owners, in registers: coupling and rhs of line step t + 1 (its operand) and, backward, y of
+  // line step t (the subtraction)
+  double pb0 = 0.0, pr0 = 0.0, py0 = 0.0, pb1 = 0.0, pr1 = 0.0, py1 = 0.0;
+  auto owner_prefetch = [&](int tw, int ty) {  // operand terms of step tw, y of step ty
+    pb0 = pr0 = py0 = pb1 = pr1 = py1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int i = q == 0 ? io0 : io1;
+      if ((q == 0 ? ob0 : ob1) < 0 || i >= kd) continue;
+      double b = 0.0, rr = 0.0, y = 0.0;
+      if (tw < nl) {
+        const int l = chain_line(phase, chain, L, tw);
+        b = b_at(phase == 0 ? (chain == 0 ? l : l + 1) : (chain == 0 ? l + 1 : l), i);
+        if (phase == 0) rr = r_at(l, i);
+      }
+      if (phase == 1 && ty >= 1 && ty < nl)
+        y = yl[static_cast<long long>(chain_line(phase, chain, L, ty)) * kd + i];
+      if (q == 0) pb0 = b, pr0 = rr, py0 = y; else pb1 = b, pr1 = rr, py1 = y;
     }
   };
-  prefetch(0);
-  __syncthreads();
+  if (owner) owner_prefetch(1, 0);
+  __syncthreads();  // operand of line 0
   PROF_DECL
 
   for (int t = 0; t < nl; ++t) {
     const int l = chain_line(phase, chain, L, t);
-    const bool subtract = phase == 1 && t > 0;
-    double cur_y[PS];
-#pragma unroll
-    for (int q = 0; q < PS; ++q) {
-      const int j = tid + kST * q;
-      if (j < kd)
-        wv[j] = (phase == 0) ? pf_r[q] - pf_b[q] * xprev[j]
-                             : (t == 0 ? pf_r[q] : pf_b[q] * xprev[j]);
-      cur_y[q] = pf_y[q];
+    const uint32_t par = t & 1;
+    if (t > 0) mbar_wait_g(&w_bar[par], ((t - 1) >> 1) & 1);  // operand of line t, all owners
+    const double* wt = wv + par * kdp_max;
+    PROF_MARK(0); TL_MARK(0);
+    if (tid == 0 && t + 1 < nl) {
+      mbar_arrive_expect(&w_bar[par ^ 1], w_tx);
+      // stage (t + 1) & 1: the phase of line t - 1 has completed (its contributions are in
+      // the operand of line t); the copies of line t + 1 may already be landing
+      if (t >= 1 && !(dbg & 4)) mbar_expect_tx(&full[(t + 1) & 1], static_cast<uint32_t>(cta_doubles) * 8u);
     }
-    prefetch(t + 1);
-    __syncthreads();
-    PROF_MARK(0);
-    double colacc[MAXM];
+    if (lane == 0) {
+      if (ob0 >= 0) mbar_arrive_expect(&blk_bar[ob0], blk_tx0);
+      if (ob1 >= 0) mbar_arrive_expect(&blk_bar[ob1], blk_tx1);
+    }
+    if (has_tile) {
+      // my tile from its stage into registers. In the diagonal tile the entries right of the
+      // diagonal are zero and the diagonal is halved: the row and the column partial take the
+      // same FMA loop and add up to the full term.
+      double a[8][4];
+      if (!(dbg & 4)) mbar_wait_g(&full[par], (t >> 1) & 1);
+      const double* Ts = stage + static_cast<size_t>(par) * stage_doubles + my_off;
+      if (!diag && th == 32) {
+        const double* p = Ts + 256 * rg + 2 * cg;
 #pragma unroll
-    for (int mm = 0; mm < MAXM; ++mm) colacc[mm] = 0.0;
-    for (int i = rlo + warp; i < rhi; i += kSW) {
-      double cur[MAXM];
+        for (int k = 0; k < 8; ++k) {
+          const double2 v0 = *reinterpret_cast<const double2*>(p + 32 * k);
+          const double2 v1 = *reinterpret_cast<const double2*>(p + 32 * k + 16);
+          a[k][0] = v0.x, a[k][1] = v0.y, a[k][2] = v1.x, a[k][3] = v1.y;
+        }
+      } else if (!diag) {  // last tile row: th < 32 rows
+        const double* p = Ts + 256 * rg + 2 * cg;
 #pragma unroll
-      for (int mm = 0; mm < MAXM; ++mm) cur[mm] = buf[mm];
-      ni += kSW;
-      load_next();  // next row (possibly of the next line) in flight during this row
-      const double wi = wv[i];
-      double racc = 0.0;
+        for (int k = 0; k < 8; ++k) {
+          const bool live = 8 * rg + k < th;
+          const double2 v0 = live ? *reinterpret_cast<const double2*>(p + 32 * k) : make_double2(0.0, 0.0);
+          const double2 v1 = live ? *reinterpret_cast<const double2*>(p + 32 * k + 16) : make_double2(0.0, 0.0);
+          a[k][0] = v0.x, a[k][1] = v0.y, a[k][2] = v1.x, a[k][3] = v1.y;
+        }
+      } else {  // packed lower rows: row rr at prow_off(rr), rr + 1 entries padded to even
+        int ro = prow_off32(8 * rg);
 #pragma unroll
-      for (int mm = 0; mm < MAXM; ++mm) {
-        const int j = lane + 32 * mm;
-        if (32 * mm > i) break;
-        if (j <= i) {
-          racc = fma(cur[mm], wv[j], racc);
-          if (j < i) colacc[mm] = fma(cur[mm], wi, colacc[mm]);
+        for (int k = 0; k < 8; ++k) {
+          const int rr = 8 * rg + k;
+          const bool live = rr < th;
+          const double2 v0 = live && 2 * cg <= rr ? *reinterpret_cast<const double2*>(Ts + ro + 2 * cg)
+                                                 : make_double2(0.0, 0.0);
+          const double2 v1 = live && 16 + 2 * cg <= rr
+                                 ? *reinterpret_cast<const double2*>(Ts + ro + 16 + 2 * cg)
+                                 : make_double2(0.0, 0.0);
+          a[k][0] = v0.x, a[k][1] = v0.y, a[k][2] = v1.x, a[k][3] = v1.y;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int cc = 2 * cg + (c & 1) + (c & 2 ? 16 : 0);
+            a[k][c] = cc > rr ? 0.0 : (cc == rr ? 0.5 * a[k][c] : a[k][c]);
+          }
+          ro += (rr + 2) & ~1;
         }
       }
-#pragma unroll
-      for (int off = 16; off; off >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, off);
-      if (lane == 0) yrow[i] = racc;
-    }
-    PROF_MARK(2);
-#pragma unroll
-    for (int mm = 0; mm < MAXM; ++mm) {
-      const int j = lane + 32 * mm;
-      if (j < rhi) colpart[warp * kd_max + j] = colacc[mm];
-    }
-    __syncthreads();
-    PROF_MARK(3);
-    int owner = 0;
-    for (int j = tid; j < rhi; j += kST) {
-      double tv = (j >= rlo) ? yrow[j] : 0.0;
-#pragma unroll 4
-      for (int w = 0; w < kSW; ++w) tv += colpart[w * kd_max + j];
-      while (owner + 1 < C && row_lo(owner + 1, C, kd) <= j) ++owner;
-      if (C == 1)
-        red[j] = tv;
-      else
-        cl_map(red, static_cast<unsigned>(owner))[crank * kd_max + j] = tv;
-    }
-    if (C == 1) __syncthreads(); else cl_sync();
-    PROF_MARK(4);
-#pragma unroll
-    for (int q = 0; q < PS; ++q) {
-      const int j = rlo + tid + kST * q;
-      if (j >= rhi) continue;
-      double tv = 0.0;
-      if (C == 1) {
-        tv = red[j];
-      } else {
-        for (int c = crank; c < C; ++c) tv += red[c * kd_max + j];
+      double racc[8], cacc[4];
+      double wc[4];
+      {
+        const double2 u0 = *reinterpret_cast<const double2*>(wt + jc0);
+        const double2 u1 = *reinterpret_cast<const double2*>(wt + jc0 + 16);
+        wc[0] = u0.x, wc[1] = u0.y, wc[2] = u1.x, wc[3] = u1.y;
       }
-      const long long k = static_cast<long long>(l) * kd + j;
-      double v;
-      if (!subtract) {
-        v = tv;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cacc[c] = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double wr = wt[i0 + k];
+        racc[k] = a[k][0] * wc[0];
+#pragma unroll
+        for (int c = 1; c < 4; ++c) racc[k] = fma(a[k][c], wc[c], racc[k]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cacc[c] = fma(a[k][c], wr, cacc[c]);
+      }
+      PROF_MARK(2); TL_MARK(2);
+      // rows: sum over the 8 lanes of the row group (lane bits 0-2); lane ends with row
+      // i0 + cg. Columns: sum over the 4 row groups (lane bits 3-4); lane ends with column
+      // c = rg of its four.
+      {
+        const bool b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double send = b2 ? racc[k] : racc[k + 4];
+          racc[k] = (b2 ? racc[k + 4] : racc[k]) + __shfl_xor_sync(~0u, send, 4);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const double send = b1 ? racc[k] : racc[k + 2];
+          racc[k] = (b1 ? racc[k + 2] : racc[k]) + __shfl_xor_sync(~0u, send, 2);
+        }
+        {
+          const double send = b0 ? racc[0] : racc[1];
+          racc[0] = (b0 ? racc[1] : racc[0]) + __shfl_xor_sync(~0u, send, 1);
+        }
+        const bool b4 = lane & 16, b3 = lane & 8;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double send = b4 ? cacc[c] : cacc[c + 2];
+          cacc[c] = (b4 ? cacc[c + 2] : cacc[c]) + __shfl_xor_sync(~0u, send, 16);
+        }
+        {
+          const double send = b3 ? cacc[0] : cacc[1];
+          cacc[0] = (b3 ? cacc[1] : cacc[0]) + __shfl_xor_sync(~0u, send, 8);
+        }
+      }
+      if (orow == crank) slots[er] = racc[0]; else st_async_to(er_remote, racc[0], er_bar);
+      if (ocol == crank) slots[ec] = cacc[0]; else st_async_to(ec_remote, cacc[0], ec_bar);
+      if (orow == crank || ocol == crank) {
+        __syncwarp();
+        if (lane == 0) {
+          if (orow == crank) mbar_arrive(&blk_bar[TI / C]);
+          if (ocol == crank) mbar_arrive(&blk_bar[TJ / C]);
+        }
+      }
+      PROF_MARK(3); TL_MARK(3);
+      // the tile is in registers (consumed): its stage region takes line step t + 2
+      if (lane == 0) issue_tile(t + 2);
+    }
+    if (owner) {
+      // my blocks' contributions, summed in a fixed order (contribution k into acc[k & 3])
+      mbar_wait_g(&blk_bar[ob0], par);
+      if (ob1 >= 0) mbar_wait_g(&blk_bar[ob1], par);
+      PROF_MARK(5); TL_MARK(5);
+      const double* s0 = slots + static_cast<size_t>(ob0) * (nt + 1) * 32 + lane;
+      const double* s1 = slots + static_cast<size_t>(ob1 < 0 ? ob0 : ob1) * (nt + 1) * 32 + lane;
+      double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
+      int k = 0;
+      for (; k + 3 <= nt; k += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a0[u] += s0[(k + u) * 32], a1[u] += s1[(k + u) * 32];
+      }
+      // remainder (k is a multiple of 4 here: contributions k, k + 1, k + 2 -> acc 0, 1, 2)
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+        if (k + u <= nt) a0[u] += s0[(k + u) * 32], a1[u] += s1[(k + u) * 32];
+      const double tv0 = (a0[0] + a0[1]) + (a0[2] + a0[3]);
+      const double tv1 = (a1[0] + a1[1]) + (a1[2] + a1[3]);
+      // x of my rows, the outputs, and the operand of the next line
+      const bool more = t + 1 < nl;
+      double wn0 = 0.0, wn1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int i = q == 0 ? io0 : io1;
+        if ((q == 0 ? ob0 : ob1) < 0 || i >= kd) continue;
+        const double tv = q == 0 ? tv0 : tv1;
+        const long long e = static_cast<long long>(l) * kd + i;
+        double v;
         if (phase == 0) {
-          yl[k] = v;
-          if (L == 1) zl[k] = v;
-        } else if (chain == 0) {
-          zl[k] = v;
+          v = tv;
+          yl[e] = v;
+          if (L == 1) zl[e] = v;
+        } else if (t == 0) {
+          v = tv;
+          if (chain == 0) zl[e] = v;  // middle line, written once
+        } else {
+          v = (q == 0 ? py0 : py1) - tv;
+          zl[e] = v;
         }
-      } else {
-        v = cur_y[q] - tv;
-        zl[k] = v;
+        const double b = q == 0 ? pb0 : pb1, rr = q == 0 ? pr0 : pr1;
+        const double w = phase == 0 ? rr - b * v : b * v;
+        if (q == 0) wn0 = w; else wn1 = w;
       }
-      if (C == 1) {
-        xprev[j] = v;
-      } else {
-        for (int c = 0; c < C; ++c) cl_map(xprev, static_cast<unsigned>(c))[j] = v;
+      if (more) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if ((q == 0 ? ob0 : ob1) < 0) continue;
+          const int i = q == 0 ? io0 : io1;
+          const double w = q == 0 ? wn0 : wn1;
+          double* wn = wv + (par ^ 1) * kdp_max + i;
+          const uint32_t wl = smem_u32(wn), bl = smem_u32(&w_bar[par ^ 1]);
+          for (int c = 0; c < C; ++c)
+            if (c != crank) st_async_to(mapa_u32(wl, c), w, mapa_u32(bl, c));
+          *wn = w;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&w_bar[par ^ 1]);
+          if (ob1 >= 0) mbar_arrive(&w_bar[par ^ 1]);
+        }
       }
+      owner_prefetch(t + 2, t + 1);
+      PROF_MARK(6); TL_MARK(6);
     }
-    if (C == 1) __syncthreads(); else cl_sync();
-    PROF_MARK(5);
   }
-  PROF_FLUSH(16);
+  PROF_FLUSH(48);
 }
 
 }  // namespace
 
 long long packed_line_size(int kd) { return prow_off(kd); }
 
-void debug_prof(unsigned long long* out, bool reset) {
+void debug_prof(unsigned long long* out, int reset) {
 #ifdef FFB_PROFILE
   FFB_CUDA(cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 64));
+  if (reset == 2) {  // the tile kernel's event timeline instead
+    FFB_CUDA(cudaMemcpyFromSymbol(out, g_tl, sizeof(g_tl)));
+    return;
+  }
   if (reset) {
     static const unsigned long long z[64] = {0};
     FFB_CUDA(cudaMemcpyToSymbol(g_prof, z, sizeof(z)));
@@ -1499,6 +1807,80 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
   }
 }
 
+// placement tables of the register-tiled solve kernel (see c_tile_of), once per device.
+// Tiles are weighed by their bytes with full tile rows (the last row of a line is shorter,
+// so a CTA's share of any line fits the stage sized by tile_stage_doubles).
+static void build_tile_tables(unsigned char (*tile_of)[kTileMaxNt + 1][8][kTileWarps],
+                              unsigned char (*nloc)[kTileMaxNt + 1][kTileMaxNt],
+                              unsigned char (*owner)[kTileMaxNt + 1][kTileMaxNt],
+                              int (*stage)[kTileMaxNt + 1]) {
+  std::memset(tile_of, 255, sizeof(unsigned char) * 4 * (kTileMaxNt + 1) * 8 * kTileWarps);
+  std::memset(nloc, 0, sizeof(unsigned char) * 4 * (kTileMaxNt + 1) * kTileMaxNt);
+  std::memset(owner, 0, sizeof(unsigned char) * 4 * (kTileMaxNt + 1) * kTileMaxNt);
+  for (int ci = 0; ci < 4; ++ci) {
+    const int C = 1 << ci;
+    for (int nt = 1; nt <= kTileMaxNt; ++nt) {
+      stage[ci][nt] = 0;
+      const int T = nt * (nt + 1) / 2;
+      if (T > kTileWarps * C) continue;
+      const int total = 1024 * (T - nt) + 544 * nt;
+      const int cap = (total + C - 1) / C + 1024;  // bytes/8 per CTA, one tile of slack
+      int cnt[8] = {0}, load[8] = {0};
+      int tau = 0;
+      for (int I = 0; I < nt; ++I)
+        for (int J = 0; J <= I; ++J, ++tau) {
+          const int wgt = I == J ? 544 : 1024;
+          const int a = I % C, b = J % C;
+          auto fits = [&](int c) { return cnt[c] < kTileWarps && load[c] + wgt <= cap; };
+          int c = load[a] <= load[b] ? a : b;
+          if (!fits(c)) c = c == a ? b : a;
+          if (!fits(c)) {  // both owners full: the least loaded CTA with a free warp
+            c = -1;
+            for (int q = 0; q < C; ++q)
+              if (cnt[q] < kTileWarps && (c < 0 || load[q] < load[c])) c = q;
+          }
+          tile_of[ci][nt][c][cnt[c]++] = static_cast<unsigned char>(tau);
+          load[c] += wgt;
+          if (c == a) ++nloc[ci][nt][I];  // row partial stays local
+          if (c == b) ++nloc[ci][nt][J];  // column partial stays local
+        }
+      for (int c = 0; c < C; ++c) {
+        stage[ci][nt] = std::max(stage[ci][nt], load[c]);
+        const int n_own = (nt - c + C - 1) / C, nfree = kTileWarps - cnt[c];
+        const bool dedicated = nfree > 0 && (n_own + nfree - 1) / nfree <= kTileMaxOwn;
+        for (int q = 0; q < n_own; ++q)
+          owner[ci][nt][q * C + c] =
+              static_cast<unsigned char>(dedicated ? kTileWarps - 1 - q % nfree : q);
+      }
+    }
+  }
+}
+static unsigned char h_tile_of[4][kTileMaxNt + 1][8][kTileWarps];
+static unsigned char h_nloc[4][kTileMaxNt + 1][kTileMaxNt];
+static unsigned char h_owner[4][kTileMaxNt + 1][kTileMaxNt];
+static int h_stage[4][kTileMaxNt + 1];
+static void ensure_tile_tables_host() {
+  static bool built = false;
+  if (!built) build_tile_tables(h_tile_of, h_nloc, h_owner, h_stage), built = true;
+}
+static void set_tile_tables() {
+  static unsigned done_mask = 0;
+  int dev = 0;
+  FFB_CUDA(cudaGetDevice(&dev));
+  if (dev < 32 && (done_mask >> dev) & 1u) return;
+  ensure_tile_tables_host();
+  FFB_CUDA(cudaMemcpyToSymbol(c_tile_of, h_tile_of, sizeof(h_tile_of)));
+  FFB_CUDA(cudaMemcpyToSymbol(c_nloc, h_nloc, sizeof(h_nloc)));
+  FFB_CUDA(cudaMemcpyToSymbol(c_owner, h_owner, sizeof(h_owner)));
+  if (dev < 32) done_mask |= 1u << dev;
+}
+
+void tile_pack(const SubInfo* d_subs, int nsub, int L_max, const double* fac, double* fac_t,
+               cudaStream_t st) {
+  k_tile_pack<<<dim3(L_max, nsub), 256, 0, st>>>(d_subs, fac, fac_t);
+  FFB_LAUNCHED();
+}
+
 void set_solve_dbg(int v) { FFB_CUDA(cudaMemcpyToSymbol(g_solve_dbg, &v, sizeof(int))); }
 
 SolvePlan solve_plan(int kd_max, int C) {
@@ -1537,9 +1919,38 @@ SolvePlan solve_plan(int kd_max, int C) {
   pl.smem = fixed + static_cast<size_t>(stages) * cap * sizeof(double);
   pl.maxm = (kd_max + 31) / 32;
   pl.kd_max = kd_max;
-  pl.ldg = 0;
-  if (const char* e = std::getenv("FFB_SOLVE")) pl.ldg = std::string(e) == "ldg";
-
+  // register-tiled kernel when the line's 32x32 tiles fit one per warp over the cluster and
+  // two lines of a CTA's share fit shared memory (the latency regime: c1, c2); FFB_SOLVE=ring
+  // forces the shared-memory ring kernel
+  const int nt = (kd_max + 31) / 32;
+  pl.tile = 0;
+  if (nt <= kTileMaxNt && nt * (nt + 1) / 2 <= kTileWarps * C) {
+    ensure_tile_tables_host();
+    const int ci = C == 1 ? 0 : (C == 2 ? 1 : (C == 4 ? 2 : 3));
+    // a stage holds a CTA's tiles of one line: the most over the CTAs and every line width
+    // up to kd_max (each width uses the table of its own tile count)
+    int stage = 0;
+    for (int kd = 1; kd <= kd_max; ++kd) {
+      const int n = (kd + 31) / 32;
+      for (int c = 0; c < C; ++c) {
+        int sz = 0;
+        for (int q = 0; q < kTileWarps; ++q) {
+          const int tq = h_tile_of[ci][n][c][q];
+          if (tq == 255) break;
+          int I = 0;
+          while ((I + 1) * (I + 2) / 2 <= tq) ++I;
+          sz += tile_size(I, tq - I * (I + 1) / 2, kd);
+        }
+        stage = std::max(stage, sz);
+      }
+    }
+    pl.stage_doubles = (stage + 1) & ~1;
+    const int nown = (nt + C - 1) / C;
+    const size_t smem = 256 + (2 * static_cast<size_t>(pl.stage_doubles) + 4 * static_cast<size_t>(nt) * 32 +
+                               static_cast<size_t>(nown) * (nt + 1) * 32) * sizeof(double);
+    if (smem <= 227 * 1024) pl.tile = 1, pl.smem = smem;
+  }
+  if (const char* e = std::getenv("FFB_SOLVE")) pl.tile = pl.tile && std::string(e) != "ring";
   return pl;
 }
 
@@ -1549,15 +1960,15 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
                            double* ylocal, double* zlocal, int W, int nc, const int* flags,
                            const double* rlocal, cudaStream_t st) {
   for (int phase = 0; phase <= 1; ++phase) {
-    if (pl.ldg) {
-      const size_t smem = (static_cast<size_t>(kSW) * pl.kd_max + 11 * pl.kd_max) * sizeof(double);
-      launch_cluster(k_line_solve_ldg<M>, 2 * nsub * pl.C, kST, smem, pl.C, st, d_subs, fac, coef,
-                     N, r, ylocal, zlocal, W, nc, pl.kd_max, phase, flags, rlocal);
+    if (pl.tile) {
+      set_tile_tables();
+      launch_cluster(k_line_solve_tile, 2 * nsub * pl.C, kTileThreads, pl.smem, pl.C, st, d_subs,
+                     fac, coef, N, r, ylocal, zlocal, W, nc, (pl.maxm) * 32, pl.stage_doubles,
+                     phase, flags, rlocal);
     } else {
       launch_cluster(k_line_solve<M>, 2 * nsub * pl.C, kST, pl.smem, pl.C, st, d_subs, fac, coef,
                      N, r, ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, pl.row_cost,
-                     phase, flags,
-                     rlocal);
+                     phase, flags, rlocal);
     }
     FFB_LAUNCHED();
   }

@@ -40,7 +40,7 @@ void note_launch(long long n) { g_launches += n; }
 
 // fill kernels live in operator.cu's translation unit family; declared here
 void fill(double* p, double v, long long n, cudaStream_t st);
-void debug_prof(unsigned long long* out, bool reset);
+void debug_prof(unsigned long long* out, int reset);
 
 template <class T>
 struct DBuf {
@@ -111,7 +111,8 @@ struct ffb_ctx {
   std::vector<SubInfo> subs;
   DBuf<SubInfo> d_subs;
   DBuf<AxisMap> d_col, d_row;
-  DBuf<double> fac, dscratch, ylocal, zlocal, rlocal, xlocal, G0, G1, incs;
+  DBuf<double> fac, fac_t, dscratch, ylocal, zlocal, rlocal, xlocal, G0, G1, incs;
+  int L_max = 0;  // lines of the longest subdomain
   DBuf<int> own_col, own_row;
   // linsolve boundary on an explicit CSR system (ffb_csr_*)
   DBuf<int> csr_rp, csr_ci, csr_perm, csr_iperm, csr_bad;
@@ -320,6 +321,9 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
   FFB_CUDA(cudaMemcpyAsync(c->d_row.p, row.data(), H * sizeof(AxisMap), cudaMemcpyHostToDevice,
                            c->st));
   c->fac.ensure(fac_off);
+  if (c->plan.tile) c->fac_t.ensure(fac_off);  // tile-major copy for the register-tiled solve
+  c->L_max = 0;
+  for (int p = c->s_lo; p < c->s_hi; ++p) c->L_max = std::max(c->L_max, c->subs[p].L);
   c->dscratch.ensure(factor_scratch_doubles(c->s_hi - c->s_lo, kd_max));
   c->ylocal.ensure(vec_off);
   c->zlocal.ensure(vec_off);
@@ -350,6 +354,7 @@ void ensure_factor(ffb_ctx* c, int nc) {
   line_factor(c->d_subs.p + c->s_lo, np, c->ccl, c->nbf, c->kd_max, c->coef.p, c->N, c->W, nc,
               c->fac.p, c->dscratch.p, static_cast<long long>(c->kd_max) * c->kd_max, c->d_bad.p,
               c->st, changed);
+  if (c->plan.tile) tile_pack(c->d_subs.p + c->s_lo, np, c->L_max, c->fac.p, c->fac_t.p, c->st);
   FFB_CUDA(cudaMemcpyAsync(c->alpha_fact.ensure(c->ntri), c->alpha.p, c->ntri * sizeof(double),
                            cudaMemcpyDeviceToDevice, c->st));
   std::vector<int> bad(np);
@@ -365,6 +370,10 @@ void ensure_factor(ffb_ctx* c, int nc) {
   c->fact_valid = 1;
 }
 
+// the factor layout the subdomain solve streams: the tile-major copy for the register-tiled
+// kernel, else the packed rows
+const double* solve_factor(const ffb_ctx* c) { return c->plan.tile ? c->fac_t.p : c->fac.p; }
+
 void launch_asm(ffb_ctx* c, int nc, const double* rvec, const int* flags) {
   EventPair* ev = nullptr;
   if (c->time_asm) {
@@ -374,7 +383,7 @@ void launch_asm(ffb_ctx* c, int nc, const double* rvec, const int* flags) {
     FFB_CUDA(cudaEventCreate(&ev->b));
     FFB_CUDA(cudaEventRecord(ev->a, c->st));
   }
-  line_solve(c->d_subs.p + c->s_lo, c->s_hi - c->s_lo, c->plan, c->fac.p, c->coef.p, c->N, rvec,
+  line_solve(c->d_subs.p + c->s_lo, c->s_hi - c->s_lo, c->plan, solve_factor(c), c->coef.p, c->N, rvec,
              c->ylocal.p, c->zlocal.p, c->W, nc, flags, c->st);
   if (ev) FFB_CUDA(cudaEventRecord(ev->b, c->st));
 }
@@ -600,7 +609,7 @@ int ffb_destroy(ffb_ctx* ctx) {
 // development probe: clock64 phase accumulators of the factor/solve kernels (zeros unless
 // built with FFB_PROFILE=1); not part of the public header
 int ffb_debug_prof(unsigned long long* out64, int reset) {
-  return guard([&] { debug_prof(out64, reset != 0); });
+  return guard([&] { debug_prof(out64, reset); });
 }
 
 // development probe: average time of `n` applications of the Schwarz preconditioner with
@@ -1083,13 +1092,13 @@ int ffb_schwarz_solve(ffb_ctx* c, int n_iters, int nc, int adapt, int n_adapt, d
       ensure_coef(c, nc);
       ensure_factor(c, nc);  // refactors iff alpha changed (schwarz.cpp:238-241)
       ras_rhs(c->d_subs.p, np, c->coef.p, c->b.p, G, N, c->W, c->H, nc, rl, c->st);
-      line_solve(c->d_subs.p, np, c->plan, c->fac.p, c->coef.p, N, nullptr, c->ylocal.p,
+      line_solve(c->d_subs.p, np, c->plan, solve_factor(c), c->coef.p, N, nullptr, c->ylocal.p,
                  c->zlocal.p, c->W, nc, nullptr, c->st, rl);
       const double* dl = nullptr;
       if (refine) {  // x += A^-1 (rhs - A x)   (schwarz.cpp:242-247)
         vec_copy(xl, c->zlocal.p, vec_len, c->st);
         ras_residual(c->d_subs.p, np, c->coef.p, N, c->W, nc, rl, xl, rl, c->st);
-        line_solve(c->d_subs.p, np, c->plan, c->fac.p, c->coef.p, N, nullptr, c->ylocal.p,
+        line_solve(c->d_subs.p, np, c->plan, solve_factor(c), c->coef.p, N, nullptr, c->ylocal.p,
                    c->zlocal.p, c->W, nc, nullptr, c->st, rl);
         dl = c->zlocal.p;
       } else {

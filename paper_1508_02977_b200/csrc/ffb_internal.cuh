@@ -90,10 +90,13 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max, con
 void changed_lines(const SubInfo* d_subs, int nsub, const double* alpha, const double* alpha_fact,
                    int W, int H, int2* changed, cudaStream_t st);
 struct SolvePlan {
-  int stages, cap, maxm, C, kd_max, ldg, row_cost, ncs;
+  int stages, cap, maxm, C, kd_max, tile, row_cost, ncs, stage_doubles;
   size_t smem;
 };
 SolvePlan solve_plan(int kd_max, int C);
+// packed line inverses -> the tile-major copy the register-tiled solve streams (plan.tile)
+void tile_pack(const SubInfo* d_subs, int nsub, int L_max, const double* fac, double* fac_t,
+               cudaStream_t st);
 void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,
                 const double* coef, size_t N, const double* r, double* ylocal, double* zlocal,
                 int W, int nc, const int* flags, cudaStream_t st,
