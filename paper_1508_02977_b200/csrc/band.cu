@@ -60,7 +60,17 @@ __device__ unsigned long long g_tl[16][16][8];
     if (blockIdx.x == 0 && phase == 0 && t >= 8 && t < 24 && (threadIdx.x & 31) == 0) \
       g_tl[t - 8][threadIdx.x >> 5][i] = clock64();                                  \
   } while (0)
+// per-warp event timeline of CTA 0 for the sweep steps of line 10 (factor kernel)
+__device__ unsigned long long g_ftl[16][16][8];
+#define FTL_MARK(i)                                                                    \
+  do {                                                                                 \
+    if (blockIdx.x == 0 && bad_base == 10 * kd && step < 16 && (threadIdx.x & 31) == 0) \
+      g_ftl[step][threadIdx.x >> 5][i] = clock64();                                    \
+  } while (0)
 #else
+#define FTL_MARK(i) \
+  do {              \
+  } while (0)
 #define TL_MARK(i) \
   do {             \
   } while (0)
@@ -144,6 +154,13 @@ __device__ __forceinline__ unsigned cl_size() {
 __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
                    : "memory");
+}
+// the same barrier in two halves (arrive early, wait late)
+__device__ __forceinline__ void cl_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cl_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // address of `p` (a shared-memory variable of this CTA) in CTA `rank` of the cluster
 template <class T>
@@ -469,7 +486,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       cnt[(step + 1) & 1] = 0;
       cnt[3 + ((step + 1) & 1)] = 0;
     }
-    PROF_MARK(1);
+    PROF_MARK(1); FTL_MARK(0);
     // ---- Z = A_RK Li^T, thread per row: all loads issued first, 32 independent chains
     for (int i = tid; i < kdp; i += kFT) {
       const bool live = i < kd && (i < k0 || i >= k1);
@@ -498,7 +515,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
     // la_reg: A_RK is overwritten during this step's tile phase, so every CTA's Z must be
     // done first (cluster barrier); otherwise a CTA barrier suffices here
     if (la_reg && C > 1) cl_sync(); else __syncthreads();
-    PROF_MARK(2);
+    PROF_MARK(2); FTL_MARK(1);
     // ---- A_RR -= Z Z^T, 32x32 tiles from a shared queue (tiles q, q + C, ... of the
     // cluster's CTA q). Look-ahead (la, single CTA): warp 0 first finishes the tile holding
     // the next pivot block and factors that block meanwhile.
@@ -511,13 +528,13 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       // so there is no ordering against the other CTAs' updates.
       kk_update<NB>(D, kd, zs, Z, nbk, k1, min(NB, kd - k1), P, lane, warp);
       asm volatile("bar.sync 2, 128;" ::: "memory");
-      PROF_MARK(6);
+      PROF_MARK(6); FTL_MARK(2);
       if (warp < 2)
         pivot_pair<NB>(P, NB + 1, k1, min(NB, kd - k1), P, Lnext, ir, first_bad, bad_base,
                        cnt + 2, ++pv_tag, nullptr);
       else
         ++pv_tag;
-      PROF_MARK(5);
+      PROF_MARK(5); FTL_MARK(3);
     } else if (warp == 0 && special >= 0) {
       {
         rupd_tile(D, kd, zs, Z, nbk, k0, k1, nx, nx, lane);
@@ -532,14 +549,27 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       // A_RK <- Z L^-1 (row tiles q, q + C, ... of the cluster) and A_KK, concurrently with the
       // trailing updates: they touch only the columns of K, which the tiles exclude
       if (q == C - 1 && warp == kFW - 1) tile_akk<NB>(D, kd, Li, k0, nbk, lane);
+#ifdef FFB_PROFILE
+      long long ftl_t0 = clock64(), ftl_n = 0;
+#endif
       for (;;) {
         int T = 0;
         if (lane == 0) T = q + C * atomicAdd(cnt + 3 + (step & 1), 1);
         T = __shfl_sync(~0u, T, 0);
         if (32 * T >= kd) break;
         tile_ark<NB>(D, kd, zs, Z, Li, 32 * T, k0, k1, lane);
+#ifdef FFB_PROFILE
+        ++ftl_n;
+#endif
       }
+#ifdef FFB_PROFILE
+      if (blockIdx.x == 0 && bad_base == 10 * kd && step < 16 && lane == 0)
+        g_ftl[step][warp][6] = (clock64() - ftl_t0) * 16 + ftl_n;
+#endif
     }
+#ifdef FFB_PROFILE
+    long long ftl_t1 = clock64(), ftl_m = 0;
+#endif
     for (;;) {
       int idx = 0;
       if (lane == 0) idx = q + C * atomicAdd(cnt + (step & 1), 1);
@@ -553,12 +583,19 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
         rupd_tile_mma(D, kd, zs, Z, nbk, k0, k1, TU, idx - TU * (TU + 1) / 2, lane);
       else
         rupd_tile(D, kd, zs, Z, nbk, k0, k1, TU, idx - TU * (TU + 1) / 2, lane);
+#ifdef FFB_PROFILE
+      ++ftl_m;
+#endif
     }
+#ifdef FFB_PROFILE
+    if (blockIdx.x == 0 && bad_base == 10 * kd && step < 16 && lane == 0)
+      g_ftl[step][warp][7] = (clock64() - ftl_t1) * 16 + ftl_m;
+#endif
     // all tile updates (and, across the cluster, all reads of A_RK for Z) are done
     if (!la_reg) {
       if (C > 1) cl_sync(); else __syncthreads();
     }
-    PROF_MARK(3);
+    PROF_MARK(3); FTL_MARK(4);
     if (la_reg) {
       // A_RK, A_KK done in the tile phase
     } else if (!la && warp == 0) {
@@ -578,7 +615,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
     }
     PROF_MARK(7);
     if (C > 1) cl_sync();  // A_RK, A_KK written cluster-wide before the next Z / pack
-    PROF_MARK(4);
+    PROF_MARK(4); FTL_MARK(5);
   }
   __syncthreads();
   PROF_FLUSH(32);
@@ -1675,8 +1712,9 @@ long long packed_line_size(int kd) { return prow_off(kd); }
 void debug_prof(unsigned long long* out, int reset) {
 #ifdef FFB_PROFILE
   FFB_CUDA(cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 64));
-  if (reset == 2) {  // the tile kernel's event timeline instead
-    FFB_CUDA(cudaMemcpyFromSymbol(out, g_tl, sizeof(g_tl)));
+  if (reset == 2 || reset == 3) {  // the solve (2) or factor (3) kernel's event timeline
+    if (reset == 2) FFB_CUDA(cudaMemcpyFromSymbol(out, g_tl, sizeof(g_tl)));
+    else FFB_CUDA(cudaMemcpyFromSymbol(out, g_ftl, sizeof(g_ftl)));
     return;
   }
   if (reset) {

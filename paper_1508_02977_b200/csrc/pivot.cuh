@@ -10,6 +10,8 @@
 // (shared) MIO pipe. The forward substitution for Li reuses the same rows.
 #pragma once
 
+#include <type_traits>
+
 namespace ffb {
 
 // row stride of the L^-1 tiles (even: rows stay 16-byte aligned for paired loads)
@@ -125,8 +127,10 @@ __device__ __noinline__ void pivot_pair(const double* src, long long ld, int k0,
       dkk = 1.0;
     }
     double r = rsqrt(dkk);
-#pragma unroll 1
-    for (int k = 0; k < NB; ++k) {
+    // step k touches rotated entries t < NB - k only (rows k + t < NB): the second half of
+    // the steps updates half the registers
+    auto step = [&](int k, auto width) {
+      constexpr int WD = decltype(width)::value;
       const double l = (lane == k) ? dkk * r : c[0] * r;
       double dn = __shfl_sync(~0u, c[1] - l * l, (k + 1) & 31);
       if (k + 1 < NB && (!(dn > 0.0) || !isfinite(dn))) {
@@ -141,21 +145,25 @@ __device__ __noinline__ void pivot_pair(const double* src, long long ld, int k0,
       if (lane == 0) st_release_shared(progress, tag * 64 + k + 1);
       c[0] = c[1] - row[1] * l;
 #pragma unroll
-      for (int t = 2; t < NB; t += 2) {
+      for (int t = 2; t < WD; t += 2) {
         const double2 v = *reinterpret_cast<const double2*>(row + t);
         c[t - 1] = c[t] - v.x * l;
         c[t] = c[t + 1] - v.y * l;
       }
-      c[NB - 1] = 0.0;
+      c[WD - 1] = 0.0;
       dkk = dn;
       r = rn;
-    }
+    };
+#pragma unroll 1
+    for (int k = 0; k < NB / 2; ++k) step(k, std::integral_constant<int, NB>());
+#pragma unroll 1
+    for (int k = NB / 2; k < NB; ++k) step(k, std::integral_constant<int, NB / 2>());
     first_bad = fb;
   } else {  // forward substitution for L^-1, one column of L behind
 #pragma unroll
     for (int t = 0; t < NB; ++t) c[t] = (t == lane) ? 1.0 : 0.0;
-#pragma unroll 1
-    for (int k = 0; k < NB; ++k) {
+    auto step = [&](int k, auto width) {
+      constexpr int WD = decltype(width)::value;
       while (ld_acquire_shared(progress) < tag * 64 + k + 1) {
       }
       __syncwarp();
@@ -167,13 +175,17 @@ __device__ __noinline__ void pivot_pair(const double* src, long long ld, int k0,
       const double* row = LR + k * NB;
       c[0] = c[1] - row[1] * y;
 #pragma unroll
-      for (int t = 2; t < NB; t += 2) {
+      for (int t = 2; t < WD; t += 2) {
         const double2 v = *reinterpret_cast<const double2*>(row + t);
         c[t - 1] = c[t] - v.x * y;
         c[t] = c[t + 1] - v.y * y;
       }
-      c[NB - 1] = 0.0;
-    }
+      c[WD - 1] = 0.0;
+    };
+#pragma unroll 1
+    for (int k = 0; k < NB / 2; ++k) step(k, std::integral_constant<int, NB>());
+#pragma unroll 1
+    for (int k = NB / 2; k < NB; ++k) step(k, std::integral_constant<int, NB / 2>());
   }
   __syncwarp();
 }
