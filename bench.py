@@ -15,6 +15,7 @@ and the time is the max over ranks.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -299,6 +300,14 @@ def main():
         pg.destroy_process_group()
         return
     asm_bytes = 8.0 * s.factor_doubles  # packed line inverses, forward + backward sweep
+    try:
+        from paper_1508_02977_b200 import _lib
+        fn = _lib.load().ffb_debug_solve_kernel
+        fn.restype, fn.argtypes = ctypes.c_int, [ctypes.c_void_p]
+        kind = fn(ctx.handle)
+    except Exception:
+        kind = -1
+    kname = {1: "k_line_solve_tile", 0: "k_line_solve"}.get(kind, "k_line_solve*")
     achieved = asm_bytes / (s.ms_asm_per_iter * 1e-3) / 1e9 if s.ms_asm_per_iter > 0 else None
     iters_total = s.pcg_iterations
     line = {
@@ -312,7 +321,10 @@ def main():
                    "l2": "flushed (256 MB write) between steps; band factors > L2"},
         "gpu_launches": int(launches),
         "e2e": e2e,
-        "roofline": {"bound": "hbm", "kernel": "k_line_solve (subdomain fwd/bwd sweeps)",
+        "roofline": {"bound": "hbm", "kernel": f"{kname} (subdomain fwd/bwd sweeps)",
+                     "unit_of_work": "one preconditioner application = forward + backward "
+                                     "sweep launch (bytes_per_launch / ms_per_launch are per "
+                                     "application)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
                      "traffic": profiled_traffic(cfg.name), "peak_kind": peak_kind,

@@ -612,6 +612,13 @@ int ffb_debug_prof(unsigned long long* out64, int reset) {
   return guard([&] { debug_prof(out64, reset); });
 }
 
+// development probe: which subdomain-solve kernel the resident partition uses (1 the
+// register-tiled k_line_solve_tile, 0 the shared-memory ring k_line_solve, -1 none yet)
+int ffb_debug_solve_kernel(ffb_ctx* c) {
+  if (!c || !c->have_part) return -1;
+  return c->plan.tile ? 1 : 0;
+}
+
 // development probe: average time of `n` applications of the Schwarz preconditioner with
 // the context's resident factorisation (after a solve), on the current residual vector
 int ffb_debug_time_asm(ffb_ctx* c, int nc, int n, int dbg, double* ms) {
