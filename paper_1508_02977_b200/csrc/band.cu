@@ -1962,7 +1962,9 @@ SolvePlan solve_plan(int kd_max, int C) {
   // forces the shared-memory ring kernel
   const int nt = (kd_max + 31) / 32;
   pl.tile = 0;
-  if (nt <= kTileMaxNt && nt * (nt + 1) / 2 <= kTileWarps * C) {
+  const char* force = std::getenv("FFB_SOLVE");
+  const bool ring_forced = force && std::string(force) == "ring";
+  if (!ring_forced && nt <= kTileMaxNt && nt * (nt + 1) / 2 <= kTileWarps * C) {
     ensure_tile_tables_host();
     const int ci = C == 1 ? 0 : (C == 2 ? 1 : (C == 4 ? 2 : 3));
     // a stage holds a CTA's tiles of one line: the most over the CTAs and every line width
@@ -1988,7 +1990,6 @@ SolvePlan solve_plan(int kd_max, int C) {
                                static_cast<size_t>(nown) * (nt + 1) * 32) * sizeof(double);
     if (smem <= 227 * 1024) pl.tile = 1, pl.smem = smem;
   }
-  if (const char* e = std::getenv("FFB_SOLVE")) pl.tile = pl.tile && std::string(e) != "ring";
   return pl;
 }
 

@@ -1,0 +1,87 @@
+"""The register-tiled subdomain solve (k_line_solve_tile, band.cu) against the shared-memory
+ring kernel (k_line_solve) and the oracle CG, on line widths that exercise its edge cases:
+a last tile row of full height (kd a multiple of 32), short last rows, one-tile lines, two
+components, and every cluster size the placement tables cover (FFB_CLUSTER = 1, 2, 4, 8).
+Both kernels apply the same block LDL^T preconditioner with different summation orders, so
+the converged fields agree to the solve tolerance, and each equals the oracle's.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from paper_1508_02977_b200 import flowfem as ff
+
+pytestmark = pytest.mark.gpu
+
+
+def rand_pair(H, W, seed):
+    rng = np.random.default_rng(seed)
+    f0 = rng.uniform(0, 255, (H, W))
+    f1 = np.clip(np.roll(f0, 1, axis=1) * 1.02 + rng.normal(0, 3, (H, W)), 0, 255)
+    return f0, f1
+
+
+def solve(t, a, l, px, py, ov, nc):
+    ctx = ff.Context(0)
+    try:
+        s = ff.SchwarzSolver(ctx)
+        s.set_terms(ff.DataTerms(t))
+        s.set_reg(ff.RegField(a, l))
+        s.set_partition(px, py, ov)
+        u, it, res = s.solve(components=nc, tol=1e-12)
+        fn = ctx.lib.ffb_debug_solve_kernel
+        fn.restype, fn.argtypes = C.c_int, [C.c_void_p]
+        return u.planes()[:nc], it, res, fn(ctx.handle)
+    finally:
+        ctx.close()
+
+
+# (H, W, px, py, ov, nc, cluster): kd = nc * short side of the free rectangle
+CASES = [
+    (40, 32, 1, 1, 0, 3, None),   # kd 96: three full tile rows, C = 8
+    (40, 32, 1, 1, 0, 3, "1"),    # one CTA: every block and tile local
+    (40, 32, 1, 1, 0, 2, "2"),    # kd 64, two components
+    (12, 9, 1, 1, 0, 3, None),    # kd 27: one diagonal tile, short
+    (96, 80, 4, 4, 2, 3, None),   # 16 subdomains, C = 4
+    (130, 160, 2, 2, 3, 3, None),  # kd ~ 200: seven tile rows, short last row, C = 8
+    (130, 160, 2, 2, 3, 3, "2"),  # the same on 2-CTA clusters (28 tiles on 32 warps)
+    (50, 44, 3, 2, 4, 2, "4"),    # two components on 4-CTA clusters
+]
+
+
+@pytest.mark.parametrize("H,W,px,py,ov,nc,cluster", CASES)
+def test_tile_solve_matches_ring_and_oracle(monkeypatch, port, H, W, px, py, ov, nc, cluster):
+    f0, f1 = rand_pair(H, W, 7 * H + W)
+    t = port.frames_to_terms(f0, f1, 1.0, 2.5)
+    rng = np.random.default_rng(H + W)
+    ntri = 2 * (W - 1) * (H - 1)
+    a = rng.uniform(20, 1000, ntri)
+    l = np.full(ntri, 1000.0)
+    if cluster:
+        monkeypatch.setenv("FFB_CLUSTER", cluster)
+    monkeypatch.delenv("FFB_SOLVE", raising=False)
+    u_t, it_t, res_t, kind_t = solve(t, a, l, px, py, ov, nc)
+    monkeypatch.setenv("FFB_SOLVE", "ring")
+    u_r, it_r, res_r, kind_r = solve(t, a, l, px, py, ov, nc)
+    assert kind_t == 1, "the register-tiled kernel was not selected"
+    assert kind_r == 0
+    assert res_t <= 1e-12 and res_r <= 1e-12
+    assert abs(it_t - it_r) <= 2  # same preconditioner up to rounding
+    ref_u, _, _ = port.cg_solve(t, a, l, nc, 1e-13)
+    for c in range(nc):
+        assert rel_l2(u_t[c], u_r[c]) < 1e-9, c
+        assert rel_l2(u_t[c], ref_u[c]) < 1e-9, c
+
+
+def test_tile_solve_deterministic(port):
+    H, W = 96, 80
+    f0, f1 = rand_pair(H, W, 3)
+    t = port.frames_to_terms(f0, f1, 1.0, 2.5)
+    ntri = 2 * (W - 1) * (H - 1)
+    a, l = np.full(ntri, 300.0), np.full(ntri, 1000.0)
+    u1, it1, _, k1 = solve(t, a, l, 4, 4, 2, 3)
+    u2, it2, _, k2 = solve(t, a, l, 4, 4, 2, 3)
+    assert k1 == k2 == 1 and it1 == it2
+    assert np.array_equal(u1, u2)  # fixed-order reductions: bitwise run to run
