@@ -1326,7 +1326,9 @@ __global__ void __launch_bounds__(256) k_tile_pack(const SubInfo* __restrict__ s
     const double* srow = src + prow_off(32 * I + r) + 32 * J;
     double* drow = dst + tile_off(I, J, kd) + (I == J ? prow_off(r) : 32LL * r);
     const int len = I == J ? ((r + 2) & ~1) : 32;  // the diagonal row with its even pad
-    if (lane < len) drow[lane] = srow[lane];
+    // diagonal tiles carry half their diagonal: the solve's row and column partials of the
+    // tile then take the same products and add up to the full diagonal term (exact)
+    if (lane < len) drow[lane] = (I == J && lane == r) ? 0.5 * srow[lane] : srow[lane];
   }
 }
 
@@ -1531,9 +1533,9 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       if (ob1 >= 0) mbar_arrive_expect(&blk_bar[ob1], blk_tx1);
     }
     if (has_tile) {
-      // my tile from its stage into registers. In the diagonal tile the entries right of the
-      // diagonal are zero and the diagonal is halved: the row and the column partial take the
-      // same FMA loop and add up to the full term.
+      // my tile from its stage into registers. The diagonal tile's entries right of the
+      // diagonal read as zero (pads) and its diagonal is stored halved (k_tile_pack): the row
+      // and the column partial take the same FMA loop and add up to the full term.
       double a[8][4];
       if (!(dbg & 4)) mbar_wait_g(&full[par], (t >> 1) & 1);
       const double* Ts = stage + static_cast<size_t>(par) * stage_doubles + my_off;
@@ -1555,6 +1557,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
           a[k][0] = v0.x, a[k][1] = v0.y, a[k][2] = v1.x, a[k][3] = v1.y;
         }
       } else {  // packed lower rows: row rr at prow_off(rr), rr + 1 entries padded to even
+        // (pads are zero and the diagonal is stored halved, so a loaded pair needs no masking)
         int ro = prow_off32(8 * rg);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -1566,11 +1569,6 @@ __global__ void __launch_bounds__(kTileThreads, 1)
                                  ? *reinterpret_cast<const double2*>(Ts + ro + 16 + 2 * cg)
                                  : make_double2(0.0, 0.0);
           a[k][0] = v0.x, a[k][1] = v0.y, a[k][2] = v1.x, a[k][3] = v1.y;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int cc = 2 * cg + (c & 1) + (c & 2 ? 16 : 0);
-            a[k][c] = cc > rr ? 0.0 : (cc == rr ? 0.5 * a[k][c] : a[k][c]);
-          }
           ro += (rr + 2) & ~1;
         }
       }
