@@ -7,4 +7,4 @@ timeout 300 python bench.py --config c1 > gpurun_out/r1e_bench_c1.json 2> gpurun
 timeout 120 python tools/solve_probe.py c2 > gpurun_out/r1e_probe_c2.log 2>&1 &&
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_line_solve -s 120 -c 2 -o gpurun_out/r1e_solve_c2 python tools/solve_probe.py c2 > gpurun_out/r1e_ncu_solve_c2.log 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_line_factor -c 1 -o gpurun_out/r1e_factor_c2 python tools/profile_case.py c2 0 > gpurun_out/r1e_ncu_factor.log 2>&1
-ls -la gpurun_out/ | grep r1d
+ls -la gpurun_out/ | grep r1e
