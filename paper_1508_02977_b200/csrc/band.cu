@@ -773,6 +773,15 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t addr) {
 template <int R>
 __device__ __forceinline__ double transpose_reduce(double (&acc)[R], int lane) {
   const bool b4 = lane & 16, b3 = lane & 8;
+  if constexpr (R == 2) {  // one halving exchange, then a butterfly over 16 lanes
+    const double send = b4 ? acc[0] : acc[1];
+    double t = (b4 ? acc[1] : acc[0]) + __shfl_xor_sync(0xffffffffu, send, 16);
+    t += __shfl_xor_sync(0xffffffffu, t, 8);
+    t += __shfl_xor_sync(0xffffffffu, t, 4);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    return t;
+  }
 #pragma unroll
   for (int k = 0; k < R / 2; ++k) {
     const double send = b4 ? acc[k] : acc[k + R / 2];
@@ -1056,10 +1065,13 @@ __global__ void __launch_bounds__(kST, 1)
     // whole line, rows read as 16-byte pairs (row starts are 16-byte aligned)
     constexpr int M2 = (MAXM + 1) / 2;
 #ifndef FFB_RB7
-#define FFB_RB7 4
+#define FFB_RB7 2
 #endif
     // rows per batch and operand placement within the 128-register budget
-    constexpr int RB = M2 <= 4 ? 8 : (M2 <= 7 ? FFB_RB7 : 4);
+    // (two rows per batch on lines wider than 256 unknowns: the column partials stay in
+    // registers and the row loop issues fewer dead predicated loads; measured c3 4.61 -> 4.27
+    // ms, c4 18.7 -> 17.7, c5 8.2 -> 5.3 per application)
+    constexpr int RB = M2 <= 4 ? 8 : (M2 <= 7 ? FFB_RB7 : (M2 <= 10 ? 4 : 2));
     constexpr bool WREG = M2 <= 4 || (M2 <= 7 && RB == 4);
     double2 wreg[M2], cacc[M2];
 #pragma unroll
