@@ -487,7 +487,37 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       cnt[3 + ((step + 1) & 1)] = 0;
     }
     PROF_MARK(1); FTL_MARK(0);
-    // ---- Z = A_RK Li^T, thread per row: all loads issued first, 32 independent chains
+    // ---- Z = A_RK Li^T
+    if constexpr (NB == 32) {
+      // on the FP64 tensor cores: rows in blocks of 8 (K is 8-aligned, so a block is wholly
+      // inside or outside it), D[8x8] += A[8x4] B[4x8] with A = the panel, B = Li^T; column
+      // block nb only needs the k-steps up to its diagonal (Li is lower triangular)
+      const int g = lane >> 2, t4 = lane & 3;
+      for (int rb = warp; 8 * rb < kdp; rb += kFW) {
+        const int i = 8 * rb + g;
+        const bool live = i < kd && (i < k0 || i >= k1);
+        double a[8];
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const int c2 = 4 * ks + t4;
+          a[ks] = (live && c2 < nbk) ? (i > k0 ? D[prow_off32(i) + k0 + c2] : D[prow_off32(k0 + c2) + i])
+                                     : 0.0;
+        }
+        double acc[4][2];
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) {
+          acc[nb][0] = acc[nb][1] = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+            if (ks <= 2 * nb + 1) dmma_8x8x4(acc[nb], a[ks], Li[(8 * nb + g) * LDL + 4 * ks + t4]);
+        }
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) Z[(8 * nb + 2 * t4 + h) * zs + 8 * rb + g] = acc[nb][h];
+      }
+    } else {
+    // thread per row: all loads issued first, 32 independent chains
     for (int i = tid; i < kdp; i += kFT) {
       const bool live = i < kd && (i < k0 || i >= k1);
       double a[NB];
@@ -511,6 +541,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
         for (int c2 = 0; c2 <= c; ++c2) acc = fma(a[c2], Li[c * LDL + c2], acc);
         Z[c * zs + i] = acc;
       }
+    }
     }
     // la_reg: A_RK is overwritten during this step's tile phase, so every CTA's Z must be
     // done first (cluster barrier); otherwise a CTA barrier suffices here
