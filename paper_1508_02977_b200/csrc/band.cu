@@ -289,6 +289,44 @@ __device__ __forceinline__ void kk_update(const double* __restrict__ D, int kd, 
   }
 }
 
+// kk_update on the FP64 tensor cores (NB = 32; defined after dmma_8x8x4)
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b);
+__device__ __forceinline__ void kk_update_mma(const double* __restrict__ D, int zs,
+                                              const double* __restrict__ Z, int nbk, int k1,
+                                              int nb1, double* P, int lane, int part) {
+  // row block `part` (rows 8 part .. 8 part + 7 of K'), column blocks 0..part; the A_K'K'
+  // entries are loaded first so their latency hides behind the products
+  const int g = lane >> 2, t = lane & 3;
+  const int u = 8 * part + g;
+  double d0[4][2];
+#pragma unroll
+  for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int v = 8 * nb + 2 * t + h;
+      d0[nb][h] = (nb <= part && v <= u && u < nb1) ? D[prow_off32(k1 + u) + k1 + v] : 0.0;
+    }
+  double acc[4][2];
+#pragma unroll
+  for (int nb = 0; nb < 4; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    if (4 * ks >= nbk) break;
+    const double* zc = Z + (4 * ks + t) * zs + k1;  // A[m][k] = Z[k][k1+m], B[k][n] = Z[k][k1+n]
+    const double a = zc[8 * part + g];
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb)
+      if (nb <= part) dmma_8x8x4(acc[nb], a, zc[8 * nb + g]);
+  }
+#pragma unroll
+  for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int v = 8 * nb + 2 * t + h;
+      if (nb <= part && v <= u && u < nb1) P[u * 33 + v] = d0[nb][h] - acc[nb][h];
+    }
+}
+
 // A_RK <- Z L^-1 on rows r0..r0+31 (rows of K skipped): out[u][c] = sum_c2 Z[c2][u] Li[c2][c],
 // written to D[u][k0 + c] (u > k0) or its transpose D[k0 + c][u] (u < k0). Lane: 4 rows x 4
 // columns per pass, NB/16 passes (register budget of the factor kernel).
@@ -493,16 +531,24 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       // inside or outside it), D[8x8] += A[8x4] B[4x8] with A = the panel, B = Li^T; column
       // block nb only needs the k-steps up to its diagonal (Li is lower triangular)
       const int g = lane >> 2, t4 = lane & 3;
-      for (int rb = warp; 8 * rb < kdp; rb += kFW) {
+      // the next row block's panel loads are issued before this block's products
+      double an[8];
+      auto load_panel = [&](int rb) {
         const int i = 8 * rb + g;
-        const bool live = i < kd && (i < k0 || i >= k1);
-        double a[8];
+        const bool live = 8 * rb < kdp && i < kd && (i < k0 || i >= k1);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
           const int c2 = 4 * ks + t4;
-          a[ks] = (live && c2 < nbk) ? (i > k0 ? D[prow_off32(i) + k0 + c2] : D[prow_off32(k0 + c2) + i])
-                                     : 0.0;
+          an[ks] = (live && c2 < nbk) ? (i > k0 ? D[prow_off32(i) + k0 + c2] : D[prow_off32(k0 + c2) + i])
+                                      : 0.0;
         }
+      };
+      load_panel(warp);
+      for (int rb = warp; 8 * rb < kdp; rb += kFW) {
+        double a[8];
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) a[ks] = an[ks];
+        load_panel(rb + kFW);
         double acc[4][2];
 #pragma unroll
         for (int nb = 0; nb < 4; ++nb) {
@@ -557,7 +603,10 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       // pivot (A_KK is overwritten at its own step). Every CTA of the cluster updates a
       // private copy in P (warps 0-3) and factors it (warp 0); nobody writes the tile back,
       // so there is no ordering against the other CTAs' updates.
-      kk_update<NB>(D, kd, zs, Z, nbk, k1, min(NB, kd - k1), P, lane, warp);
+      if constexpr (NB == 32)
+        kk_update_mma(D, zs, Z, nbk, k1, min(NB, kd - k1), P, lane, warp);
+      else
+        kk_update<NB>(D, kd, zs, Z, nbk, k1, min(NB, kd - k1), P, lane, warp);
       asm volatile("bar.sync 2, 128;" ::: "memory");
       PROF_MARK(6); FTL_MARK(2);
       if (warp < 2)
