@@ -454,6 +454,9 @@ __device__ __forceinline__ void rupd_tile_mma(double* __restrict__ D, int kd, in
       for (int j = 0; j < 4; ++j)
         if (!diag || j <= i) dmma_8x8x4(acc[i][j], a[i], b[j]);
   }
+  // read-modify-write in 16-byte pairs (v even; K is 32-aligned, so a pair is wholly inside
+  // or outside it). The pair at v = u of an even row u also rewrites the row's pad, which
+  // nothing reads during the sweep and pack_line zeroes at its end.
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int u = u0 + 8 * i + g;
@@ -462,10 +465,13 @@ __device__ __forceinline__ void rupd_tile_mma(double* __restrict__ D, int kd, in
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (diag && j > i) continue;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int v = v0 + 8 * j + 2 * t + h;
-        if (v <= u && (v < k0 || v >= k1)) rowp[v] -= acc[i][j][h];
+      const int v = v0 + 8 * j + 2 * t;
+      if (v <= u && (v < k0 || v >= k1)) {
+        double2* pp = reinterpret_cast<double2*>(rowp + v);
+        double2 x = *pp;
+        x.x -= acc[i][j][0];
+        x.y -= acc[i][j][1];
+        *pp = x;
       }
     }
   }
