@@ -235,15 +235,22 @@ __device__ __forceinline__ void rupd_tile(double* __restrict__ D, int kd, int kd
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
   }
+  // read-modify-write in 16-byte pairs (see rupd_tile_mma)
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int u = ub0 + 16 * (i >> 1) + (i & 1);
     if (u >= kd || (u >= k0 && u < k1)) continue;
     double* rowp = D + prow_off32(u);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int v = vb0 + 8 * (j >> 1) + (j & 1);
-      if (v <= u && (v < k0 || v >= k1)) rowp[v] -= acc[i][j];
+    for (int m = 0; m < 4; ++m) {
+      const int v = vb0 + 8 * m;
+      if (v <= u && (v < k0 || v >= k1)) {
+        double2* pp = reinterpret_cast<double2*>(rowp + v);
+        double2 x = *pp;
+        x.x -= acc[i][2 * m];
+        x.y -= acc[i][2 * m + 1];
+        *pp = x;
+      }
     }
   }
 }
@@ -360,18 +367,32 @@ __device__ __forceinline__ void tile_ark(double* __restrict__ D, int kd, int kdp
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
     }
+    // 16-byte stores: column pairs (c, c + 1) of a row below K, row pairs (u, u + 1) of the
+    // transposed block above K (u even, k0 even)
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int u = r0 + 2 * ui + 16 * (i >> 1) + (i & 1);
-      if (u >= kd || (u >= k0 && u < k1)) continue;
+      if (u >= kd || (u >= k0 && u < k1) || u < k0) continue;
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int c = cb + 8 * m;
+        if (c + 1 < nbk)
+          *reinterpret_cast<double2*>(D + prow_off32(u) + k0 + c) =
+              make_double2(acc[i][2 * m], acc[i][2 * m + 1]);
+        else if (c < nbk)
+          D[prow_off32(u) + k0 + c] = acc[i][2 * m];
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {  // rows u = r0 + 2 ui + 16 m and u + 1 above K
+      const int u = r0 + 2 * ui + 16 * m;
+      if (u >= k0) continue;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int c = cb + 8 * (j >> 1) + (j & 1);
         if (c >= nbk) continue;
-        if (u > k0)
-          D[prow_off32(u) + k0 + c] = acc[i][j];
-        else
-          D[prow_off32(k0 + c) + u] = acc[i][j];
+        *reinterpret_cast<double2*>(D + prow_off32(k0 + c) + u) =
+            make_double2(acc[2 * m][j], acc[2 * m + 1][j]);
       }
     }
   }
