@@ -1932,13 +1932,13 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
   }
   // the look-ahead through D is a single-CTA schedule; the NB = 32 one works in clusters
   int lac = (C > 1 && nb != 32) ? 0 : la;
-  // DMMA tile updates for NB = 32 (measured c2 -9%, c3 -13% of the factorisation time);
-  // the NB = 16 sweep (c5) is faster with the FFMA register tiles. FFB_FACTOR_MMA=0/1 forces.
+  // DMMA tile updates (measured c2 -9%, c3 -13% of the factorisation time; NB = 16, c5: -14%
+  // once the tiles' read-modify-writes went to 16-byte pairs). FFB_FACTOR_MMA=0 forces FFMA.
   static const int mma = [] {
     const char* e = std::getenv("FFB_FACTOR_MMA");
     return e ? std::atoi(e) : -1;
   }();
-  if (mma == 1 || (mma < 0 && nb == 32)) lac |= 2;
+  if (mma != 0) lac |= 2;
   // subdomains per launch (FFB_FGROUP): the lines being inverted stay L2-resident only while
   // the chains in flight are few enough (every sweep step rewrites each line once)
   int G = nsub;
