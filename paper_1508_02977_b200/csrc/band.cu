@@ -1981,16 +1981,27 @@ static void build_tile_tables(unsigned char (*tile_of)[kTileMaxNt + 1][8][kTileW
       const int total = 1024 * (T - nt) + 544 * nt;
       const int cap = (total + C - 1) / C + 1024;  // bytes/8 per CTA, one tile of slack
       int cnt[8] = {0}, load[8] = {0};
+      // leave each CTA one warp per block it reduces; when the warps run out, the CTA of the
+      // last block (short when kd is just past a multiple of 32) takes the extra tile and
+      // its owner warp reduces that block too
+      int wcap[8];
+      const int c_last = (nt - 1) % C;
+      for (int c = 0; c < C; ++c)
+        wcap[c] = kTileWarps - (nt - c + C - 1) / C + (c == c_last && nt > C ? 1 : 0);
       int tau = 0;
       for (int I = 0; I < nt; ++I)
         for (int J = 0; J <= I; ++J, ++tau) {
           const int wgt = I == J ? 544 : 1024;
           const int a = I % C, b = J % C;
-          auto fits = [&](int c) { return cnt[c] < kTileWarps && load[c] + wgt <= cap; };
+          auto fits = [&](int c) { return cnt[c] < wcap[c] && load[c] + wgt <= cap; };
           int c = load[a] <= load[b] ? a : b;
           if (!fits(c)) c = c == a ? b : a;
-          if (!fits(c)) {  // both owners full: the least loaded CTA with a free warp
+          if (!fits(c)) {  // both owners full: the least loaded CTA with a free slot
             c = -1;
+            for (int q = 0; q < C; ++q)
+              if (cnt[q] < wcap[q] && (c < 0 || load[q] < load[c])) c = q;
+          }
+          if (c < 0) {  // every CTA at its reserve: any warp left
             for (int q = 0; q < C; ++q)
               if (cnt[q] < kTileWarps && (c < 0 || load[q] < load[c])) c = q;
           }
@@ -2000,13 +2011,24 @@ static void build_tile_tables(unsigned char (*tile_of)[kTileMaxNt + 1][8][kTileW
           if (c == b) ++nloc[ci][nt][J];  // column partial stays local
         }
       for (int c = 0; c < C; ++c) {
-        stage[ci][nt] = std::max(stage[ci][nt], load[c]);
+        if (stage[ci][nt] >= 0) stage[ci][nt] = std::max(stage[ci][nt], load[c]);
         const int n_own = (nt - c + C - 1) / C, nfree = kTileWarps - cnt[c];
         const bool dedicated = nfree > 0 && (n_own + nfree - 1) / nfree <= kTileMaxOwn;
+        for (int q = 0; q < n_own; ++q) {
+          int w = dedicated ? kTileWarps - 1 - q % nfree : q;
+          // exactly one warp short in the CTA of the last block: that (short) block shares
+          // the first owner's warp, every other block has its own
+          if (dedicated && c == c_last && nfree == n_own - 1)
+            w = q == n_own - 1 ? kTileWarps - 1 : kTileWarps - 1 - q;
+          owner[ci][nt][q * C + c] = static_cast<unsigned char>(w);
+        }
+        // the kernel reduces at most kTileMaxOwn blocks per warp: a table that asks for more
+        // is not used (stage 0 -> solve_plan keeps the ring kernel)
+        int per_warp[kTileWarps] = {0};
         for (int q = 0; q < n_own; ++q)
-          owner[ci][nt][q * C + c] =
-              static_cast<unsigned char>(dedicated ? kTileWarps - 1 - q % nfree : q);
+          if (++per_warp[owner[ci][nt][q * C + c]] > kTileMaxOwn) stage[ci][nt] = -1;
       }
+      if (stage[ci][nt] < 0) stage[ci][nt] = 0;
     }
   }
 }
@@ -2105,7 +2127,9 @@ SolvePlan solve_plan(int kd_max, int C) {
     const int nown = (nt + C - 1) / C;
     const size_t smem = 256 + (2 * static_cast<size_t>(pl.stage_doubles) + 4 * static_cast<size_t>(nt) * 32 +
                                static_cast<size_t>(nown) * (nt + 1) * 32) * sizeof(double);
-    if (smem <= 227 * 1024) pl.tile = 1, pl.smem = smem;
+    bool tables_ok = true;  // every tile count a subdomain of this plan can have
+    for (int n = 1; n <= nt; ++n) tables_ok = tables_ok && h_stage[ci][n] > 0;
+    if (tables_ok && smem <= 227 * 1024) pl.tile = 1, pl.smem = smem;
   }
   return pl;
 }
