@@ -755,15 +755,49 @@ __device__ void build_line(const SubInfo& s, const double* __restrict__ coef, si
   __syncthreads();
 }
 
+// ---- tile-major line layout (the register-tiled solve streams whole tiles) ----------------
+// A line's lower triangle as 32x32 tiles (I, J), I >= J, row-major; tile row I has
+// h = min(32, kd - 32 I) rows. An off-diagonal tile stores its h rows of 32 entries, a
+// diagonal tile its packed lower triangle (local row r: r + 1 entries padded to even, at
+// prow_off(r)). Same number of doubles as the packed row layout (tile_line_size == prow_off).
+__host__ __device__ __forceinline__ int tile_h(int I, int kd) { return min(32, kd - 32 * I); }
+__host__ __device__ __forceinline__ long long tile_row_off(int I, int kd) {
+  // tile rows before I are full (h = 32): I off-diagonal tiles of 1024 + one diagonal of 544
+  (void)kd;
+  return 1024LL * I * (I - 1) / 2 + 544LL * I;
+}
+__host__ __device__ __forceinline__ long long tile_off(int I, int J, int kd) {
+  return tile_row_off(I, kd) + 32LL * tile_h(I, kd) * J;
+}
+__host__ __device__ __forceinline__ int tile_size(int I, int J, int kd) {
+  const int h = tile_h(I, kd);
+  return I == J ? static_cast<int>(prow_off(h)) : 32 * h;
+}
+
 // the sweep leaves -D^-1 in place in the packed line: negate it, zero the pads of even rows
-__device__ void pack_line(const SubInfo& s, int l, double* F, int q, int C) {
+// (Ft: the tile-major copy the register-tiled solve streams, written in the same pass with the
+// diagonal halved — see k_line_solve_tile; nullptr when that solve is not used)
+__device__ __noinline__ void pack_line(const SubInfo& s, int l, double* F, int q, int C, double* Ft) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kd = s.kd;
   double* Fl = F + static_cast<long long>(l) * s.line_sz;
+  double* Tl = Ft ? Ft + s.fac_off + static_cast<long long>(l) * s.line_sz : nullptr;
   for (int i = warp + kFW * q; i < kd; i += kFW * C) {
     const int o = prow_off32(i);
-    for (int j = lane; j <= i; j += 32) Fl[o + j] = -Fl[o + j];
-    if ((i & 1) == 0 && lane == 0) Fl[o + i + 1] = 0.0;
+    const int I = i >> 5, r = i & 31;
+    for (int j = lane; j <= i; j += 32) {
+      const double v = -Fl[o + j];
+      Fl[o + j] = v;
+      if (Tl) {
+        const int J = j >> 5;
+        const long long d = tile_off(I, J, kd) + (I == J ? prow_off32(r) + (j & 31) : 32 * r + (j & 31));
+        Tl[d] = j == i ? 0.5 * v : v;
+      }
+    }
+    if ((i & 1) == 0 && lane == 0) {
+      Fl[o + i + 1] = 0.0;
+      if (Tl) Tl[tile_off(I, I, kd) + prow_off32(r) + r + 1] = 0.0;
+    }
   }
   __syncthreads();
 }
@@ -776,7 +810,8 @@ __device__ void pack_line(const SubInfo& s, int l, double* F, int q, int C) {
 template <int NB>
 __global__ void __launch_bounds__(kFT, 1)
     k_line_factor(const SubInfo* __restrict__ subs, const double* __restrict__ coef, size_t N,
-                  int W, int nc, double* __restrict__ fac, double* __restrict__ scratch,
+                  int W, int nc, double* __restrict__ fac, double* __restrict__ fac_t,
+                  double* __restrict__ scratch,
                   long long scratch_stride, int kdp, int mid, int* __restrict__ bad,
                   const int2* __restrict__ changed, int la) {
   const int C = static_cast<int>(cl_size()), q = static_cast<int>(cl_rank());
@@ -809,7 +844,7 @@ __global__ void __launch_bounds__(kFT, 1)
     if (C > 1) cl_sync();
     PROF_MARK(0);
     sweep_invert<NB>(D, kd, kdp, P, Li, ir, cnt, Z, first_bad, m * kd, la, q, C);
-    pack_line(s, m, F, q, C);
+    pack_line(s, m, F, q, C, fac_t);
   } else {
     const int nlines = chain == 0 ? m : L - 1 - m;
     const int t0 = chain == 0 ? chg.x : L - 1 - chg.y;
@@ -822,7 +857,7 @@ __global__ void __launch_bounds__(kFT, 1)
       if (C > 1) cl_sync();
       PROF_MARK(0);
       sweep_invert<NB>(D, kd, kdp, P, Li, ir, cnt, Z, first_bad, l * kd, la, q, C);
-      pack_line(s, l, F, q, C);
+      pack_line(s, l, F, q, C, fac_t);
       PROF_MARK(5);
     }
   }
@@ -1403,25 +1438,6 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) 
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// ---- tile-major line layout (the register-tiled solve streams whole tiles) ----------------
-// A line's lower triangle as 32x32 tiles (I, J), I >= J, row-major; tile row I has
-// h = min(32, kd - 32 I) rows. An off-diagonal tile stores its h rows of 32 entries, a
-// diagonal tile its packed lower triangle (local row r: r + 1 entries padded to even, at
-// prow_off(r)). Same number of doubles as the packed row layout (tile_line_size == prow_off).
-__host__ __device__ __forceinline__ int tile_h(int I, int kd) { return min(32, kd - 32 * I); }
-__host__ __device__ __forceinline__ long long tile_row_off(int I, int kd) {
-  // tile rows before I are full (h = 32): I off-diagonal tiles of 1024 + one diagonal of 544
-  (void)kd;
-  return 1024LL * I * (I - 1) / 2 + 544LL * I;
-}
-__host__ __device__ __forceinline__ long long tile_off(int I, int J, int kd) {
-  return tile_row_off(I, kd) + 32LL * tile_h(I, kd) * J;
-}
-__host__ __device__ __forceinline__ int tile_size(int I, int J, int kd) {
-  const int h = tile_h(I, kd);
-  return I == J ? static_cast<int>(prow_off(h)) : 32 * h;
-}
-
 // packed rows -> tile-major, one CTA per (line, subdomain), one warp per tile row segment
 __global__ void __launch_bounds__(256) k_tile_pack(const SubInfo* __restrict__ subs,
                                                    const double* __restrict__ fac,
@@ -1913,7 +1929,8 @@ void changed_lines(const SubInfo* d_subs, int nsub, const double* alpha, const d
 
 void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
                  const double* coef, size_t N, int W, int nc, double* fac, double* scratch,
-                 long long scratch_stride, int* d_bad, cudaStream_t st, const int2* changed) {
+                 long long scratch_stride, int* d_bad, cudaStream_t st, const int2* changed,
+                 double* fac_t) {
   const int kdp = (kd_max + 31) / 32 * 32;
   static const int la = [] {
     const char* e = std::getenv("FFB_LOOKAHEAD");
@@ -1950,10 +1967,10 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
       const int grid = (mid ? ng : 2 * ng) * C;
       if (nb == 32) {
         launch_cluster(k_line_factor<32>, grid, kFT, smem, C, st, d_subs + g0, coef, N, W, nc,
-                       fac, scratch, scratch_stride, kdp, mid, d_bad + g0, chg, lac);
+                       fac, fac_t, scratch, scratch_stride, kdp, mid, d_bad + g0, chg, lac);
       } else if (nb == 16) {
         launch_cluster(k_line_factor<16>, grid, kFT, smem, C, st, d_subs + g0, coef, N, W, nc,
-                       fac, scratch, scratch_stride, kdp, mid, d_bad + g0, chg, lac);
+                       fac, fac_t, scratch, scratch_stride, kdp, mid, d_bad + g0, chg, lac);
       } else {
         fail("internal: unsupported pivot block size");
       }

@@ -353,8 +353,7 @@ void ensure_factor(ffb_ctx* c, int nc) {
   }
   line_factor(c->d_subs.p + c->s_lo, np, c->ccl, c->nbf, c->kd_max, c->coef.p, c->N, c->W, nc,
               c->fac.p, c->dscratch.p, static_cast<long long>(c->kd_max) * c->kd_max, c->d_bad.p,
-              c->st, changed);
-  if (c->plan.tile) tile_pack(c->d_subs.p + c->s_lo, np, c->L_max, c->fac.p, c->fac_t.p, c->st);
+              c->st, changed, c->plan.tile ? c->fac_t.p : nullptr);
   FFB_CUDA(cudaMemcpyAsync(c->alpha_fact.ensure(c->ntri), c->alpha.p, c->ntri * sizeof(double),
                            cudaMemcpyDeviceToDevice, c->st));
   std::vector<int> bad(np);

@@ -86,7 +86,8 @@ long long packed_line_size(int kd);
 size_t factor_scratch_doubles(int nsub, int kd_max);
 void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max, const double* coef,
                  size_t N, int W, int nc, double* fac, double* scratch, long long scratch_stride,
-                 int* d_bad, cudaStream_t st, const int2* changed = nullptr);
+                 int* d_bad, cudaStream_t st, const int2* changed = nullptr,
+                 double* fac_t = nullptr);
 void changed_lines(const SubInfo* d_subs, int nsub, const double* alpha, const double* alpha_fact,
                    int W, int H, int2* changed, cudaStream_t st);
 struct SolvePlan {
