@@ -1438,35 +1438,6 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) 
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// packed rows -> tile-major, one CTA per (line, subdomain), one warp per tile row segment
-__global__ void __launch_bounds__(256) k_tile_pack(const SubInfo* __restrict__ subs,
-                                                   const double* __restrict__ fac,
-                                                   double* __restrict__ fac_t) {
-  const SubInfo s = subs[blockIdx.y];
-  const int l = blockIdx.x;
-  if (l >= s.L) return;
-  const int kd = s.kd, nt = (kd + 31) >> 5;
-  const double* src = fac + s.fac_off + static_cast<long long>(l) * s.line_sz;
-  double* dst = fac_t + s.fac_off + static_cast<long long>(l) * s.line_sz;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int T = nt * (nt + 1) / 2;
-  for (int q = warp; q < T * 32; q += 8) {  // (tile, local row)
-    const int tau = q >> 5, r = q & 31;
-    int I = static_cast<int>((sqrt(8.0 * tau + 1.0) - 1.0) * 0.5);
-    while (I * (I + 1) / 2 > tau) --I;
-    while ((I + 1) * (I + 2) / 2 <= tau) ++I;
-    const int J = tau - I * (I + 1) / 2;
-    const int h = tile_h(I, kd);
-    if (r >= h) continue;
-    const double* srow = src + prow_off(32 * I + r) + 32 * J;
-    double* drow = dst + tile_off(I, J, kd) + (I == J ? prow_off(r) : 32LL * r);
-    const int len = I == J ? ((r + 2) & ~1) : 32;  // the diagonal row with its even pad
-    // diagonal tiles carry half their diagonal: the solve's row and column partials of the
-    // tile then take the same products and add up to the full diagonal term (exact)
-    if (lane < len) drow[lane] = (I == J && lane == r) ? 0.5 * srow[lane] : srow[lane];
-  }
-}
-
 // ---- K6, register-tiled ---------------------------------------------------------------------
 // Placement tables (built on the host by set_tile_tables) for cluster-size index ci (C = 1,
 // 2, 4, 8) and nt tile rows:
@@ -1669,7 +1640,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     }
     if (has_tile) {
       // my tile from its stage into registers. The diagonal tile's entries right of the
-      // diagonal read as zero (pads) and its diagonal is stored halved (k_tile_pack): the row
+      // diagonal read as zero (pads) and its diagonal is stored halved (pack_line): the row
       // and the column partial take the same FMA loop and add up to the full term.
       double a[8][4];
       if (!(dbg & 4)) mbar_wait_g(&full[par], (t >> 1) & 1);
@@ -2067,12 +2038,6 @@ static void set_tile_tables() {
   FFB_CUDA(cudaMemcpyToSymbol(c_nloc, h_nloc, sizeof(h_nloc)));
   FFB_CUDA(cudaMemcpyToSymbol(c_owner, h_owner, sizeof(h_owner)));
   if (dev < 32) done_mask |= 1u << dev;
-}
-
-void tile_pack(const SubInfo* d_subs, int nsub, int L_max, const double* fac, double* fac_t,
-               cudaStream_t st) {
-  k_tile_pack<<<dim3(L_max, nsub), 256, 0, st>>>(d_subs, fac, fac_t);
-  FFB_LAUNCHED();
 }
 
 void set_solve_dbg(int v) { FFB_CUDA(cudaMemcpyToSymbol(g_solve_dbg, &v, sizeof(int))); }

@@ -112,7 +112,6 @@ struct ffb_ctx {
   DBuf<SubInfo> d_subs;
   DBuf<AxisMap> d_col, d_row;
   DBuf<double> fac, fac_t, dscratch, ylocal, zlocal, rlocal, xlocal, G0, G1, incs;
-  int L_max = 0;  // lines of the longest subdomain
   DBuf<int> own_col, own_row;
   // linsolve boundary on an explicit CSR system (ffb_csr_*)
   DBuf<int> csr_rp, csr_ci, csr_perm, csr_iperm, csr_bad;
@@ -322,8 +321,6 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
                            c->st));
   c->fac.ensure(fac_off);
   if (c->plan.tile) c->fac_t.ensure(fac_off);  // tile-major copy for the register-tiled solve
-  c->L_max = 0;
-  for (int p = c->s_lo; p < c->s_hi; ++p) c->L_max = std::max(c->L_max, c->subs[p].L);
   c->dscratch.ensure(factor_scratch_doubles(c->s_hi - c->s_lo, kd_max));
   c->ylocal.ensure(vec_off);
   c->zlocal.ensure(vec_off);

@@ -95,9 +95,6 @@ struct SolvePlan {
   size_t smem;
 };
 SolvePlan solve_plan(int kd_max, int C);
-// packed line inverses -> the tile-major copy the register-tiled solve streams (plan.tile)
-void tile_pack(const SubInfo* d_subs, int nsub, int L_max, const double* fac, double* fac_t,
-               cudaStream_t st);
 void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,
                 const double* coef, size_t N, const double* r, double* ylocal, double* zlocal,
                 int W, int nc, const int* flags, cudaStream_t st,
