@@ -615,6 +615,18 @@ int ffb_debug_solve_kernel(ffb_ctx* c) {
   return c->plan.tile ? 1 : 0;
 }
 
+// development probe (host only, no device needed): the subdomain-solve plan for a widest
+// line of kd_max unknowns on C-CTA clusters — tile (1: register-tiled, 0: ring), its dynamic
+// shared memory and, for the tiled kernel, the per-CTA line stage in doubles
+int ffb_debug_solve_plan(int kd_max, int C, int* tile, long long* smem, int* stage) {
+  return guard([&] {
+    const SolvePlan pl = solve_plan(kd_max, C);
+    if (tile) *tile = pl.tile;
+    if (smem) *smem = static_cast<long long>(pl.smem);
+    if (stage) *stage = pl.tile ? pl.stage_doubles : 0;
+  });
+}
+
 // development probe: average time of `n` applications of the Schwarz preconditioner with
 // the context's resident factorisation (after a solve), on the current residual vector
 int ffb_debug_time_asm(ffb_ctx* c, int nc, int n, int dbg, double* ms) {
