@@ -23,6 +23,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", CSR
           "-I", os.path.join(ROOT, "include")]
 if os.environ.get("FFB_PROFILE"):
     COMMON.append("-DFFB_PROFILE")
+COMMON += os.environ.get("FFB_NVCC_FLAGS", "").split()  # development experiments (-D...)
 CU = {
     "imaging.cu": ["--fmad=false"],
     "operator.cu": ["--fmad=false"],

@@ -477,24 +477,38 @@ __device__ __forceinline__ void rupd_tile_mma(double* __restrict__ D, int kd, in
   }
   // read-modify-write in 16-byte pairs (v even; K is 32-aligned, so a pair is wholly inside
   // or outside it). The pair at v = u of an even row u also rewrites the row's pad, which
-  // nothing reads during the sweep and pack_line zeroes at its end.
+  // nothing reads during the sweep and pack_line zeroes at its end. The loads of RG row blocks
+  // are all issued before their stores: written load-store per pair, the compiler keeps the
+  // order (the stores may alias the next loads) and the tile pays one L2 round trip per pair.
+#ifndef FFB_RG
+#define FFB_RG 2
+#endif
+  constexpr int RG = FFB_RG;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int u = u0 + 8 * i + g;
-    if (u >= kd || (u >= k0 && u < k1)) continue;
-    double* rowp = D + prow_off32(u);
+  for (int i0 = 0; i0 < 4; i0 += RG) {
+    double2 x[RG][4];
+    double2* pp[RG][4];
+    bool on[RG][4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (diag && j > i) continue;
-      const int v = v0 + 8 * j + 2 * t;
-      if (v <= u && (v < k0 || v >= k1)) {
-        double2* pp = reinterpret_cast<double2*>(rowp + v);
-        double2 x = *pp;
-        x.x -= acc[i][j][0];
-        x.y -= acc[i][j][1];
-        *pp = x;
+    for (int ii = 0; ii < RG; ++ii) {
+      const int i = i0 + ii;
+      const int u = u0 + 8 * i + g;
+      const bool row_on = u < kd && !(u >= k0 && u < k1);
+      double* rowp = D + prow_off32(u);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int v = v0 + 8 * j + 2 * t;
+        on[ii][j] = row_on && !(diag && j > i) && v <= u && (v < k0 || v >= k1);
+        pp[ii][j] = reinterpret_cast<double2*>(rowp + v);
+        x[ii][j] = on[ii][j] ? *pp[ii][j] : make_double2(0.0, 0.0);
       }
     }
+#pragma unroll
+    for (int ii = 0; ii < RG; ++ii)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (on[ii][j])
+          *pp[ii][j] = make_double2(x[ii][j].x - acc[i0 + ii][j][0], x[ii][j].y - acc[i0 + ii][j][1]);
   }
 }
 
@@ -536,7 +550,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
     pivot_warp<NB>(P, NB + 1, 0, min(NB, kd), P, Li2, ir, first_bad, bad_base, nullptr);
   }
   const bool la_reg = NB == 32 && la;  // look-ahead on a private copy of the next pivot block
-  int pv_tag = 0;                      // pivot_pair progress tags (same on every warp)
+  int pv_tag = 0;                      // pivot_pair progress tags (warps 0-3)
   if (tid == 0) cnt[2] = 0;
   const int nt = (kd + 31) / 32;
   const int ntiles = nt * (nt + 1) / 2;
@@ -570,12 +584,23 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
                                       : 0.0;
         }
       };
-      load_panel(warp);
-      for (int rb = warp; 8 * rb < kdp; rb += kFW) {
+      // la_reg on a cluster: the row blocks are split between groups of FFB_ZSPLIT CTAs, and
+      // each block is stored into the Z of every CTA of its group (distributed shared memory;
+      // the cluster barrier after the Z phase orders it, the previous step's final one frees
+      // the buffers). The panel loads are the cost (one L2 round trip per row block); 2-way
+      // beats 4-way, where the remote stores (~20 B/clk per SM) take what the loads saved.
+#ifndef FFB_ZSPLIT
+#define FFB_ZSPLIT 2
+#endif
+      const int zs_n = la_reg ? min(C, FFB_ZSPLIT) : 1;  // CTAs sharing the Z row blocks
+      const int zs_base = q - q % zs_n;
+      const int rb0 = (q % zs_n) * kFW + warp, rstep = kFW * zs_n;
+      load_panel(rb0);
+      for (int rb = rb0; 8 * rb < kdp; rb += rstep) {
         double a[8];
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) a[ks] = an[ks];
-        load_panel(rb + kFW);
+        load_panel(rb + rstep);
         double acc[4][2];
 #pragma unroll
         for (int nb = 0; nb < 4; ++nb) {
@@ -588,7 +613,17 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
         for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
           for (int h = 0; h < 2; ++h) Z[(8 * nb + 2 * t4 + h) * zs + 8 * rb + g] = acc[nb][h];
+#pragma unroll 1
+        for (int r = 1; r < zs_n; ++r) {
+          double* Zr = cl_map(Z, static_cast<unsigned>(zs_base + (q % zs_n + r) % zs_n));
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) Zr[(8 * nb + 2 * t4 + h) * zs + 8 * rb + g] = acc[nb][h];
+        }
+        if (warp >= 4 && rb == rb0) FTL_MARK(3);  // first row block stored
       }
+      if (warp >= 4) FTL_MARK(2);  // Z loop done (before the barrier)
     } else {
     // thread per row: all loads issued first, 32 independent chains
     for (int i = tid; i < kdp; i += kFT) {

@@ -104,6 +104,22 @@ __device__ __forceinline__ void st_release_shared(int* p, int v) {
                : "memory");
 }
 
+// The elimination steps in kPivStages stages of NB / kPivStages steps: step k touches the
+// rotated entries t < NB - k only, so stage s runs with width NB - s NB / kPivStages (FP64
+// instructions are what the pivot warps compete for with the tile warps' DMMA).
+#ifndef FFB_PIVS
+#define FFB_PIVS 8
+#endif
+constexpr int kPivStages = FFB_PIVS;
+template <int NB, int S = 0, class F>
+__device__ __forceinline__ void pivot_stages(F& step) {
+  constexpr int n = NB / kPivStages, W = NB - S * n;
+  static_assert(NB % kPivStages == 0 && W % 2 == 0, "pivot stage widths");
+#pragma unroll 1
+  for (int k = S * n; k < (S + 1) * n; ++k) step(k, std::integral_constant<int, W>());
+  if constexpr (S + 1 < kPivStages) pivot_stages<NB, S + 1>(step);
+}
+
 template <int NB>
 __device__ __noinline__ void pivot_pair(const double* src, long long ld, int k0, int nbk,
                                         double* LR, double* Li, double* ir, int& first_bad,
@@ -127,8 +143,7 @@ __device__ __noinline__ void pivot_pair(const double* src, long long ld, int k0,
       dkk = 1.0;
     }
     double r = rsqrt(dkk);
-    // step k touches rotated entries t < NB - k only (rows k + t < NB): the second half of
-    // the steps updates half the registers
+    // step k touches rotated entries t < NB - k only (rows k + t < NB): see pivot_stages
     auto step = [&](int k, auto width) {
       constexpr int WD = decltype(width)::value;
       const double l = (lane == k) ? dkk * r : c[0] * r;
@@ -154,10 +169,7 @@ __device__ __noinline__ void pivot_pair(const double* src, long long ld, int k0,
       dkk = dn;
       r = rn;
     };
-#pragma unroll 1
-    for (int k = 0; k < NB / 2; ++k) step(k, std::integral_constant<int, NB>());
-#pragma unroll 1
-    for (int k = NB / 2; k < NB; ++k) step(k, std::integral_constant<int, NB / 2>());
+    pivot_stages<NB>(step);
     first_bad = fb;
   } else {  // forward substitution for L^-1, one column of L behind
 #pragma unroll
@@ -182,10 +194,7 @@ __device__ __noinline__ void pivot_pair(const double* src, long long ld, int k0,
       }
       c[WD - 1] = 0.0;
     };
-#pragma unroll 1
-    for (int k = 0; k < NB / 2; ++k) step(k, std::integral_constant<int, NB>());
-#pragma unroll 1
-    for (int k = NB / 2; k < NB; ++k) step(k, std::integral_constant<int, NB / 2>());
+    pivot_stages<NB>(step);
   }
   __syncwarp();
 }

@@ -16,6 +16,7 @@ r = ff.run_on_frames(f0, f1, rc, ctx)
 buf = (C.c_ulonglong * (16 * 16 * 8))()
 lib.ffb_debug_prof(buf, 3)
 a = np.frombuffer(buf, dtype=np.uint64).reshape(16, 16, 8).astype(np.int64)
+# warps >= 4: "kk" = Z loop done before the barrier, "pivot" = first Z row block stored
 names = ["start", "Zdone", "kk", "pivot", "tiles", "end"]
 print(f"{name}: factor {r.stats.ms_factor:.1f} ms")
 for st in range(2, 5):
