@@ -537,9 +537,11 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
                              int la, int q, int C) {
   const bool use_mma = la & 2;  // tile updates on the FP64 tensor cores
   la &= 1;
-  // Z row stride: kdp + 8 doubles puts the 4 pivot-column rows a DMMA fragment load touches
-  // on alternating 64-byte bank halves (2 wavefronts per load instead of 4)
-  const int zs = kdp + 8;
+  // Z row stride: kdp + 4 doubles. A 64-bit shared load is served per half-warp (16 lanes,
+  // 128 B); a DMMA fragment load's half-warp touches 4 pivot-column rows x 32 B, which this
+  // stride puts on 4 distinct 32-byte bank groups (one wavefront; kdp + 8 took two — ncu
+  // r1f_factor_c2: 2x the ideal wavefronts), and the Z stores' rows 2 apart on two (was four).
+  const int zs = kdp + 4;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int LDL = li_stride<NB>();
   constexpr int LS = NB * LDL;
@@ -718,7 +720,9 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       idx = __shfl_sync(~0u, idx, 0);
       if (idx >= ntiles) break;
       if (idx == special) continue;
-      int TU = static_cast<int>((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
+      // tile row from the triangular index: single-precision estimate, exact integer fix-up
+      // (a double sqrt here stalled the queue loop: 5% of the kernel's warp stall samples)
+      int TU = static_cast<int>((sqrtf(8.0f * static_cast<float>(idx) + 1.0f) - 1.0f) * 0.5f);
       while (TU * (TU + 1) / 2 > idx) --TU;
       while ((TU + 1) * (TU + 2) / 2 <= idx) ++TU;
       if (use_mma)
