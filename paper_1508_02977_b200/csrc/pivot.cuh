@@ -20,6 +20,21 @@ __host__ __device__ constexpr int li_stride() {
   return NB + 2;
 }
 
+// a usable pivot: positive and finite (false for NaN)
+__device__ __forceinline__ bool pivot_ok(double d) { return d > 0.0 && d <= 1.7976931348623157e308; }
+
+// 1/sqrt(x) for a positive normal x without branches: the hardware approximation refined by
+// two Newton steps y <- y + y (1/2 - x/2 y^2), each doubling the correct bits
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  double e = fma(-h * y, y, 0.5);
+  y = fma(y, e, y);
+  e = fma(-h * y, y, 0.5);
+  return fma(y, e, y);
+}
+
 // src: the block's lower triangle with leading dimension ld (global D or a shared tile,
 // which may alias LR); k0: its first row, for the breakdown index.
 template <int NB>
@@ -39,11 +54,10 @@ __device__ __noinline__ void pivot_warp(const double* src, long long ld, int k0,
 #pragma unroll 1
   for (int k = 0; k < NB; ++k) {
     double dkk = __shfl_sync(~0u, c[0], k);
-    if (!(dkk > 0.0) || !isfinite(dkk)) {
-      if (k < nbk) fb = min(fb, bad_base + k0 + k);
-      dkk = 1.0;
-    }
-    const double r = rsqrt(dkk);
+    const bool bad = !pivot_ok(dkk);
+    fb = (bad && k < nbk) ? min(fb, bad_base + k0 + k) : fb;
+    dkk = bad ? 1.0 : dkk;
+    const double r = rsqrt_nr(dkk);
     const double l = (lane == k) ? dkk * r : c[0] * r;  // L[lane][k] for lane >= k
     double* row = LR + k * NB;                           // row[t] = L[k + t][k]
     if (lane >= k && lane < NB) row[lane - k] = l;
@@ -147,17 +161,19 @@ __device__ __noinline__ void pivot_pair(const double* src, long long ld, int k0,
     auto step = [&](int k, auto width) {
       constexpr int WD = decltype(width)::value;
       const double l = (lane == k) ? dkk * r : c[0] * r;
-      double dn = __shfl_sync(~0u, c[1] - l * l, (k + 1) & 31);
-      if (k + 1 < NB && (!(dn > 0.0) || !isfinite(dn))) {
-        if (k + 1 < nbk) fb = min(fb, bad_base + k0 + k + 1);
-        dn = 1.0;
-      }
-      const double rn = rsqrt(dn);
+      const double dn0 = __shfl_sync(~0u, c[1] - l * l, (k + 1) & 31);
       double* row = LR + k * NB;
       if (lane >= k && lane < NB) row[lane - k] = l;
       if (lane == k) ir[k] = r;
       __syncwarp();
       if (lane == 0) st_release_shared(progress, tag * 64 + k + 1);
+      // branch-free pivot check and rsqrt: the step stays one basic block, so the scheduler
+      // interleaves the Newton steps with the column update below instead of the warp
+      // stalling on each of them in turn (the library rsqrt branches to a slow path)
+      const bool bad = k + 1 < NB && !pivot_ok(dn0);
+      fb = (bad && k + 1 < nbk) ? min(fb, bad_base + k0 + k + 1) : fb;
+      const double dn = bad ? 1.0 : dn0;
+      const double rn = rsqrt_nr(dn);
       c[0] = c[1] - row[1] * l;
 #pragma unroll
       for (int t = 2; t < WD; t += 2) {
