@@ -313,9 +313,13 @@ __device__ __forceinline__ void kk_update_mma(const double* __restrict__ D, int 
       const int v = 8 * nb + 2 * t + h;
       d0[nb][h] = (nb <= part && v <= u && u < nb1) ? D[prow_off32(k1 + u) + k1 + v] : 0.0;
     }
-  double acc[4][2];
+  // even and odd k-steps in separate accumulators: two dependent DMMA chains of 4 instead of
+  // one of 8 (a warp has at most 4 blocks, too few to hide the DMMA latency otherwise)
+  double acc[2][4][2];
 #pragma unroll
-  for (int nb = 0; nb < 4; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
+  for (int e = 0; e < 2; ++e)
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) acc[e][nb][0] = acc[e][nb][1] = 0.0;
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks) {
     if (4 * ks >= nbk) break;
@@ -323,14 +327,15 @@ __device__ __forceinline__ void kk_update_mma(const double* __restrict__ D, int 
     const double a = zc[8 * part + g];
 #pragma unroll
     for (int nb = 0; nb < 4; ++nb)
-      if (nb <= part) dmma_8x8x4(acc[nb], a, zc[8 * nb + g]);
+      if (nb <= part) dmma_8x8x4(acc[ks & 1][nb], a, zc[8 * nb + g]);
   }
 #pragma unroll
   for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int v = 8 * nb + 2 * t + h;
-      if (nb <= part && v <= u && u < nb1) P[u * 33 + v] = d0[nb][h] - acc[nb][h];
+      if (nb <= part && v <= u && u < nb1)
+        P[u * 33 + v] = d0[nb][h] - (acc[0][nb][h] + acc[1][nb][h]);
     }
 }
 
@@ -568,6 +573,19 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       cnt[3 + ((step + 1) & 1)] = 0;
     }
     PROF_MARK(1); FTL_MARK(0);
+#ifndef FFB_KKPF
+#define FFB_KKPF 1
+#endif
+    if (FFB_KKPF && la_reg && warp < 4 && k1 < kd && lane < 16) {
+      // the next pivot block A_K'K' is final since the previous step (its tile is the
+      // look-ahead's private copy now): pull its rows into L1 while Z is formed, so the
+      // look-ahead update after the Z barrier does not wait a full L2 round trip for them
+      const int u = 8 * warp + (lane >> 1);
+      if (u < min(NB, kd - k1)) {
+        const double* pf = D + prow_off32(k1 + u) + k1 + 16 * (lane & 1);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(pf));
+      }
+    }
     // ---- Z = A_RK Li^T
     if constexpr (NB == 32) {
       // on the FP64 tensor cores: rows in blocks of 8 (K is 8-aligned, so a block is wholly
@@ -603,13 +621,17 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) a[ks] = an[ks];
         load_panel(rb + rstep);
-        double acc[4][2];
+        // two accumulator chains per column block (even / odd k-steps; see kk_update_mma)
+        double acc[4][2], acc1[4][2];
 #pragma unroll
         for (int nb = 0; nb < 4; ++nb) {
-          acc[nb][0] = acc[nb][1] = 0.0;
+          acc[nb][0] = acc[nb][1] = acc1[nb][0] = acc1[nb][1] = 0.0;
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks)
-            if (ks <= 2 * nb + 1) dmma_8x8x4(acc[nb], a[ks], Li[(8 * nb + g) * LDL + 4 * ks + t4]);
+            if (ks <= 2 * nb + 1)
+              dmma_8x8x4((ks & 1) ? acc1[nb] : acc[nb], a[ks], Li[(8 * nb + g) * LDL + 4 * ks + t4]);
+          acc[nb][0] += acc1[nb][0];
+          acc[nb][1] += acc1[nb][1];
         }
 #pragma unroll
         for (int nb = 0; nb < 4; ++nb)
