@@ -1964,7 +1964,8 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
                  long long scratch_stride, int* d_bad, cudaStream_t st, const int2* changed,
                  double* fac_t) {
   const int kdp = (kd_max + 31) / 32 * 32;
-  static const int la = [] {
+  // schedule switches are read per call (tests switch them within one process)
+  const int la = [] {
     const char* e = std::getenv("FFB_LOOKAHEAD");
     return e ? std::atoi(e) : 1;
   }();
@@ -1983,7 +1984,7 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
   int lac = (C > 1 && nb != 32) ? 0 : la;
   // DMMA tile updates (measured c2 -9%, c3 -13% of the factorisation time; NB = 16, c5: -14%
   // once the tiles' read-modify-writes went to 16-byte pairs). FFB_FACTOR_MMA=0 forces FFMA.
-  static const int mma = [] {
+  const int mma = [] {
     const char* e = std::getenv("FFB_FACTOR_MMA");
     return e ? std::atoi(e) : -1;
   }();
