@@ -517,6 +517,70 @@ __device__ __forceinline__ void rupd_tile_mma(double* __restrict__ D, int kd, in
   }
 }
 
+// tile_ark on the FP64 tensor cores (NB = 32): out[u][c] = sum_c2 Z[c2][u] Li[c2][c] as 4x4
+// DMMA blocks, A[m][k] = Z[c0+k][r0+m], B[k][n] = Li[c0+k][n]; column block j needs only the
+// k-steps from its diagonal on (Li is lower triangular). Besides a quarter of the issue
+// slots of the FFMA tile, it keeps the FP64 FFMA pipe free for the pivot warps' chain.
+__device__ __forceinline__ void tile_ark_mma(double* __restrict__ D, int kd, int zs,
+                                             const double* Z, const double* Li, int r0, int k0,
+                                             int k1, int lane) {
+  constexpr int LDL = li_stride<32>();
+  const int g = lane >> 2, t = lane & 3;
+  const int nbk = k1 - k0;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 2
+  for (int ks = 0; ks < 8; ++ks) {
+    const double* zc = Z + (4 * ks + t) * zs + r0;
+    const double* lc = Li + (4 * ks + t) * LDL;
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = zc[8 * i + g];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = lc[8 * j + g];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (ks >= 2 * j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int u = r0 + 8 * i + g;
+    if (u >= kd || (u >= k0 && u < k1)) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = 8 * j + 2 * t;
+      if (u >= k1) {  // row u below K: columns (c, c + 1) of its K segment, 16-byte store
+        if (c + 1 < nbk)
+          *reinterpret_cast<double2*>(D + prow_off32(u) + k0 + c) =
+              make_double2(acc[i][j][0], acc[i][j][1]);
+        else if (c < nbk)
+          D[prow_off32(u) + k0 + c] = acc[i][j][0];
+      } else {  // row u above K: stored transposed, in rows k0 + c and k0 + c + 1
+        if (c < nbk) D[prow_off32(k0 + c) + u] = acc[i][j][0];
+        if (c + 1 < nbk) D[prow_off32(k0 + c + 1) + u] = acc[i][j][1];
+      }
+    }
+  }
+}
+
+#ifndef FFB_ARK_MMA
+#define FFB_ARK_MMA 1
+#endif
+template <int NB>
+__device__ __forceinline__ void ark_tile(bool use_mma, double* __restrict__ D, int kd, int zs,
+                                         const double* Z, const double* Li, int r0, int k0,
+                                         int k1, int lane) {
+  if constexpr (NB == 32 && FFB_ARK_MMA) {
+    if (use_mma) return tile_ark_mma(D, kd, zs, Z, Li, r0, k0, k1, lane);
+  }
+  tile_ark<NB>(D, kd, zs, Z, Li, r0, k0, k1, lane);
+}
+
 // P (stride NB+1) <- the nbk x nbk diagonal block at (k, k) of the packed line D (lower)
 template <int NB>
 __device__ __forceinline__ void load_block(const double* __restrict__ D, int k, int nbk,
@@ -723,7 +787,7 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
         if (lane == 0) T = q + C * atomicAdd(cnt + 3 + (step & 1), 1);
         T = __shfl_sync(~0u, T, 0);
         if (32 * T >= kd) break;
-        tile_ark<NB>(D, kd, zs, Z, Li, 32 * T, k0, k1, lane);
+        ark_tile<NB>(use_mma, D, kd, zs, Z, Li, 32 * T, k0, k1, lane);
 #ifdef FFB_PROFILE
         ++ftl_n;
 #endif
@@ -777,8 +841,9 @@ __device__ void sweep_invert(double* __restrict__ D, int kd, int kdp, double* P,
       // ---- A_RK <- Z Li ; A_KK <- -Li^T Li, as 32x32 tiles (4x8 per lane): row tiles
       // q, q + C, ... of the cluster over this CTA's participating warps; A_KK by one warp
       const int w0 = la ? 0 : 1, nw = kFW - w0, wi = warp - w0;
-      for (int T = q + C * wi; 32 * T < kd; T += C * nw)
-        tile_ark<NB>(D, kd, zs, Z, Li, 32 * T, k0, k1, lane);
+      for (int T = q + C * wi; 32 * T < kd; T += C * nw) {
+        ark_tile<NB>(use_mma, D, kd, zs, Z, Li, 32 * T, k0, k1, lane);
+      }
       if (q == C - 1 && warp == kFW - 1) tile_akk<NB>(D, kd, Li, k0, nbk, lane);
     }
     PROF_MARK(7);
