@@ -1887,29 +1887,18 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       const double tv1 = (a1[0] + a1[1]) + (a1[2] + a1[3]);
       // x of my rows, the outputs, and the operand of the next line
       const bool more = t + 1 < nl;
-      double wn0 = 0.0, wn1 = 0.0;
+      double wn0 = 0.0, wn1 = 0.0, vo0 = 0.0, vo1 = 0.0;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int i = q == 0 ? io0 : io1;
         if ((q == 0 ? ob0 : ob1) < 0 || i >= kd) continue;
         const double tv = q == 0 ? tv0 : tv1;
-        const long long e = static_cast<long long>(l) * kd + i;
-        double v;
-        if (phase == 0) {
-          v = tv;
-          yl[e] = v;
-          if (L == 1) zl[e] = v;
-        } else if (t == 0) {
-          v = tv;
-          if (chain == 0) zl[e] = v;  // middle line, written once
-        } else {
-          v = (q == 0 ? py0 : py1) - tv;
-          zl[e] = v;
-        }
+        const double v = (phase == 1 && t > 0) ? (q == 0 ? py0 : py1) - tv : tv;
         const double b = q == 0 ? pb0 : pb1, rr = q == 0 ? pr0 : pr1;
         const double w = phase == 0 ? rr - b * v : b * v;
-        if (q == 0) wn0 = w; else wn1 = w;
+        if (q == 0) wn0 = w, vo0 = v; else wn1 = w, vo1 = v;
       }
+      TL_MARK(1);  // owners: sums done
       if (more) {
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
@@ -1922,10 +1911,26 @@ __global__ void __launch_bounds__(kTileThreads, 1)
             if (c != crank) st_async_to(mapa_u32(wl, c), w, mapa_u32(bl, c));
           *wn = w;
         }
+        TL_MARK(4);  // owners: operand broadcast issued
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&w_bar[par ^ 1]);
           if (ob1 >= 0) mbar_arrive(&w_bar[par ^ 1]);
+        }
+      }
+      // the outputs after the broadcast: they are off the chain to the next line, and global
+      // stores issued before it would queue in the memory pipeline ahead of the broadcast
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int i = q == 0 ? io0 : io1;
+        if ((q == 0 ? ob0 : ob1) < 0 || i >= kd) continue;
+        const long long e = static_cast<long long>(l) * kd + i;
+        const double v = q == 0 ? vo0 : vo1;
+        if (phase == 0) {
+          yl[e] = v;
+          if (L == 1) zl[e] = v;
+        } else if (t > 0 || chain == 0) {
+          zl[e] = v;  // (t == 0: the middle line, written once)
         }
       }
       owner_prefetch(t + 2, t + 1);

@@ -1,8 +1,7 @@
-# tile warps serialised after the Cholesky chain: off (default) / warps >= 4 / warps >= 10
+# tile solve: owner outputs stored after the broadcast; tests, c2 timings, timeline
 set -x
 timeout 600 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/e_build.log 2>&1
-for v in 4 10 0; do
-  touch paper_1508_02977_b200/csrc/band.cu
-  FFB_NVCC_FLAGS=-DFFB_SERIAL=$v timeout 600 python -c "import __graft_entry__ as g; g.build()" >> gpurun_out/e_build.log 2>&1
-  for c in c2 c2 c3; do echo "SERIAL=$v" >> gpurun_out/e_cases.log; timeout 300 python tools/profile_case.py $c >> gpurun_out/e_cases.log 2>&1; done
-done
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_tile_solve.py tests/test_gpu_ras.py -x -q -m gpu > gpurun_out/e_pytest.log 2>&1; echo "pytest rc $?" >> gpurun_out/e_pytest.log
+for c in c2 c2 c1; do timeout 300 python tools/profile_case.py $c >> gpurun_out/e_cases.log 2>&1; done
+timeout 120 python tools/solve_probe.py c2 >> gpurun_out/e_cases.log 2>&1
+FFB_PROFILE=1 timeout 600 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/t_build.log 2>&1; FFB_PROFILE=1 timeout 300 python tools/tile_timeline.py c2 > gpurun_out/t_tl.log 2>&1
