@@ -1873,16 +1873,12 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       PROF_MARK(5); TL_MARK(5);
       const double* s0 = slots + static_cast<size_t>(ob0) * (nt + 1) * 32 + lane;
       const double* s1 = slots + static_cast<size_t>(ob1 < 0 ? ob0 : ob1) * (nt + 1) * 32 + lane;
+      // unrolled to the table maximum and predicated, so every slot load is issued before the
+      // first add (a runtime-bounded loop serialised load -> add per group of four)
       double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
-      int k = 0;
-      for (; k + 3 <= nt; k += 4) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) a0[u] += s0[(k + u) * 32], a1[u] += s1[(k + u) * 32];
-      }
-      // remainder (k is a multiple of 4 here: contributions k, k + 1, k + 2 -> acc 0, 1, 2)
-#pragma unroll
-      for (int u = 0; u < 3; ++u)
-        if (k + u <= nt) a0[u] += s0[(k + u) * 32], a1[u] += s1[(k + u) * 32];
+      for (int k = 0; k <= kTileMaxNt; ++k)
+        if (k <= nt) a0[k & 3] += s0[k * 32], a1[k & 3] += s1[k * 32];
       const double tv0 = (a0[0] + a0[1]) + (a0[2] + a0[3]);
       const double tv1 = (a1[0] + a1[1]) + (a1[2] + a1[3]);
       // x of my rows, the outputs, and the operand of the next line
