@@ -1557,7 +1557,8 @@ __device__ __forceinline__ void mbar_wait_g(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ uint32_t mapa_u32(uint32_t local, unsigned rank) {
   uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  // not volatile: a pure address translation, so the compiler may hoist it out of the line loop
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
   return r;
 }
 __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
