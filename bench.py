@@ -33,9 +33,11 @@ METRIC = "full flow solve Mpixel/s (fp64)"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default=os.environ.get("FFB_BENCH_CONFIG", "c2"))
+    # c4 (2160x3840, 16x16 subdomains): the largest configuration, the one the north_star's
+    # targets are quoted on; it fits one B200 (45 GB of factors)
+    ap.add_argument("--config", default=os.environ.get("FFB_BENCH_CONFIG", "c4"))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -120,18 +122,59 @@ def run_config_for(cfg, ff):
                         cg_tolerance=cfg.tol)
 
 
+def workload_config(cfg):
+    """The `config` block of both arms' lines: the workload only (identical in both)."""
+    from paper_1508_02977_b200 import flowfem as ff
+    sp = ff.choose_split(cfg.W, cfg.H, cfg.parts)  # host-only (schwarz.cpp:32-44)
+    px, py = sp.parts_x, sp.parts_y
+    return {"workload": cfg.name, "H": cfg.H, "W": cfg.W, "parts": f"{px}x{py}",
+            "overlap": cfg.overlap, "n_passes": cfg.n_passes, "tol": cfg.tol,
+            "protocol": "converged-pass (SURVEY D2): n_passes x {solve to tol, "
+                        "error_indicator, update_alpha} + final solve",
+            "l2": "GPU arm: flushed (256 MB write) between steps; band factors > L2"}
+
+
+def ref_iters(cfg):
+    """Per-solve CG iteration counts of a full reference chain at the config's tolerance
+    (tests/golden/ref_chain_iters.json, made by tests/golden/make_golden_large.py --iters)."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "ref_chain_iters.json")) as fh:
+            return json.load(fh).get(cfg.name)
+    except Exception:
+        return None
+
+
 def cpu_reference_step(f0, f1, cfg):
-    """The reference's own CPU path (oracle/_ref; else the C port), converged-pass protocol."""
+    """One bounded step of the reference's own CPU path (oracle/_ref; the C port when the
+    reference was not built), converged-pass protocol, all host cores. Configurations whose
+    full chain is short (c1, c2) run it whole; the others run one timed instance of every
+    stage (ref_chain_sample: imaging, mesh, assemble, CG set-up + iterations, indicator +
+    update) and extrapolate the chain with the per-solve iteration counts of a committed full
+    reference run. Returns (seconds, kind, cores, sample description)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
     o = pyoracle.REF or pyoracle.PORT
     cores = os.cpu_count() or 1
     o.set_threads(cores)
-    t = time.perf_counter()
-    r = o.converged_chain(f0, f1, cfg.sigma, rho=cfg.rho, alpha0=cfg.alpha0,
-                          lambda0=cfg.lambda0, n_passes=cfg.n_passes, kappa=cfg.kappa,
-                          thr=cfg.eta_threshold, tol=cfg.tol)
-    return time.perf_counter() - t, o.kind, cores, r
+    it = ref_iters(cfg)
+    full = it is None or o is not pyoracle.REF or it["seconds"] * it["threads"] / cores <= 20.0
+    if full:
+        t = time.perf_counter()
+        o.converged_chain(f0, f1, cfg.sigma, rho=cfg.rho, alpha0=cfg.alpha0, lambda0=cfg.lambda0,
+                          n_passes=cfg.n_passes, kappa=cfg.kappa, thr=cfg.eta_threshold,
+                          tol=cfg.tol)
+        dt = time.perf_counter() - t
+        return dt, o.kind, cores, (f"full converged-pass chain of {cfg.name} ({dt:.1f} s; "
+                                   f"reference Jacobi-CG, monolithic), {cpu_model()}")
+    smp = pyoracle.ref_chain_sample(f0, f1, cfg.sigma, rho=cfg.rho, alpha0=cfg.alpha0,
+                                    lambda0=cfg.lambda0, kappa=cfg.kappa, thr=cfg.eta_threshold)
+    dt = pyoracle.extrapolate_chain(smp, it["iters"])
+    return dt, o.kind, cores, (
+        f"extrapolated: one timed instance of every stage of the {cfg.name} chain on the real "
+        f"input ({smp['wall']:.1f} s: imaging {smp['imaging']:.2f}, assemble {smp['assemble']:.2f}, "
+        f"CG {smp['cg_iter'] * 1e3:.1f} ms/iteration, indicator+update {smp['adapt']:.2f} s) x the "
+        f"{sum(it['iters'])} CG iterations of {len(it['iters'])} solves of a full reference run "
+        f"(tests/golden/ref_chain_iters.json) = {dt:.1f} s per chain; {cpu_model()}")
 
 
 def cpu_model():
@@ -149,39 +192,78 @@ def bench_reference(args, cfg, f0, f1):
     if rank != 0:
         return
     npx = cfg.H * cfg.W
-    for _ in range(min(args.warmup, 1)):
+    for _ in range(args.warmup):
         cpu_reference_step(f0, f1, cfg)
     times = []
-    kind = cores = None
+    kind = cores = sample = None
     for _ in range(args.steps):
-        dt, kind, cores, _r = cpu_reference_step(f0, f1, cfg)
+        dt, kind, cores, sample = cpu_reference_step(f0, f1, cfg)
         times.append(dt)
     tot = sum(times)
     v = npx * len(times) / tot / 1e6
-    # the B200 arm's config block, so the two lines describe the same workload
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle
-    o = pyoracle.REF or pyoracle.PORT
-    px, py = o.choose_split(cfg.W, cfg.H, cfg.parts)[:2]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "Mpixel/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1),
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "H": cfg.H, "W": cfg.W, "parts": f"{px}x{py}",
-                   "overlap": cfg.overlap, "n_passes": cfg.n_passes, "tol": cfg.tol,
-                   "parallelism": "host cores (OpenMP)"},
+        "config": workload_config(cfg),
         "cpu_baseline": {"value": v, "unit": "Mpixel/s", "cores": cores, "kind": kind,
-                         "sample": f"{args.steps} full converged-pass solves of {cfg.name} "
-                                   f"(reference Jacobi-CG, monolithic), {cpu_model()}"},
+                         "sample": f"each step: {sample}"},
         "e2e": {"value": v, "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def fp64_peak():
+    """FP64 denominator of the factor's roofline: profiles/fp64_peak.json (tools/microbench/
+    fp64_peak.cu on the B200: device-wide DMMA rate), else the nominal DMMA rate."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
+            return float(json.load(fh)["dmma_tflops"]), "measured (profiles/fp64_peak.json)"
+    except Exception:
+        return 2 * 64 * 148 * 1.965e9 / 1e12, "nominal (64 DMMA FMA/clk/SM x 148 SMs x 1.965 GHz)"
+
+
+def roofline_factor(s):
+    """Second roofline: the subdomain factorisation (k_line_factor) against the FP64 tensor
+    (DMMA) rate — algorithmic flops of one full factorisation (sum_i n_i kd_i^2, 2 flops per
+    FMA) over the first pass's factorisation time (CUDA events on the launching stream; the
+    later passes refactor incrementally)."""
+    if not s.ms_factor_full or not s.factor_flops:
+        return None
+    peak, kind = fp64_peak()
+    ach = s.factor_flops / (s.ms_factor_full * 1e-3) / 1e12
+    return {"bound": "fp64 tensor (DMMA)", "kernel": "k_line_factor (full factorisation)",
+            "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+            "peak_kind": kind, "flops_per_launch": s.factor_flops,
+            "ms_per_launch": s.ms_factor_full, "traffic": None}
+
+
+def maybe_spawn(args):
+    """`bench.py --gpus N` without torchrun: launch the N ranks ourselves (one per GPU) through
+    torch.distributed.run on 127.0.0.1, then exit with its status."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} needs {args.gpus} GPUs, "
+                                                     f"found {have}"}), flush=True)
+        sys.exit(2)
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    maybe_spawn(args)
     rank, world, local = dist_env()
     from paper_1508_02977_b200 import synth
     f0, f1, _, cfg = synth.make(args.config, seed=0)
@@ -297,9 +379,8 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic",
-                "config": {"workload": cfg.name, "H": H, "W": W, "parts": cfg.parts,
-                           "overlap": cfg.overlap, "n_passes": cfg.n_passes, "tol": cfg.tol,
-                           "parallelism": f"subdomains sharded over {world} GPUs"},
+                "config": workload_config(cfg),
+                "parallelism": f"subdomains sharded over {world} GPUs",
                 "gpu_launches": int(launches), "e2e": e2e, "roofline": None,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
@@ -321,10 +402,8 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": cfg.name, "H": H, "W": W, "parts": f"{s.parts_x}x{s.parts_y}",
-                   "overlap": cfg.overlap, "n_passes": cfg.n_passes, "tol": cfg.tol,
-                   "parallelism": f"subdomains sharded over {world} GPUs" if world > 1 else "1gpu",
-                   "l2": "flushed (256 MB write) between steps; band factors > L2"},
+        "config": workload_config(cfg),
+        "parallelism": f"subdomains sharded over {world} GPUs" if world > 1 else "1gpu",
         "gpu_launches": int(launches),
         "e2e": e2e,
         "roofline": {"bound": "hbm", "kernel": f"{kname} (subdomain fwd/bwd sweeps)",
@@ -335,6 +414,7 @@ def main():
                      "frac": (achieved / peak) if achieved else None,
                      "traffic": profiled_traffic(cfg.name), "peak_kind": peak_kind,
                      "bytes_per_launch": asm_bytes, "ms_per_launch": s.ms_asm_per_iter},
+        "roofline_factor": roofline_factor(s),
         "solver": {"pcg_iterations_per_step": iters_total, "iters": s.iters,
                    "ms_terms": s.ms_terms, "ms_factor": s.ms_factor, "ms_pcg": s.ms_pcg,
                    "ms_adapt": s.ms_adapt, "ms_total": s.ms_total,
@@ -344,11 +424,9 @@ def main():
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        dt, kind, cores, _ = cpu_reference_step(f0, f1, cfg)
+        dt, kind, cores, sample = cpu_reference_step(f0, f1, cfg)
         line["cpu_baseline"] = {"value": npx / dt / 1e6, "unit": "Mpixel/s", "cores": cores,
-                                "kind": kind,
-                                "sample": f"1 full converged-pass solve of {cfg.name} "
-                                          f"({dt:.1f} s; reference Jacobi-CG), {cpu_model()}"}
+                                "kind": kind, "sample": sample}
     print(json.dumps(line), flush=True)
     if pg:
         pg.destroy_process_group()

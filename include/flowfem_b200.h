@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define FFB_ABI_VERSION 1
+#define FFB_ABI_VERSION 2
 
 typedef struct ffb_ctx ffb_ctx;
 
@@ -52,7 +52,7 @@ typedef struct ffb_run_config {
   int n_passes;          /* AdaptConfig::n_adapt: alpha updates; n_passes+1 solves */
   double kappa;          /* update_alpha (adapt.cpp:101-112) */
   double eta_threshold;
-  double alpha_th;       /* <= 0 -> alpha0/100 (pipeline.cpp:71) */
+  double alpha_th;       /* NaN -> alpha0/100 (unset std::optional, pipeline.cpp:71) */
   double tol;            /* SolverConfig::cg_tolerance, true relative residual */
   int max_iters;         /* 0 -> 10 * unknowns (linsolve.cpp:333) */
 } ffb_run_config;
@@ -71,6 +71,9 @@ typedef struct ffb_run_stats {
                                            preconditioner application streams */
   double iter_bytes;                    /* algorithmic HBM bytes per PCG iteration */
   double ms_asm_per_iter;               /* mean duration of the subdomain-solve kernel */
+  double ms_factor_full;                /* the first pass's (full) factorisation */
+  double factor_flops;                  /* algorithmic flops of one full factorisation,
+                                           sum_i n_i kd_i^2 (n kd^2 / 2 FMAs per subdomain) */
 } ffb_run_stats;
 
 /* ---- library ---------------------------------------------------------------------- */
@@ -190,17 +193,54 @@ int ffb_pcg_solve(ffb_ctx* ctx, int nc, double tol, int max_iters, int warm, dou
 int ffb_adapt(ffb_ctx* ctx, int nc, double kappa, double eta_thr, double alpha_th,
               double* eta_max);
 
+/* SchwarzOptions (schwarz.hpp:59-66) with its AdaptConfig (adapt.hpp:24-30) and
+ * SolverConfig (linsolve.hpp:12-17) flattened. */
+typedef struct ffb_schwarz_options {
+  int n_iters;              /* 10 */
+  int workers;              /* accepted for signature parity; the device ignores it (results are
+                               independent of workers in the reference too) */
+  int components;           /* 3, or 2 without the illumination field */
+  int adapt;                /* AdaptConfig::enabled */
+  int n_adapt;              /* AdaptConfig::n_adapt: iterations that update alpha */
+  double kappa, eta_threshold, alpha_th;
+  int method;               /* FFB_SOLVE_CHOLESKY | FFB_SOLVE_CG (SolverConfig::method) */
+  int cg_max_iters;         /* SolverConfig::cg_max_iters, 0 -> 10 n */
+  double cg_tolerance;      /* SolverConfig::cg_tolerance */
+  int record_alpha_history; /* SchwarzOptions::record_alpha_history */
+} ffb_schwarz_options;
+
+/* SchwarzStats (schwarz.hpp:68-73): caller-owned arrays, each may be NULL. */
+typedef struct ffb_schwarz_stats {
+  double* increments;    /* [n_iters] max-norm change of the composed field */
+  double* seconds;       /* [n_iters] wall time per iteration (adds one sync per iteration) */
+  double* eta_max;       /* [min(n_adapt, n_iters)] indicator max per alpha update */
+  double* alpha_history; /* [min(n_adapt, n_iters) * ntri] alpha after each update, when
+                            record_alpha_history != 0 */
+  int n_updates;         /* out: alpha updates performed */
+} ffb_schwarz_stats;
+
 /* schwarz_solve (schwarz.hpp:79-81, schwarz.cpp:162-319): the reference's own synchronous
  * restricted-additive-Schwarz loop on the resident terms / reg / partition — per iteration
- * every subdomain solves with Dirichlet traces from the previous composed field (one step of
- * iterative refinement when refine != 0, as the reference's Cholesky path), cores are
- * composed, increments[it] = max-norm change; when adapt != 0 alpha is updated after each of
- * the first n_adapt iterations (eta_max[k] recorded) and the factors are refreshed. u3:
- * planes3 out; increments: n_iters; eta_max: min(n_adapt, n_iters). Resident alpha is
- * updated in place (RegField& reg). */
+ * every subdomain solves its Dirichlet problem with traces from the previous composed field,
+ * cores are composed, increments[it] = max-norm change; with adapt, alpha is updated after
+ * each of the first n_adapt iterations and the subdomain operators follow. Subdomain solver:
+ * FFB_SOLVE_CHOLESKY = the device factorisation + one refinement step (schwarz.cpp:236-247);
+ * FFB_SOLVE_CG = the reference's Jacobi-PCG per subdomain warm-started from the previous
+ * iteration's subdomain solution (schwarz.cpp:248-252), bitwise equal to the reference's.
+ * u3: planes3 out. Resident alpha is updated in place (RegField& reg). */
+int ffb_schwarz_run(ffb_ctx* ctx, const ffb_schwarz_options* opt, double* u3,
+                    ffb_schwarz_stats* stats);
+/* ABI-1 form of ffb_schwarz_run with the Cholesky subdomain solver (refine must be 1). */
 int ffb_schwarz_solve(ffb_ctx* ctx, int n_iters, int nc, int adapt, int n_adapt, double kappa,
                       double eta_thr, double alpha_th, int refine, double* u3,
                       double* increments, double* eta_max);
+
+/* energy (assembly.hpp:70-73, assembly.cpp:201-238): the discrete energy whose gradient is
+ * A x - b, as a deterministic device reduction (u3 planes3). */
+int ffb_energy(ffb_ctx* ctx, int W, int H, const double* t10, const double* alpha,
+               const double* lambda, const double* u3, int nc, double* e);
+/* energy of the resident solution with the resident terms and regularisation */
+int ffb_energy_resident(ffb_ctx* ctx, int nc, double* e);
 
 /* ---- multi-GPU: subdomains sharded over ranks (one process per GPU) ------------------
  * Rank r of `world` factors and solves subdomains [lo, hi) (contiguous in partition order);

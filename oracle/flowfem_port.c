@@ -952,3 +952,61 @@ int fp_converged_chain(int W, int H, const double* f0, const double* f1, double 
   if (seconds_out) *seconds_out = (ts1.tv_sec - ts0.tv_sec) + 1e-9 * (ts1.tv_nsec - ts0.tv_nsec);
   return rc;
 }
+
+/* ---------------------------------------------------------------- energy */
+
+/* Discrete energy (assembly.cpp:201-238): 1/2 (sum_t area (alpha |grad u1|^2 + alpha
+ * |grad u2|^2 + lambda |grad mt|^2) + sum_v lumped_v (U^T A_v U - 2 F_v^T U + c_v)).
+ * Both sums run serially in the reference's order, so the result is bitwise equal. */
+int fp_energy(int W, int H, const double* t10, const double* alpha, const double* lambda,
+              const double* u3, int nc, double* e_out) {
+  if (nc != 2 && nc != 3) return fail("assembly.energy: components must be 2 or 3");
+  const size_t n = (size_t)W * H;
+  const long ntri = 2L * (W - 1) * (H - 1);
+  const double* u1 = u3;
+  const double* u2 = u3 + n;
+  const double* mt = u3 + 2 * n;
+  double e_grad = 0.0;
+  for (long t = 0; t < ntri; ++t) {
+    long v[3];
+    tri_vertices(W, t, v);
+    const double* gx = (t & 1) ? GX_UP : GX_LO;
+    const double* gy = (t & 1) ? GY_UP : GY_LO;
+    double du1x = 0, du1y = 0, du2x = 0, du2y = 0, dmx = 0, dmy = 0;
+    for (int k = 0; k < 3; ++k) {
+      du1x += gx[k] * u1[v[k]];
+      du1y += gy[k] * u1[v[k]];
+      du2x += gx[k] * u2[v[k]];
+      du2y += gy[k] * u2[v[k]];
+      if (nc == 3) {
+        dmx += gx[k] * mt[v[k]];
+        dmy += gy[k] * mt[v[k]];
+      }
+    }
+    double s = alpha[t] * (du1x * du1x + du1y * du1y + du2x * du2x + du2y * du2y);
+    if (nc == 3) s += lambda[t] * (dmx * dmx + dmy * dmy);
+    e_grad += 0.5 * s;
+  }
+  double e_data = 0.0;
+  for (int y = 0; y < H; ++y)
+    for (int x = 0; x < W; ++x) {
+      const size_t v = (size_t)y * W + x;
+      double A[9] = {0}, F[3] = {0};
+      A[0] = t10[0 * n + v], A[1] = t10[1 * n + v], A[3] = t10[1 * n + v], A[4] = t10[3 * n + v];
+      F[0] = t10[6 * n + v], F[1] = t10[7 * n + v];
+      if (nc == 3) {
+        A[2] = t10[2 * n + v], A[5] = t10[4 * n + v];
+        A[6] = t10[2 * n + v], A[7] = t10[4 * n + v], A[8] = t10[5 * n + v];
+        F[2] = t10[8 * n + v];
+      }
+      const double U[3] = {u1[v], u2[v], nc == 3 ? mt[v] : 0.0};
+      double quad = 0.0, lin = 0.0;
+      for (int c = 0; c < nc; ++c) {
+        for (int c2 = 0; c2 < nc; ++c2) quad += U[c] * A[c * 3 + c2] * U[c2];
+        lin += F[c] * U[c];
+      }
+      e_data += lumped_weight(x, y, W, H) * (quad - 2.0 * lin + t10[9 * n + v]);
+    }
+  *e_out = 0.5 * (e_grad + e_data);
+  return 0;
+}

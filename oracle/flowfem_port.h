@@ -47,6 +47,8 @@ int fp_error_indicator(int W, int H, const double* t10, const double* alpha,
                        double* eta_max);
 int fp_update_alpha(int ntri, const double* alpha, const double* eta, double eta_max,
                     double kappa, double eta_thr, double alpha_th, double* alpha_out);
+int fp_energy(int W, int H, const double* t10, const double* alpha, const double* lambda,
+              const double* u3, int nc, double* e);
 int fp_converged_chain(int W, int H, const double* f0, const double* f1, double sigma,
                        double rho, double alpha0, double lambda0, int nc, int n_passes,
                        double kappa, double eta_thr, double alpha_th, double tol, double* out3,

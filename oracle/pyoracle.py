@@ -158,6 +158,14 @@ class Oracle:
                        C.c_double(alpha_th), _ptr(out))
         return out
 
+    def energy(self, terms, alpha, lam, u3, nc=3):
+        """energy (assembly.cpp:201-238)."""
+        terms, alpha, lam, u3 = map(_f64, (terms, alpha, lam, u3))
+        H, W = terms.shape[1:]
+        e = C.c_double()
+        self._call("energy", W, H, _ptr(terms), _ptr(alpha), _ptr(lam), _ptr(u3), nc, C.byref(e))
+        return e.value
+
     def converged_chain(self, f0, f1, sigma, rho=2.5, alpha0=1000.0, lambda0=1000.0, nc=3,
                         n_passes=3, kappa=10.0, thr=0.1, alpha_th=None, tol=1e-10):
         """D2 converged-pass protocol; returns dict(u3, alpha, eta_max, iters, seconds)."""
@@ -303,6 +311,33 @@ def _load(sub, name, prefix, kind):
 
 PORT = _load("_port", "libflowfem_port.so", "fp_", "port")
 REF = _load("_ref", "libflowfem_ref.so", "ref_", "reference")
+
+
+def ref_chain_sample(f0, f1, sigma, rho=2.5, alpha0=1000.0, lambda0=1000.0, nc=3, kappa=10.0,
+                     thr=0.1, alpha_th=None, cap_lo=2, cap_hi=12):
+    """A timed one-of-each-stage sample of the reference's converged-pass chain
+    (ref_capi.cpp ref_chain_sample); returns the stage seconds as a dict."""
+    if REF is None:
+        raise OracleError("reference oracle not built")
+    f0, f1 = _f64(f0), _f64(f1)
+    H, W = f0.shape
+    if alpha_th is None:
+        alpha_th = alpha0 / 100.0
+    t = np.zeros(8)
+    REF._call("chain_sample", W, H, _ptr(f0), _ptr(f1), C.c_double(sigma), C.c_double(rho),
+              C.c_double(alpha0), C.c_double(lambda0), nc, C.c_double(kappa), C.c_double(thr),
+              C.c_double(alpha_th), int(cap_lo), int(cap_hi), _ptr(t))
+    keys = ("imaging", "mesh_reg", "assemble", "cg_setup", "cg_iter", "expand", "adapt", "wall")
+    return dict(zip(keys, t.tolist()))
+
+
+def extrapolate_chain(sample: dict, iters) -> float:
+    """Seconds of a full converged-pass chain from a ref_chain_sample and the per-solve CG
+    iteration counts of a full reference run (len(iters) = n_passes + 1 solves)."""
+    n_solves = len(iters)
+    return (sample["imaging"] + sample["mesh_reg"]
+            + n_solves * (sample["assemble"] + sample["cg_setup"] + sample["expand"])
+            + sum(iters) * sample["cg_iter"] + (n_solves - 1) * sample["adapt"])
 
 
 def ref_schwarz_solve(terms, alpha, lam, px, py, ov, n_iters, workers=1, nc=3, adapt=False,

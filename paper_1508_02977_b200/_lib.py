@@ -30,7 +30,21 @@ class RunStatsC(C.Structure):
                 ("ms_terms", C.c_double), ("ms_factor", C.c_double), ("ms_pcg", C.c_double),
                 ("ms_adapt", C.c_double), ("ms_total", C.c_double),
                 ("factor_doubles", C.c_double), ("iter_bytes", C.c_double),
-                ("ms_asm_per_iter", C.c_double)]
+                ("ms_asm_per_iter", C.c_double), ("ms_factor_full", C.c_double),
+                ("factor_flops", C.c_double)]
+
+
+class SchwarzOptionsC(C.Structure):
+    _fields_ = [("n_iters", C.c_int), ("workers", C.c_int), ("components", C.c_int),
+                ("adapt", C.c_int), ("n_adapt", C.c_int), ("kappa", C.c_double),
+                ("eta_threshold", C.c_double), ("alpha_th", C.c_double), ("method", C.c_int),
+                ("cg_max_iters", C.c_int), ("cg_tolerance", C.c_double),
+                ("record_alpha_history", C.c_int)]
+
+
+class SchwarzStatsC(C.Structure):
+    _fields_ = [("increments", C.c_void_p), ("seconds", C.c_void_p), ("eta_max", C.c_void_p),
+                ("alpha_history", C.c_void_p), ("n_updates", C.c_int)]
 
 
 _vp = C.c_void_p
@@ -73,6 +87,9 @@ SIGNATURES = {
     "ffb_pcg_solve": (_i, [_vp, _i, _d, _i, _i, _vp, _vp, _vp]),
     "ffb_adapt": (_i, [_vp, _i, _d, _d, _d, _vp]),
     "ffb_schwarz_solve": (_i, [_vp, _i, _i, _i, _i, _d, _d, _d, _i, _vp, _vp, _vp]),
+    "ffb_schwarz_run": (_i, [_vp, C.POINTER(SchwarzOptionsC), _vp, C.POINTER(SchwarzStatsC)]),
+    "ffb_energy": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _i, _vp]),
+    "ffb_energy_resident": (_i, [_vp, _i, _vp]),
     "ffb_shard_range": (_i, [_i, _i, _i, _vp, _vp]),
     "ffb_set_shard": (_i, [_vp, _i, _i]),
     "ffb_pcg_begin": (_i, [_vp, _i, _d, _i, _i, _vp]),

@@ -223,7 +223,99 @@ __global__ void k_update_alpha(double* __restrict__ out, const double* __restric
   }
 }
 
+// a25: discrete energy (assembly.cpp:201-238), a device reduction. One thread takes the
+// two triangles of a cell (gradient term) and the vertex of the same index (data term);
+// per-thread sums, warp/block reduction, per-block partials, and the last CTA sums the
+// partials in block order, so the result is deterministic (not bitwise equal to the
+// reference's serial sum: the summation order differs, rel. error ~1e-15).
+__device__ __forceinline__ double lumped_weight(int x, int y, int W, int H) {
+  int cnt = 0;  // incident triangles (mesh.cpp:122-126: area/3 each)
+  if (x > 0 && y > 0) cnt += 2;
+  if (x < W - 1 && y > 0) cnt += 1;
+  if (x > 0 && y < H - 1) cnt += 1;
+  if (x < W - 1 && y < H - 1) cnt += 2;
+  double s = 0.0;
+  for (int k = 0; k < cnt; ++k) s += 0.5 / 3.0;
+  return s;
+}
+
+__global__ void k_energy(const double* __restrict__ t10, const double* __restrict__ alpha,
+                         const double* __restrict__ lambda, const double* __restrict__ u3, int W,
+                         int H, int nc, double* __restrict__ part, double* __restrict__ out,
+                         unsigned* __restrict__ counter) {
+  const int cw = W - 1, ch = H - 1;
+  const size_t n = static_cast<size_t>(W) * H;
+  const double* u1 = u3;
+  const double* u2 = u3 + n;
+  const double* mt = u3 + 2 * n;
+  const long long ncell = static_cast<long long>(cw) * ch;
+  const long long nwork = ncell > static_cast<long long>(n) ? ncell : static_cast<long long>(n);
+  double eg = 0.0, ed = 0.0;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < nwork;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (i < ncell) {
+      const int x = static_cast<int>(i % cw), y = static_cast<int>(i / cw);
+#pragma unroll
+      for (int up = 0; up < 2; ++up) {
+        const Grad g = tri_grad(u1, u2, mt, W, x, y, up, nc);
+        double s = alpha[2 * i + up] * (g.g[0] * g.g[0] + g.g[1] * g.g[1] + g.g[2] * g.g[2] +
+                                        g.g[3] * g.g[3]);
+        if (nc == 3) s += lambda[2 * i + up] * (g.g[4] * g.g[4] + g.g[5] * g.g[5]);
+        eg += 0.5 * s;  // area 1/2
+      }
+    }
+    if (i < static_cast<long long>(n)) {
+      const int x = static_cast<int>(i % W), y = static_cast<int>(i / W);
+      // nodal_terms (assembly.cpp:19-28) and the reference's loop order
+      double A[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, F[3] = {0, 0, 0};
+      A[0] = t10[i], A[1] = t10[n + i], A[3] = t10[n + i], A[4] = t10[3 * n + i];
+      F[0] = t10[6 * n + i], F[1] = t10[7 * n + i];
+      if (nc == 3) {
+        A[2] = t10[2 * n + i], A[5] = t10[4 * n + i];
+        A[6] = t10[2 * n + i], A[7] = t10[4 * n + i], A[8] = t10[5 * n + i];
+        F[2] = t10[8 * n + i];
+      }
+      const double U[3] = {u1[i], u2[i], nc == 3 ? mt[i] : 0.0};
+      double quad = 0.0, lin = 0.0;
+      for (int c = 0; c < nc; ++c) {
+        for (int c2 = 0; c2 < nc; ++c2) quad += U[c] * A[c * 3 + c2] * U[c2];
+        lin += F[c] * U[c];
+      }
+      ed += lumped_weight(x, y, W, H) * (quad - 2.0 * lin + t10[9 * n + i]);
+    }
+  }
+  __shared__ double sm[2][32];
+  for (int off = 16; off; off >>= 1) {
+    eg += __shfl_xor_sync(~0u, eg, off);
+    ed += __shfl_xor_sync(~0u, ed, off);
+  }
+  if ((threadIdx.x & 31) == 0) sm[0][threadIdx.x >> 5] = eg, sm[1][threadIdx.x >> 5] = ed;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (blockDim.x >> 5); ++w) a += sm[0][w], b += sm[1][w];
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+    __threadfence();
+    const unsigned t = atomicAdd(counter, 1u);
+    if (t == gridDim.x - 1) {
+      double sg = 0.0, sd = 0.0;
+      for (unsigned k = 0; k < gridDim.x; ++k) sg += __ldcg(part + 2 * k), sd += __ldcg(part + 2 * k + 1);
+      *out = 0.5 * (sg + sd);
+      *counter = 0;
+    }
+  }
+}
+
 }  // namespace
+
+void energy(const double* t10, const double* alpha, const double* lambda, const double* u3,
+            int W, int H, int nc, double* out_dev, double* scratch, unsigned* counter,
+            cudaStream_t st) {
+  k_energy<<<kRedBlocks, kRedThreads, 0, st>>>(t10, alpha, lambda, u3, W, H, nc, scratch,
+                                               out_dev, counter);
+  FFB_LAUNCHED();
+}
 
 void error_indicator(const double* t10, const double* alpha, const double* lambda,
                      const double* u3, int W, int H, int nc, double* eta, double* eta_max_dev,

@@ -28,6 +28,8 @@
 // rows, producing the row dot products and, for the symmetric half, per-lane column partial
 // sums in registers, combined in a fixed order (deterministic).
 #include "ffb_internal.cuh"
+
+#include <mutex>
 #include "pivot.cuh"
 
 #include <algorithm>
@@ -1535,7 +1537,9 @@ __device__ __forceinline__ void st_async_to(uint32_t dst_cluster, double v, uint
                "d"(v), "r"(bar_cluster)
                : "memory");
 }
-// mbarrier wait that fails loudly instead of hanging: traps after ~4e9 cycles (~2 s)
+// mbarrier wait that fails loudly instead of hanging forever: traps after ~1e11 cycles
+// (~50 s at 1.965 GHz) — far beyond any legitimate wait, including time-slicing or compute
+// preemption by other tenants, so only a genuine deadlock ends there
 __device__ __forceinline__ void mbar_wait_g(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -1547,7 +1551,7 @@ __device__ __forceinline__ void mbar_wait_g(uint64_t* bar, uint32_t parity) {
       "@P1 bra DONEG_%=;\n"
       "mov.u64 t1, %%clock64;\n"
       "sub.s64 t1, t1, t0;\n"
-      "setp.lt.s64 P1, t1, 4000000000;\n"
+      "setp.lt.s64 P1, t1, 100000000000;\n"
       "@P1 bra WAITG_%=;\n"
       "trap;\n"
       "DONEG_%=:\n"
@@ -2022,6 +2026,7 @@ __global__ void k_changed_lines(const SubInfo* __restrict__ subs, const double* 
 
 void changed_lines(const SubInfo* d_subs, int nsub, const double* alpha, const double* alpha_fact,
                    int W, int H, int2* changed, cudaStream_t st) {
+  if (nsub <= 0) return;  // a rank without subdomains (world > parts)
   k_changed_lines<<<nsub, 256, 0, st>>>(d_subs, alpha, alpha_fact, W, H, changed);
   FFB_LAUNCHED();
 }
@@ -2030,6 +2035,7 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
                  const double* coef, size_t N, int W, int nc, double* fac, double* scratch,
                  long long scratch_stride, int* d_bad, cudaStream_t st, const int2* changed,
                  double* fac_t) {
+  if (nsub <= 0) return;  // a rank without subdomains (world > parts)
   const int kdp = (kd_max + 31) / 32 * 32;
   // schedule switches are read per call (tests switch them within one process)
   const int la = [] {
@@ -2154,19 +2160,25 @@ static unsigned char h_nloc[4][kTileMaxNt + 1][kTileMaxNt];
 static unsigned char h_owner[4][kTileMaxNt + 1][kTileMaxNt];
 static int h_stage[4][kTileMaxNt + 1];
 static void ensure_tile_tables_host() {
-  static bool built = false;
-  if (!built) build_tile_tables(h_tile_of, h_nloc, h_owner, h_stage), built = true;
+  static std::once_flag once;
+  std::call_once(once, [] { build_tile_tables(h_tile_of, h_nloc, h_owner, h_stage); });
 }
+// Uploaded once per device, under a lock (contexts may live on several host threads), and
+// followed by a device synchronisation: the solve kernels run on non-blocking streams, which
+// are not ordered after the legacy-stream symbol copies.
 static void set_tile_tables() {
-  static unsigned done_mask = 0;
+  static std::mutex mu;
+  static unsigned long long done_mask = 0;
   int dev = 0;
   FFB_CUDA(cudaGetDevice(&dev));
-  if (dev < 32 && (done_mask >> dev) & 1u) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && (done_mask >> dev) & 1ull) return;
   ensure_tile_tables_host();
   FFB_CUDA(cudaMemcpyToSymbol(c_tile_of, h_tile_of, sizeof(h_tile_of)));
   FFB_CUDA(cudaMemcpyToSymbol(c_nloc, h_nloc, sizeof(h_nloc)));
   FFB_CUDA(cudaMemcpyToSymbol(c_owner, h_owner, sizeof(h_owner)));
-  if (dev < 32) done_mask |= 1u << dev;
+  FFB_CUDA(cudaDeviceSynchronize());
+  if (dev < 64) done_mask |= 1ull << dev;
 }
 
 void set_solve_dbg(int v) { FFB_CUDA(cudaMemcpyToSymbol(g_solve_dbg, &v, sizeof(int))); }
@@ -2268,6 +2280,7 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
 void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,
                 const double* coef, size_t N, const double* r, double* ylocal, double* zlocal,
                 int W, int nc, const int* flags, cudaStream_t st, const double* rlocal) {
+  if (nsub <= 0) return;  // a rank without subdomains (world > parts)
   if (pl.maxm <= 4)
     launch_solve_m<4>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st);
   else if (pl.maxm <= 8)

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -117,15 +118,20 @@ struct ffb_ctx {
   DBuf<int> csr_rp, csr_ci, csr_perm, csr_iperm, csr_bad;
   DBuf<double> csr_v, csr_b, csr_x, csr_r, csr_z, csr_p, csr_Ap, csr_diag, csr_part, csr_AB;
   DBuf<CgCtl> cgctl;
+  // literal loop, CG subdomain mode: reference-order vectors + per-subdomain control blocks
+  DBuf<double> b_x, b_b, b_r, b_z, b_p, b_Ap, b_part;
+  DBuf<CgCtl> b_ctl;
   DBuf<double> alpha_fact;  // alpha of the resident factorisation (incremental refactor)
   DBuf<int2> d_changed;
   long long fact_key_t_full = -1;  // terms version / partition of the last full factorisation
   int fact_valid = 0;
   bool incremental = true;
   DBuf<int> d_bad;
-  double factor_doubles = 0, apply_doubles = 0, sum_n = 0;
-  // asm kernel timing
+  double factor_doubles = 0, apply_doubles = 0, sum_n = 0, factor_flops = 0;
+  // asm kernel timing: a pool of event pairs, created on first use and reused (no event
+  // creation inside a timed solve once the pool is warm)
   std::vector<EventPair> asm_events;
+  size_t asm_used = 0;
   double asm_ms_total = 0;
   long long asm_launches_timed = 0;
   bool time_asm = false;
@@ -261,7 +267,7 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
   c->s_lo = static_cast<int>(static_cast<long long>(c->shard_rank) * np / c->shard_world);
   c->s_hi = static_cast<int>(static_cast<long long>(c->shard_rank + 1) * np / c->shard_world);
   long long fac_off = 0, vec_off = 0;
-  double fd = 0, ad = 0, sn = 0;
+  double fd = 0, ad = 0, sn = 0, ff = 0;
   for (int p = 0; p < np; ++p) {
     SubInfo& s = c->subs[p];
     s.fx0 = fr[p].x0, s.fy0 = fr[p].y0, s.fw = fr[p].w(), s.fh = fr[p].h();
@@ -280,10 +286,12 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
     fac_off += (s.line_sz * s.L + 31) / 32 * 32;
     vec_off += (n + 31) / 32 * 32;
     fd += static_cast<double>(s.line_sz) * s.L;
+    ff += static_cast<double>(n) * s.kd * s.kd;  // 2 flops x n kd^2 / 2 FMAs
     ad += static_cast<double>(s.line_sz) * (2 * s.L - 1);  // forward all, backward L-1 lines
     sn += static_cast<double>(n);
   }
   c->factor_doubles = fd;
+  c->factor_flops = ff;
   c->apply_doubles = ad;
   c->sum_n = sn;
   // free-rectangle membership along each axis (free rect of part (i,j) = X_i x Y_j)
@@ -373,10 +381,13 @@ const double* solve_factor(const ffb_ctx* c) { return c->plan.tile ? c->fac_t.p 
 void launch_asm(ffb_ctx* c, int nc, const double* rvec, const int* flags) {
   EventPair* ev = nullptr;
   if (c->time_asm) {
-    c->asm_events.emplace_back();
-    ev = &c->asm_events.back();
-    FFB_CUDA(cudaEventCreate(&ev->a));
-    FFB_CUDA(cudaEventCreate(&ev->b));
+    if (c->asm_used == c->asm_events.size()) {
+      EventPair e;
+      FFB_CUDA(cudaEventCreate(&e.a));
+      FFB_CUDA(cudaEventCreate(&e.b));
+      c->asm_events.push_back(e);
+    }
+    ev = &c->asm_events[c->asm_used++];
     FFB_CUDA(cudaEventRecord(ev->a, c->st));
   }
   line_solve(c->d_subs.p + c->s_lo, c->s_hi - c->s_lo, c->plan, solve_factor(c), c->coef.p, c->N, rvec,
@@ -385,7 +396,8 @@ void launch_asm(ffb_ctx* c, int nc, const double* rvec, const int* flags) {
 }
 
 void harvest_asm_events(ffb_ctx* c) {
-  for (auto& e : c->asm_events) {
+  for (size_t k = 0; k < c->asm_used; ++k) {
+    const EventPair& e = c->asm_events[k];
     float ms = 0;
     FFB_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
     // kernels that returned at entry (converged) take ~2 us; count real applications only
@@ -393,10 +405,8 @@ void harvest_asm_events(ffb_ctx* c) {
       c->asm_ms_total += ms;
       c->asm_launches_timed++;
     }
-    cudaEventDestroy(e.a);
-    cudaEventDestroy(e.b);
   }
-  c->asm_events.clear();
+  c->asm_used = 0;
 }
 
 struct PcgResult {
@@ -490,13 +500,14 @@ void run_dev(ffb_ctx* c, int W, int H, const double* f0, const double* f1,
   const Split sp = choose_split(W, H, cfg->parts);
   ensure_partition(c, sp.px, sp.py, cfg->overlap, nc);
   FFB_CUDA(cudaEventRecord(ev[1], c->st));
-  const double alpha_th = cfg->alpha_th > 0 ? cfg->alpha_th : cfg->alpha0 / 100.0;
+  // alpha_th NaN = unset (std::optional, pipeline.cpp:71); explicit values, 0 included, are the floor
+  const double alpha_th = std::isnan(cfg->alpha_th) ? cfg->alpha0 / 100.0 : cfg->alpha_th;
   double* eh = c->eta_hist.ensure(FFB_MAX_SOLVES);
   double* eta = c->eta.ensure(c->ntri);
   double* blockmax = c->part.ensure(4 * kRedBlocks);
   unsigned* counter = c->counter.ensure(1);
   FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
-  double ms_factor = 0, ms_pcg = 0, ms_adapt = 0;
+  double ms_factor = 0, ms_pcg = 0, ms_adapt = 0, ms_factor0 = 0;
   long long total_it = 0;
   c->asm_ms_total = 0;
   c->asm_launches_timed = 0;
@@ -533,6 +544,7 @@ void run_dev(ffb_ctx* c, int W, int H, const double* f0, const double* f1,
     FFB_CUDA(cudaEventElapsedTime(&a, ev[2], ev[3]));
     FFB_CUDA(cudaEventElapsedTime(&b, ev[3], ev[4]));
     FFB_CUDA(cudaEventElapsedTime(&d, ev[4], ev[5]));
+    if (pass == 0) ms_factor0 = a;  // the full factorisation (later passes are incremental)
     ms_factor += a, ms_pcg += b, ms_adapt += d;
   }
   inter_to_planes(c->x.p, d_u3, static_cast<long long>(c->N), nc, c->st);
@@ -558,6 +570,8 @@ void run_dev(ffb_ctx* c, int W, int H, const double* f0, const double* f1,
     stats->iter_bytes = 8.0 * c->apply_doubles + (80.0 + 14.0 * 8.0 * nc) * c->N;
     stats->ms_asm_per_iter =
         c->asm_launches_timed ? c->asm_ms_total / c->asm_launches_timed : 0.0;
+    stats->ms_factor_full = ms_factor0;
+    stats->factor_flops = c->factor_flops;
   }
   for (auto& e : ev) cudaEventDestroy(e);
 }
@@ -583,7 +597,11 @@ int ffb_create(ffb_ctx** out, int device) {
     if (device < 0 || device >= n) fail("ffb: device index out of range");
     cudaDeviceProp prop{};
     FFB_CUDA(cudaGetDeviceProperties(&prop, device));
-    if (prop.major < 10) fail("ffb: requires an sm_100 (Blackwell) device");
+    // the library ships sm_100a cubins only (no PTX): refuse other devices up front instead of
+    // failing at the first launch with "no kernel image"
+    if (prop.major != 10 || prop.minor != 0)
+      fail("ffb: requires a compute capability 10.0 (B200, sm_100a) device; found " +
+           std::to_string(prop.major) + "." + std::to_string(prop.minor));
     auto c = std::make_unique<ffb_ctx>();
     c->device = device;
     FFB_CUDA(cudaSetDevice(device));
@@ -1061,22 +1079,27 @@ int ffb_device_buffer(ffb_ctx* c, int which, void** ptr, long long* n_doubles) {
 }
 
 // ---- the reference's literal Schwarz loop (schwarz.cpp:162-319) ----------------------
-int ffb_schwarz_solve(ffb_ctx* c, int n_iters, int nc, int adapt, int n_adapt, double kappa,
-                      double eta_thr, double alpha_th, int refine, double* u3,
-                      double* increments, double* eta_max) {
+int ffb_schwarz_run(ffb_ctx* c, const ffb_schwarz_options* o, double* u3, ffb_schwarz_stats* stats) {
   return guard([&] {
     check_ctx(c);
+    if (!o) fail("schwarz.schwarz_solve: null options");
+    const int nc = o->components, n_iters = o->n_iters;
     if (nc != 2 && nc != 3) fail("assembly.assemble: components must be 2 or 3");
     if (!c->alpha.p) fail("assembly.assemble: no regularization set");
     if (!c->have_part) fail("schwarz.schwarz_solve: no partition set");
     if (c->shard_world != 1) fail("schwarz.schwarz_solve: sharded context");
     if (n_iters < 0) fail("schwarz.schwarz_solve: n_iters must be >= 0");
+    if (o->method != FFB_SOLVE_CHOLESKY && o->method != FFB_SOLVE_CG)
+      fail("schwarz.schwarz_solve: unknown solver method");
+    const bool use_cg = o->method == FFB_SOLVE_CG;
     if (c->part_nc != nc) ensure_partition(c, c->part_px, c->part_py, c->part_ov, nc);
     ensure_coef(c, nc);
     ensure_rhs(c, nc);
     const size_t N = c->N;
     const int np = static_cast<int>(c->subs.size());
     const long long vec_len = c->ylocal.n;
+    int max_n = 0;
+    for (const SubInfo& sd : c->subs) max_n = std::max(max_n, sd.n);
     double* rl = c->rlocal.ensure(vec_len);
     double* xl = c->xlocal.ensure(vec_len);
     double* G = c->G0.ensure(3 * N);
@@ -1086,6 +1109,24 @@ int ffb_schwarz_solve(ffb_ctx* c, int n_iters, int nc, int adapt, int n_adapt, d
     double* eta = c->eta.ensure(c->ntri);
     double* blockmax = c->part.ensure(4 * kRedBlocks);
     unsigned* counter = c->counter.ensure(1);
+    // CG mode: persistent warm start x_prev (schwarz.cpp:250-253), reference-order vectors
+    const int maxch = ras_cg_chunks(max_n);
+    double *bx = nullptr, *bb = nullptr, *br = nullptr, *bz = nullptr, *bp = nullptr,
+           *bAp = nullptr, *bpart = nullptr;
+    CgCtl* bctl = nullptr;
+    std::vector<CgCtl> hctl;
+    if (use_cg) {
+      bx = c->b_x.ensure(vec_len);
+      bb = c->b_b.ensure(vec_len);
+      br = c->b_r.ensure(vec_len);
+      bz = c->b_z.ensure(vec_len);
+      bp = c->b_p.ensure(vec_len);
+      bAp = c->b_Ap.ensure(vec_len);
+      bpart = c->b_part.ensure(static_cast<size_t>(maxch) * np);
+      bctl = c->b_ctl.ensure(np);
+      hctl.resize(np);
+      FFB_CUDA(cudaMemsetAsync(bx, 0, vec_len * sizeof(double), c->st));  // no x_prev yet
+    }
     FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
     FFB_CUDA(cudaMemsetAsync(G, 0, 3 * N * sizeof(double), c->st));  // G = 0 (schwarz.cpp:190)
     // owner (core) of every column / row (schwarz.cpp:87-91)
@@ -1102,42 +1143,138 @@ int ffb_schwarz_solve(ffb_ctx* c, int n_iters, int nc, int adapt, int n_adapt, d
                                cudaMemcpyHostToDevice, c->st));
       sync(c);
     }
+    const int n_adapt = o->adapt ? std::max(0, o->n_adapt) : 0;
     int n_upd = 0;
     for (int iter = 0; iter < n_iters; ++iter) {
+      const auto t0 = std::chrono::steady_clock::now();
       ensure_coef(c, nc);
-      ensure_factor(c, nc);  // refactors iff alpha changed (schwarz.cpp:238-241)
       ras_rhs(c->d_subs.p, np, c->coef.p, c->b.p, G, N, c->W, c->H, nc, rl, c->st);
-      line_solve(c->d_subs.p, np, c->plan, solve_factor(c), c->coef.p, N, nullptr, c->ylocal.p,
-                 c->zlocal.p, c->W, nc, nullptr, c->st, rl);
       const double* dl = nullptr;
-      if (refine) {  // x += A^-1 (rhs - A x)   (schwarz.cpp:242-247)
+      if (use_cg) {  // cg_solve per subdomain, warm-started from x_prev (schwarz.cpp:248-252)
+        ras_perm(c->d_subs.p, np, nc, rl, bb, 1, c->st);
+        ras_cg_begin(c->d_subs.p, np, maxch, c->coef.p, N, c->W, nc, o->cg_tolerance,
+                     o->cg_max_iters, bb, bx, br, bz, bp, bAp, bpart, bctl, c->st);
+        for (;;) {
+          FFB_CUDA(cudaMemcpyAsync(hctl.data(), bctl, np * sizeof(CgCtl), cudaMemcpyDeviceToHost,
+                                   c->st));
+          sync(c);
+          bool all = true;
+          for (const CgCtl& h : hctl) all = all && h.done;
+          if (all) break;
+          ras_cg_iterations(c->d_subs.p, np, maxch, c->coef.p, N, c->W, nc, 16, bx, br, bz, bp,
+                            bAp, bpart, bctl, c->st);
+        }
+        for (const CgCtl& h : hctl) {
+          if (h.err == 2)
+            fail("linsolve.cg: indefinite matrix detected at iteration " + std::to_string(h.it));
+          if (!h.zero && h.res > o->cg_tolerance)
+            fail("linsolve.cg: no convergence after " + std::to_string(h.it) +
+                 " iterations, relative residual " + std::to_string(h.res));
+        }
+        ras_cg_zero(c->d_subs.p, np, bx, bctl, c->st);
+        ras_perm(c->d_subs.p, np, nc, bx, xl, 0, c->st);
+      } else {
+        ensure_factor(c, nc);  // refactors iff alpha changed (schwarz.cpp:238-241)
+        line_solve(c->d_subs.p, np, c->plan, solve_factor(c), c->coef.p, N, nullptr, c->ylocal.p,
+                   c->zlocal.p, c->W, nc, nullptr, c->st, rl);
+        // x += A^-1 (rhs - A x): one step of iterative refinement (schwarz.cpp:242-247)
         vec_copy(xl, c->zlocal.p, vec_len, c->st);
         ras_residual(c->d_subs.p, np, c->coef.p, N, c->W, nc, rl, xl, rl, c->st);
         line_solve(c->d_subs.p, np, c->plan, solve_factor(c), c->coef.p, N, nullptr, c->ylocal.p,
                    c->zlocal.p, c->W, nc, nullptr, c->st, rl);
         dl = c->zlocal.p;
-      } else {
-        vec_copy(xl, c->zlocal.p, vec_len, c->st);
       }
       ras_compose(c->own_col.p, c->own_row.p, c->d_subs.p, c->part_px, xl, dl, G, Gn, c->W, c->H,
                   nc, blockmax, inc + iter, counter, c->st);
       std::swap(G, Gn);
-      if (adapt && iter < n_adapt) {  // schwarz.cpp:303-311
+      if (iter < n_adapt) {  // schwarz.cpp:303-311
         double* u = c->work.ensure(3 * N);
         inter_to_planes(G, u, static_cast<long long>(N), nc, c->st);
         error_indicator(c->t10.p, c->alpha.p, c->lambda.p, u, c->W, c->H, nc, eta, em + n_upd,
                         blockmax, counter, c->st);
-        update_alpha(c->alpha.p, c->alpha.p, eta, em + n_upd, c->ntri, kappa, eta_thr, alpha_th,
-                     c->st);
+        update_alpha(c->alpha.p, c->alpha.p, eta, em + n_upd, c->ntri, o->kappa,
+                     o->eta_threshold, o->alpha_th, c->st);
         c->alpha_version++;
+        if (stats && stats->alpha_history && o->record_alpha_history)
+          download(stats->alpha_history + static_cast<size_t>(n_upd) * c->ntri, c->alpha.p,
+                   c->ntri, c->st);
         ++n_upd;
+      }
+      if (stats && stats->seconds) {  // wall time per iteration (schwarz.cpp:312-316)
+        sync(c);
+        stats->seconds[iter] =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       }
     }
     double* u = c->work.ensure(3 * N);
     inter_to_planes(G, u, static_cast<long long>(N), nc, c->st);
     if (u3) download(u3, u, 3 * N, c->st);
-    if (increments && n_iters > 0) download(increments, inc, n_iters, c->st);
-    if (eta_max && n_upd > 0) download(eta_max, em, n_upd, c->st);
+    if (stats && stats->increments && n_iters > 0) download(stats->increments, inc, n_iters, c->st);
+    if (stats && stats->eta_max && n_upd > 0) download(stats->eta_max, em, n_upd, c->st);
+    if (stats) stats->n_updates = n_upd;
+    sync(c);
+  });
+}
+
+int ffb_schwarz_solve(ffb_ctx* c, int n_iters, int nc, int adapt, int n_adapt, double kappa,
+                      double eta_thr, double alpha_th, int refine, double* u3,
+                      double* increments, double* eta_max) {
+  if (!refine) {
+    g_err = "schwarz.schwarz_solve: the Cholesky subdomain path always refines (schwarz.cpp:242-247)";
+    return 1;
+  }
+  ffb_schwarz_options o{};
+  o.n_iters = n_iters, o.workers = 1, o.components = nc, o.adapt = adapt, o.n_adapt = n_adapt;
+  o.kappa = kappa, o.eta_threshold = eta_thr, o.alpha_th = alpha_th;
+  o.method = FFB_SOLVE_CHOLESKY, o.cg_tolerance = 1e-10;
+  ffb_schwarz_stats st{};
+  st.increments = increments, st.eta_max = eta_max;
+  return ffb_schwarz_run(c, &o, u3, &st);
+}
+
+// energy (assembly.cpp:201-238) of a host state, as a device reduction
+int ffb_energy(ffb_ctx* c, int W, int H, const double* t10, const double* alpha,
+               const double* lambda, const double* u3, int nc, double* e) {
+  return guard([&] {
+    check_ctx(c);
+    if (nc != 2 && nc != 3) fail("assembly.energy: components must be 2 or 3");
+    check_dims(W, H, "mesh.build_pixel_mesh");
+    if (!e) fail("assembly.energy: null output");
+    set_problem(c, W, H);
+    const size_t N = c->N;
+    upload(c->t10.ensure(10 * N), t10, 10 * N, c->st);
+    c->terms_version++;
+    ensure_reg(c);
+    upload(c->alpha.p, alpha, c->ntri, c->st);
+    upload(c->lambda.p, lambda, c->ntri, c->st);
+    c->alpha_version++;
+    c->fact_valid = 0;
+    double* u = c->work.ensure(3 * N);
+    upload(u, u3, 3 * N, c->st);
+    double* out = c->eta_hist.ensure(FFB_MAX_SOLVES);
+    unsigned* counter = c->counter.ensure(1);
+    FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
+    energy(c->t10.p, c->alpha.p, c->lambda.p, u, W, H, nc, out, c->part.ensure(4 * kRedBlocks),
+           counter, c->st);
+    download(e, out, 1, c->st);
+    sync(c);
+  });
+}
+
+// energy of the resident solution (the last solve's x) with the resident terms and reg
+int ffb_energy_resident(ffb_ctx* c, int nc, double* e) {
+  return guard([&] {
+    check_ctx(c);
+    if (!c->x.p || !c->alpha.p || !c->t10.p) fail("assembly.energy: no solution on the device");
+    if (!e) fail("assembly.energy: null output");
+    double* u = c->work.ensure(3 * c->N);
+    inter_to_planes(c->x.p, u, static_cast<long long>(c->N), nc, c->st);
+    double* out = c->eta_hist.ensure(FFB_MAX_SOLVES);
+    unsigned* counter = c->counter.ensure(1);
+    FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
+    energy(c->t10.p, c->alpha.p, c->lambda.p, u, c->W, c->H, nc, out,
+           c->part.ensure(4 * kRedBlocks), counter, c->st);
+    download(e, out, 1, c->st);
     sync(c);
   });
 }

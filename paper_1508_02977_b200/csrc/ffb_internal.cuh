@@ -109,6 +109,20 @@ void ras_compose(const int* own_col, const int* own_row, const SubInfo* d_subs, 
                  const double* xl, const double* dl, const double* G, double* Gnew, int W, int H,
                  int nc, double* blockmax, double* inc_out, unsigned* counter, cudaStream_t st);
 void vec_copy(double* dst, const double* src, long long n, cudaStream_t st);
+// CG subdomain solves of the literal loop (SolveMethod::ConjugateGradient,
+// schwarz.cpp:248-252): the reference's cg_solve per subdomain, all subdomains in lockstep,
+// vectors in the reference's unknown order (ras_perm converts from / to the line layout)
+struct CgCtl;
+void ras_perm(const SubInfo* d_subs, int nsub, int nc, const double* src, double* dst, int to_ref,
+              cudaStream_t st);
+int ras_cg_chunks(int max_n);
+void ras_cg_begin(const SubInfo* d_subs, int nsub, int maxch, const double* coef, size_t N, int W,
+                  int nc, double tol, long long max_iters, const double* b, double* x, double* r,
+                  double* z, double* p, double* Ap, double* partial, CgCtl* ctl, cudaStream_t st);
+void ras_cg_iterations(const SubInfo* d_subs, int nsub, int maxch, const double* coef, size_t N,
+                       int W, int nc, int k, double* x, double* r, double* z, double* p,
+                       double* Ap, double* partial, CgCtl* ctl, cudaStream_t st);
+void ras_cg_zero(const SubInfo* d_subs, int nsub, double* x, const CgCtl* ctl, cudaStream_t st);
 
 // ---- PCG control block (solver.cu) ----------------------------------------------------
 struct PcgCtl {
@@ -143,6 +157,11 @@ void error_indicator(const double* t10, const double* alpha, const double* lambd
 void update_alpha(double* alpha_out, const double* alpha, const double* eta,
                   const double* eta_max_dev, long long ntri, double kappa, double thr,
                   double alpha_th, cudaStream_t st);
+
+// a25 energy (assembly.cpp:201-238): scratch >= 2 * kRedBlocks doubles, counter zeroed
+void energy(const double* t10, const double* alpha, const double* lambda, const double* u3,
+            int W, int H, int nc, double* out_dev, double* scratch, unsigned* counter,
+            cudaStream_t st);
 
 // reductions
 constexpr int kRedBlocks = 592;  // 4 x 148 SMs

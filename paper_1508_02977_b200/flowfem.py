@@ -617,18 +617,24 @@ class SchwarzSolver:
 @dataclass
 class SchwarzOptions:
     """schwarz.hpp:59-66 (workers only affects CPU threading in the reference and is accepted
-    for signature compatibility)."""
+    for signature compatibility). ``solver.method`` picks the subdomain solver: DirectCholesky
+    (device factorisation + one refinement step) or ConjugateGradient (the reference's
+    Jacobi-PCG per subdomain, warm-started, bitwise equal to the reference's)."""
     n_iters: int = 10
     workers: int = 1
     components: int = 3
     adapt: AdaptConfig = field(default_factory=AdaptConfig)
-    refine: bool = True
+    solver: SolverConfig = field(default_factory=SolverConfig)
+    record_alpha_history: bool = False
 
 
 @dataclass
 class SchwarzStats:
-    increments: List[float]
-    eta_max: List[float]
+    """schwarz.hpp:68-73."""
+    increments: List[float] = field(default_factory=list)
+    seconds: List[float] = field(default_factory=list)
+    eta_max: List[float] = field(default_factory=list)
+    alpha_history: List[np.ndarray] = field(default_factory=list)
 
 
 def schwarz_solve(terms: DataTerms, reg: RegField, parts_x: int, parts_y: int, overlap: int,
@@ -645,16 +651,46 @@ def schwarz_solve(terms: DataTerms, reg: RegField, parts_x: int, parts_y: int, o
     _check(lib.ffb_set_reg(ctx.handle, _p(reg.alpha), _p(_f64(reg.lambda_))))
     _check(lib.ffb_set_partition(ctx.handle, parts_x, parts_y, overlap))
     u3 = np.zeros((3, H, W))
-    inc = np.zeros(max(opt.n_iters, 1))
+    n = max(opt.n_iters, 1)
+    inc, sec = np.zeros(n), np.zeros(n)
     a = opt.adapt
     n_upd = min(a.n_adapt, opt.n_iters) if a.enabled else 0
     em = np.zeros(max(n_upd, 1))
-    _check(lib.ffb_schwarz_solve(ctx.handle, opt.n_iters, opt.components, int(a.enabled),
-                                 a.n_adapt, float(a.kappa), float(a.eta_threshold),
-                                 float(a.alpha_th), int(opt.refine), _p(u3), _p(inc), _p(em)))
+    ntri = 2 * (W - 1) * (H - 1)
+    hist = np.zeros((max(n_upd, 1), ntri)) if opt.record_alpha_history else None
+    o = _lib.SchwarzOptionsC(opt.n_iters, opt.workers, opt.components, int(a.enabled),
+                             a.n_adapt, float(a.kappa), float(a.eta_threshold), float(a.alpha_th),
+                             int(opt.solver.method), int(opt.solver.cg_max_iters),
+                             float(opt.solver.cg_tolerance), int(opt.record_alpha_history))
+    st = _lib.SchwarzStatsC(inc.ctypes.data, sec.ctypes.data, em.ctypes.data,
+                            hist.ctypes.data if hist is not None else None, 0)
+    _check(lib.ffb_schwarz_run(ctx.handle, C.byref(o), _p(u3), C.byref(st)))
     if a.enabled:
         _check(lib.ffb_get_reg(ctx.handle, _p(reg.alpha), None))
-    return FlowState.from_planes(u3), SchwarzStats(list(inc[:opt.n_iters]), list(em[:n_upd]))
+    stats = SchwarzStats(list(inc[:opt.n_iters]), list(sec[:opt.n_iters]), list(em[:st.n_updates]),
+                         [hist[k].copy() for k in range(st.n_updates)] if hist is not None else [])
+    return FlowState.from_planes(u3), stats
+
+
+def energy(terms: DataTerms, reg: RegField, state: FlowState, components: int = 3,
+           ctx: Context | None = None) -> float:
+    """energy (assembly.hpp:70-73, assembly.cpp:201-238): the discrete energy whose gradient
+    is A x - b; a deterministic device reduction."""
+    ctx = ctx or default_context()
+    t = terms.planes
+    _, H, W = t.shape
+    e = C.c_double()
+    _check(ctx.lib.ffb_energy(ctx.handle, W, H, _p(t), _p(_f64(reg.alpha)), _p(_f64(reg.lambda_)),
+                              _p(_f64(state.planes())), components, C.byref(e)))
+    return e.value
+
+
+def resident_energy(components: int = 3, ctx: Context | None = None) -> float:
+    """energy of the context's resident solution (the last solve) at the resident alpha."""
+    ctx = ctx or default_context()
+    e = C.c_double()
+    _check(ctx.lib.ffb_energy_resident(ctx.handle, components, C.byref(e)))
+    return e.value
 
 
 # ------------------------------------------------------------------------- pipeline
@@ -680,7 +716,7 @@ class RunConfig:
         return _lib.RunConfigC(self.sigma, self.rho, self.alpha0, self.lambda0,
                                int(self.illumination), self.parts, self.overlap, int(self.adapt),
                                self.adapt_iters, self.kappa, self.eta_threshold,
-                               -1.0 if self.alpha_th is None else self.alpha_th,
+                               float("nan") if self.alpha_th is None else self.alpha_th,
                                self.cg_tolerance, self.max_iters)
 
 
@@ -700,6 +736,8 @@ class RunStats:
     factor_doubles: float
     iter_bytes: float
     ms_asm_per_iter: float
+    ms_factor_full: float = 0.0
+    factor_flops: float = 0.0
 
     @staticmethod
     def from_c(s: _lib.RunStatsC, n_passes: int):
@@ -707,7 +745,7 @@ class RunStats:
         return RunStats(s.parts_x, s.parts_y, list(s.iters[:n]), list(s.residual[:n]),
                         list(s.eta_max[:max(n - 1, 0)]), s.pcg_iterations, s.ms_terms,
                         s.ms_factor, s.ms_pcg, s.ms_adapt, s.ms_total, s.factor_doubles,
-                        s.iter_bytes, s.ms_asm_per_iter)
+                        s.iter_bytes, s.ms_asm_per_iter, s.ms_factor_full, s.factor_flops)
 
 
 @dataclass

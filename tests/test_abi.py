@@ -24,7 +24,7 @@ def test_library_exports_all_symbols():
     lib = _lib.load()
     for name in header_symbols():
         assert hasattr(lib, name), name
-    assert lib.ffb_abi_version() == 1
+    assert lib.ffb_abi_version() == 2
 
 
 def test_library_is_sm100a_cuda():
