@@ -30,6 +30,7 @@ CU = {
     "adapt.cu": ["--fmad=false"],
     "band.cu": ["-Xptxas", "-v"] if os.environ.get("FFB_PTXAS_V") else [],
     "pcg.cu": [],
+    "coarse.cu": [],
     "ras.cu": ["--fmad=false"],
     "linsolve.cu": ["--fmad=false"],
     "metrics.cu": ["--fmad=false"],

@@ -114,6 +114,12 @@ struct ffb_ctx {
   DBuf<AxisMap> d_col, d_row;
   DBuf<double> fac, fac_t, dscratch, ylocal, zlocal, rlocal, xlocal, G0, G1, incs;
   DBuf<int> own_col, own_row;
+  // two-level coarse space (coarse.cu): core cuts, coarse node maps, A0 band + inverse
+  bool coarse = true;
+  int cbw = 0, n0 = 0, coarse_nc = 0;
+  long long coarse_key_a = -1, coarse_key_t = -1;
+  DBuf<int> d_xs, d_ys, d_ccol, d_crow, d_cbad;
+  DBuf<double> cAB, cAinv, cgv, cyv;
   // linsolve boundary on an explicit CSR system (ffb_csr_*)
   DBuf<int> csr_rp, csr_ci, csr_perm, csr_iperm, csr_bad;
   DBuf<double> csr_v, csr_b, csr_x, csr_r, csr_z, csr_p, csr_Ap, csr_diag, csr_part, csr_AB;
@@ -333,6 +339,36 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
   c->ylocal.ensure(vec_off);
   c->zlocal.ensure(vec_off);
   c->d_bad.ensure(np);
+  // coarse space: core cuts and the coarse node of every pixel's core, the shorter subdomain
+  // axis fastest (A0's bandwidth is then nc * min(px, py))
+  {
+    // opt-in (FFB_COARSE=1): measured to cost iterations on every config (c4 400 -> 488,
+    // c3 260 -> 338, c2 176 -> 226, c5 214 -> 259; profiles/r2_coarse_space.txt)
+    const char* e = std::getenv("FFB_COARSE");
+    c->coarse = e && std::atoi(e) == 1;
+    c->coarse_key_a = c->coarse_key_t = -1;
+    const Partition& P = c->decomp;
+    std::vector<int> ccol(W), crow(H);
+    const bool yfast = py <= px;
+    for (int x = 0; x < W; ++x) {
+      const int ix = int(std::upper_bound(P.xs.begin(), P.xs.end(), x) - P.xs.begin()) - 1;
+      ccol[x] = yfast ? ix * py : ix;
+    }
+    for (int y = 0; y < H; ++y) {
+      const int iy = int(std::upper_bound(P.ys.begin(), P.ys.end(), y) - P.ys.begin()) - 1;
+      crow[y] = yfast ? iy : iy * px;
+    }
+    c->cbw = nc * (yfast ? py : px);
+    c->n0 = nc * np;
+    FFB_CUDA(cudaMemcpyAsync(c->d_xs.ensure(px + 1), P.xs.data(), (px + 1) * sizeof(int),
+                             cudaMemcpyHostToDevice, c->st));
+    FFB_CUDA(cudaMemcpyAsync(c->d_ys.ensure(py + 1), P.ys.data(), (py + 1) * sizeof(int),
+                             cudaMemcpyHostToDevice, c->st));
+    FFB_CUDA(cudaMemcpyAsync(c->d_ccol.ensure(W), ccol.data(), W * sizeof(int),
+                             cudaMemcpyHostToDevice, c->st));
+    FFB_CUDA(cudaMemcpyAsync(c->d_crow.ensure(H), crow.data(), H * sizeof(int),
+                             cudaMemcpyHostToDevice, c->st));
+  }
   sync(c);
   c->have_part = true;
   c->part_px = px, c->part_py = py, c->part_ov = ov, c->part_nc = nc;
@@ -372,6 +408,43 @@ void ensure_factor(ffb_ctx* c, int nc) {
   c->factor_key_a = c->alpha_version;
   c->factor_key_t = c->terms_version;
   c->fact_valid = 1;
+}
+
+// A0 = Z^T A Z of the current operator, factored and inverted on the device (coarse.cu)
+void ensure_coarse(ffb_ctx* c, int nc) {
+  if (!c->coarse) return;
+  if (c->coarse_key_a == c->alpha_version && c->coarse_key_t == c->terms_version &&
+      c->coarse_nc == nc)
+    return;
+  ensure_coef(c, nc);
+  const int px = c->part_px, py = c->part_py;
+  c->n0 = nc * px * py;
+  c->cbw = nc * std::min(px, py);
+  int* bad = c->d_cbad.ensure(1);
+  FFB_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(int), c->st));
+  coarse_build(c->coef.p, c->W, c->H, nc, c->d_xs.p, c->d_ys.p, px, py, c->d_ccol.p, c->d_crow.p,
+               c->cbw, c->cAB.ensure(static_cast<size_t>(c->n0) * (c->cbw + 1)),
+               c->cAinv.ensure(static_cast<size_t>(c->n0) * c->n0), bad, c->st);
+  c->cgv.ensure(c->n0);
+  c->cyv.ensure(c->n0);
+  int hbad = -1;
+  FFB_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  if (hbad >= 0)
+    fail("linsolve.cholesky: breakdown at pivot " + std::to_string(hbad) +
+         " of the coarse problem: matrix is not positive definite");
+  c->coarse_key_a = c->alpha_version;
+  c->coarse_key_t = c->terms_version;
+  c->coarse_nc = nc;
+}
+
+// y = A0^-1 Z^T r for the combine kernel (nullptr without a coarse space; in a sharded solve
+// only rank 0 adds it, the all-reduce of z then carries it to every rank)
+const double* coarse_term(ffb_ctx* c, int nc, const double* r, const PcgCtl* ctl) {
+  if (!c->coarse || c->shard_rank != 0) return nullptr;
+  coarse_apply(r, c->W, nc, c->d_xs.p, c->d_ys.p, c->part_px, c->part_py, c->d_ccol.p,
+               c->d_crow.p, c->cAinv.p, c->cgv.p, c->cyv.p, ctl, c->st);
+  return c->cyv.p;
 }
 
 // the factor layout the subdomain solve streams: the tile-major copy for the register-tiled
@@ -419,6 +492,7 @@ PcgResult pcg(ffb_ctx* c, int nc, double tol, int max_iters, bool warm) {
   ensure_coef(c, nc);
   ensure_rhs(c, nc);
   ensure_factor(c, nc);
+  ensure_coarse(c, nc);
   const size_t N = c->N;
   const long long nvec = static_cast<long long>(N) * nc;
   double* x = c->x.ensure(3 * N);
@@ -441,7 +515,7 @@ PcgResult pcg(ffb_ctx* c, int nc, double tol, int max_iters, bool warm) {
   launch_asm(c, nc, r, flags);
   if (c->shard_world != 1) fail("schwarz.schwarz_solve: sharded context: use the staged solve");
   pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, px, c->zlocal.p, r, z, c->W, c->H, ctl,
-              part, 0, c->s_hi, 0, c->st);
+              part, 0, c->s_hi, 0, c->st, coarse_term(c, nc, r, ctl), c->d_ccol.p, c->d_crow.p);
   const int chunk = 8;
   for (;;) {
     for (int it = 0; it < chunk; ++it) {
@@ -449,7 +523,8 @@ PcgResult pcg(ffb_ctx* c, int nc, double tol, int max_iters, bool warm) {
       pcg_update(nc, x, r, P0, P1, q, nvec, max_iters, ctl, part, c->st);
       launch_asm(c, nc, r, flags);
       pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, px, c->zlocal.p, r, z, c->W, c->H,
-                  ctl, part, 0, c->s_hi, 0, c->st);
+                  ctl, part, 0, c->s_hi, 0, c->st, coarse_term(c, nc, r, ctl), c->d_ccol.p,
+                  c->d_crow.p);
     }
     FFB_CUDA(cudaMemcpyAsync(c->h_ctl, ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, c->st));
     sync(c);
@@ -967,6 +1042,7 @@ int ffb_pcg_begin(ffb_ctx* c, int nc, double tol, int max_iters, int warm, const
     ensure_coef(c, nc);
     ensure_rhs(c, nc);
     ensure_factor(c, nc);
+    ensure_coarse(c, nc);
     const size_t N = c->N;
     const long long nvec = static_cast<long long>(N) * nc;
     double* x = c->x.ensure(3 * N);
@@ -995,7 +1071,8 @@ int ffb_pcg_begin(ffb_ctx* c, int nc, double tol, int max_iters, int warm, const
     pcg_init(nc, c->coef.p, c->b.p, x, r, c->W, c->H, ctl, part, c->st);
     launch_asm(c, nc, r, &ctl->done);
     pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, c->part_px, c->zlocal.p, r, z, c->W, c->H,
-                ctl, part, c->s_lo, c->s_hi, 1, c->st);
+                ctl, part, c->s_lo, c->s_hi, 1, c->st, coarse_term(c, nc, r, ctl), c->d_ccol.p,
+                c->d_crow.p);
   });
 }
 
@@ -1013,7 +1090,8 @@ int ffb_pcg_stage(ffb_ctx* c, int stage) {
                  c->st);
       launch_asm(c, nc, c->r.p, &ctl->done);
       pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, c->part_px, c->zlocal.p, c->r.p, c->z.p,
-                  c->W, c->H, ctl, part, c->s_lo, c->s_hi, 1, c->st);
+                  c->W, c->H, ctl, part, c->s_lo, c->s_hi, 1, c->st,
+                  coarse_term(c, nc, c->r.p, ctl), c->d_ccol.p, c->d_crow.p);
     } else if (stage == 1) {  // B: r.z of the all-reduced z
       pcg_rz(c->r.p, c->z.p, nvec, ctl, part, c->st);
     } else {

@@ -141,7 +141,19 @@ void pcg_init(int nc, const double* coef, const double* b, const double* x, doub
               int H, PcgCtl* ctl, double* part, cudaStream_t st);
 void pcg_combine(int nc, const SubInfo* subs, const AxisMap* colmap, const AxisMap* rowmap,
                  int px, const double* zlocal, const double* r, double* z, int W, int H,
-                 PcgCtl* ctl, double* part, int s_lo, int s_hi, int partial, cudaStream_t st);
+                 PcgCtl* ctl, double* part, int s_lo, int s_hi, int partial, cudaStream_t st,
+                 const double* yc = nullptr, const int* ccol = nullptr,
+                 const int* crow = nullptr);
+
+// ---- two-level coarse space (coarse.cu) ---------------------------------------------------
+// xs[px+1], ys[py+1]: core cuts; ccol[W] + crow[H]: coarse node of the core of pixel (x,y);
+// AB: (nc px py) x (bw+1) band scratch; Ainv: n0 x n0; bad: Cholesky breakdown (-1 none)
+void coarse_build(const double* coef, int W, int H, int nc, const int* xs, const int* ys, int px,
+                  int py, const int* ccol, const int* crow, int bw, double* AB, double* Ainv,
+                  int* bad, cudaStream_t st);
+void coarse_apply(const double* r, int W, int nc, const int* xs, const int* ys, int px, int py,
+                  const int* ccol, const int* crow, const double* Ainv, double* g, double* y,
+                  const PcgCtl* ctl, cudaStream_t st);
 void pcg_rz(const double* r, const double* z, long long nvec, PcgCtl* ctl, double* part,
             cudaStream_t st);
 void pcg_spmv_p(int nc, const double* coef, const double* z, double* P0, double* P1, double* q,

@@ -167,7 +167,9 @@ __global__ void __launch_bounds__(T) k_combine(const SubInfo* __restrict__ subs,
                                                const double* __restrict__ r,
                                                double* __restrict__ z, int W, int H,
                                                PcgCtl* ctl, double* part, int s_lo, int s_hi,
-                                               int partial) {
+                                               int partial, const double* __restrict__ yc,
+                                               const int* __restrict__ ccol,
+                                               const int* __restrict__ crow) {
   if (ctl->done | ctl->err) return;
   __shared__ double sm[32];
   const size_t n = static_cast<size_t>(W) * H;
@@ -196,6 +198,11 @@ __global__ void __launch_bounds__(T) k_combine(const SubInfo* __restrict__ subs,
 #pragma unroll
         for (int c = 0; c < NC; ++c) acc[c] += zl[c];
       }
+    }
+    if (yc) {  // two-level: + Z A0^-1 Z^T r (coarse.cu), the core's coarse value
+      const double* yv = yc + static_cast<long long>(ccol[x] + crow[y]) * NC;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) acc[c] += yv[c];
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -359,13 +366,14 @@ void pcg_init(int nc, const double* coef, const double* b, const double* x, doub
 
 void pcg_combine(int nc, const SubInfo* subs, const AxisMap* colmap, const AxisMap* rowmap,
                  int px, const double* zlocal, const double* r, double* z, int W, int H,
-                 PcgCtl* ctl, double* part, int s_lo, int s_hi, int partial, cudaStream_t st) {
+                 PcgCtl* ctl, double* part, int s_lo, int s_hi, int partial, cudaStream_t st,
+                 const double* yc, const int* ccol, const int* crow) {
   if (nc == 3)
     k_combine<3><<<kRedBlocks, T, 0, st>>>(subs, colmap, rowmap, px, zlocal, r, z, W, H, ctl, part,
-                                           s_lo, s_hi, partial);
+                                           s_lo, s_hi, partial, yc, ccol, crow);
   else
     k_combine<2><<<kRedBlocks, T, 0, st>>>(subs, colmap, rowmap, px, zlocal, r, z, W, H, ctl, part,
-                                           s_lo, s_hi, partial);
+                                           s_lo, s_hi, partial, yc, ccol, crow);
   FFB_LAUNCHED();
 }
 
