@@ -140,6 +140,29 @@ int ffb_csr_solve(ffb_ctx* ctx, int n, int components, const int* row_ptr, const
                   const double* vals, const double* rhs, int method, double tol, int max_iters,
                   const double* warm, double* x, int* iters, double* res);
 
+/* assemble (assembly.hpp:59-61, assembly.cpp:32-166) as an explicit CSR SparseSystem with an
+ * optional Dirichlet set (n_dir vertices, nc values each): pattern on the host, values and the
+ * eliminated right-hand side from the device operator, bitwise equal to the reference. Call
+ * with row_ptr == NULL for n and nnz, then with row_ptr[n+1], cols[nnz], vals[nnz], rhs[n]
+ * and (optional) vert_to_free[W*H], free_to_vert[n/nc]. */
+int ffb_assemble_system(ffb_ctx* ctx, int W, int H, const double* t10, const double* alpha,
+                        const double* lambda, int nc, int n_dir, const int* dir_vertices,
+                        const double* dir_values, int* n, long long* nnz, int* row_ptr,
+                        int* cols, double* vals, double* rhs, int* vert_to_free,
+                        int* free_to_vert);
+/* SparseCholesky (linsolve.hpp:32-48): analyze = the reference's RCM order (bit-exact) + band
+ * width; factorize = band Cholesky of the permuted matrix on the device ("linsolve.cholesky:
+ * breakdown at pivot k (unknown u): matrix is not positive definite"); solve = permuted
+ * substitutions on the device. Handles belong to a context. */
+typedef struct ffb_chol ffb_chol;
+int ffb_chol_create(ffb_ctx* ctx, ffb_chol** chol);
+int ffb_chol_destroy(ffb_chol* chol);
+int ffb_chol_analyze(ffb_chol* chol, int n, int components, const int* row_ptr, const int* cols);
+int ffb_chol_factorize(ffb_chol* chol, int n, const double* vals);
+int ffb_chol_solve(ffb_chol* chol, int n, const double* b, double* x);
+/* band width of the permuted matrix and stored factor entries (lower band) */
+int ffb_chol_info(ffb_chol* chol, int* bandwidth, long long* factor_nonzeros);
+
 /* ---- I/O and evaluation: include/flowfem/imaging.hpp, metrics.hpp ---
  * load_image (imaging.hpp, image_io.cpp:136-145): binary PGM (8/16 bit) or non-interlaced
  * PNG, normalised to [0,1] (RGB -> 0.299 R + 0.587 G + 0.114 B). Call with out == NULL to
@@ -184,6 +207,9 @@ int ffb_set_frames(ffb_ctx* ctx, int W, int H, const double* f0, const double* f
 int ffb_set_reg(ffb_ctx* ctx, const double* alpha, const double* lambda);
 int ffb_get_reg(ffb_ctx* ctx, double* alpha, double* lambda);
 int ffb_set_partition(ffb_ctx* ctx, int px, int py, int overlap);
+/* the caller's Partition in the flat format above (schwarz_solve's `const Partition&`); it
+ * must be the grid build_partition makes for its (W, H, px, py, ov) */
+int ffb_set_partition_flat(ffb_ctx* ctx, const int* flat, long len);
 /* Additive-Schwarz-preconditioned CG to ||b-Au||/||b|| <= tol (true residual,
  * linsolve.cpp:314-356). u3 (planes3): warm start on input if warm != 0, solution on
  * output. Refactors the subdomain band factors iff alpha changed since the last factor. */
@@ -242,23 +268,37 @@ int ffb_energy(ffb_ctx* ctx, int W, int H, const double* t10, const double* alph
 /* energy of the resident solution with the resident terms and regularisation */
 int ffb_energy_resident(ffb_ctx* ctx, int nc, double* e);
 
-/* ---- multi-GPU: subdomains sharded over ranks (one process per GPU) ------------------
- * Rank r of `world` factors and solves subdomains [lo, hi) (contiguous in partition order);
- * vectors are replicated, so the only exchange per CG iteration is the sum of the
- * preconditioned residual z over ranks, done by the caller (e.g. an NCCL all-reduce on
- * the buffer from ffb_device_buffer) between the two stages:
- *   ffb_pcg_begin; allreduce(z); ffb_pcg_stage(1);
- *   repeat { ffb_pcg_stage(0); allreduce(z); ffb_pcg_stage(1); }  (status every few)
- *   ffb_pcg_end.
- * With world == 1 the same protocol reproduces ffb_pcg_solve. */
-int ffb_shard_range(int n_parts, int rank, int world, int* lo, int* hi);
-int ffb_set_shard(ffb_ctx* ctx, int rank, int world);
-int ffb_pcg_begin(ffb_ctx* ctx, int nc, double tol, int max_iters, int warm, const double* u3);
-int ffb_pcg_stage(ffb_ctx* ctx, int stage);
-int ffb_pcg_status(ffb_ctx* ctx, int* done, int* iters, double* residual, int* err);
-int ffb_pcg_end(ffb_ctx* ctx, double* u3, int* iters, double* residual);
-/* interleaved CG vectors (nc * W * H doubles): 0 z, 1 r, 2 x, 3/4 the two p buffers */
-int ffb_device_buffer(ffb_ctx* ctx, int which, void** ptr, long long* n_doubles);
+/* ---- multi-GPU: one rank per GPU, the exchange inside the library -----
+ * Rank r of `world` owns the band of subdomain rows [r py / world, (r+1) py / world) and the
+ * pixel rows of their cores; it factors and solves only those subdomains and runs the CG
+ * kernels on its rows. Per CG iteration the library exchanges, with the neighbouring ranks
+ * only: the residual on the rows its subdomains reach into (overlap width), the partial
+ * subdomain sums of z on the rows it covers in a neighbour's band, and one row of z; the CG
+ * scalars are all-reduced as per-subdomain-row values and summed in a fixed order, so the
+ * iterates, iteration counts and results are BITWISE identical for every world size. After
+ * each solve every rank holds the whole solution. Set a communicator, then call
+ * ffb_run_on_frames / ffb_run_on_frames_dev / ffb_pcg_solve on every rank with the same
+ * inputs; the call returns when the distributed solve is done. */
+typedef struct ffb_local_hub ffb_local_hub;
+/* NCCL (P2P ncclSend/ncclRecv over NVLink, ncclAllReduce, ncclBroadcast): rank 0 makes the
+ * 128-byte unique id, the caller shares it (torch.distributed, MPI, a file), every rank then
+ * calls ffb_comm_init_nccl with its rank. libnccl.so.2 is loaded at run time. */
+int ffb_comm_nccl_id(unsigned char* id128);
+int ffb_comm_init_nccl(ffb_ctx* ctx, int rank, int world, const unsigned char* id128);
+/* In-process communicator for N contexts driven by N host threads (on one or several
+ * devices): the same protocol with host rendezvous and device copies — for tests and for a
+ * single process that drives several GPUs. */
+int ffb_comm_local_hub(int world, ffb_local_hub** hub);
+int ffb_comm_local_hub_destroy(ffb_local_hub* hub);
+int ffb_comm_init_local(ffb_ctx* ctx, ffb_local_hub* hub, int rank);
+/* rank / world of the context; rows (may be NULL, needs a partition): the 12 ints
+ * y0 y1 j0 j1 fa0 fa1 fb0 fb1 ra0 ra1 rb0 rb1 of ffb_comm_rows */
+int ffb_comm_info(ffb_ctx* ctx, int* rank, int* world, int* rows);
+/* Host-only row geometry of rank/world for build_partition(W, H, px, py, ov): owned pixel
+ * rows [y0,y1), subdomain rows [j0,j1), rows its subdomains cover above [fa0,fa1) and below
+ * [fb0,fb1) (its halo of r; its partial z goes there), and its rows covered by the rank
+ * above [ra0,ra1) / below [rb0,rb1). */
+int ffb_comm_rows(int W, int H, int px, int py, int ov, int rank, int world, int* rows12);
 
 /* run_on_frames (pipeline.hpp:53, pipeline.cpp:38-78) under the converged-pass protocol:
  * n_passes x {solve to tol, error_indicator, update_alpha} + one final solve.

@@ -90,13 +90,22 @@ SIGNATURES = {
     "ffb_schwarz_run": (_i, [_vp, C.POINTER(SchwarzOptionsC), _vp, C.POINTER(SchwarzStatsC)]),
     "ffb_energy": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _i, _vp]),
     "ffb_energy_resident": (_i, [_vp, _i, _vp]),
-    "ffb_shard_range": (_i, [_i, _i, _i, _vp, _vp]),
-    "ffb_set_shard": (_i, [_vp, _i, _i]),
-    "ffb_pcg_begin": (_i, [_vp, _i, _d, _i, _i, _vp]),
-    "ffb_pcg_stage": (_i, [_vp, _i]),
-    "ffb_pcg_status": (_i, [_vp, _vp, _vp, _vp, _vp]),
-    "ffb_pcg_end": (_i, [_vp, _vp, _vp, _vp]),
-    "ffb_device_buffer": (_i, [_vp, _i, _vp, _vp]),
+    "ffb_assemble_system": (_i, [_vp, _i, _i, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp,
+                                 _vp, _vp, _vp, _vp, _vp]),
+    "ffb_chol_create": (_i, [_vp, C.POINTER(_vp)]),
+    "ffb_chol_destroy": (_i, [_vp]),
+    "ffb_chol_analyze": (_i, [_vp, _i, _i, _vp, _vp]),
+    "ffb_chol_factorize": (_i, [_vp, _i, _vp]),
+    "ffb_chol_solve": (_i, [_vp, _i, _vp, _vp]),
+    "ffb_chol_info": (_i, [_vp, _vp, _vp]),
+    "ffb_set_partition_flat": (_i, [_vp, _vp, C.c_long]),
+    "ffb_comm_nccl_id": (_i, [_vp]),
+    "ffb_comm_init_nccl": (_i, [_vp, _i, _i, _vp]),
+    "ffb_comm_local_hub": (_i, [_i, C.POINTER(_vp)]),
+    "ffb_comm_local_hub_destroy": (_i, [_vp]),
+    "ffb_comm_init_local": (_i, [_vp, _vp, _i]),
+    "ffb_comm_info": (_i, [_vp, _vp, _vp, _vp]),
+    "ffb_comm_rows": (_i, [_i, _i, _i, _i, _i, _i, _i, _vp]),
     "ffb_run_on_frames": (_i, [_vp, _i, _i, _vp, _vp, C.POINTER(RunConfigC), _vp, _vp,
                                C.POINTER(RunStatsC)]),
     "ffb_run_on_frames_dev": (_i, [_vp, _i, _i, _vp, _vp, C.POINTER(RunConfigC), _vp,

@@ -31,12 +31,13 @@ CU = {
     "band.cu": ["-Xptxas", "-v"] if os.environ.get("FFB_PTXAS_V") else [],
     "pcg.cu": [],
     "coarse.cu": [],
+    "comm.cu": [],
     "ras.cu": ["--fmad=false"],
     "linsolve.cu": ["--fmad=false"],
     "metrics.cu": ["--fmad=false"],
 }
 CPP = ["capi.cpp", "partition.cpp", "rcm.cpp", "io.cpp"]
-HEADERS = ["ffb_internal.cuh", "partition.hpp"]
+HEADERS = ["ffb_internal.cuh", "partition.hpp", "comm.hpp"]
 
 
 def _newer(src_list, dst):

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/flowfem_b200.h"
+#include "comm.hpp"
 #include "ffb_internal.cuh"
 #include "partition.hpp"
 
@@ -90,6 +91,7 @@ struct ffb_ctx {
   long long ntri = 0;
   DBuf<double> t10, alpha, lambda, coef, b, x, r, z, p0, p1, q, eta, part, tmp, work, frames;
   DBuf<double> eta_hist;
+  DBuf<double> red;  // reduction scratch of the indicator / energy / compose kernels
   DBuf<int> bad_diag;
   DBuf<unsigned> counter;
   DBuf<PcgCtl> ctl;
@@ -105,7 +107,13 @@ struct ffb_ctx {
   int part_px = 0, part_py = 0, part_ov = -1, part_nc = 0;
   Partition decomp;
   int nbf = 32, kd_max = 0, ccl = 1;
-  int shard_rank = 0, shard_world = 1, s_lo = 0, s_hi = 0;  // multi-GPU: own subdomains
+  // multi-GPU (comm.hpp): this rank's row band of subdomains; s_lo/s_hi = its subdomains
+  std::unique_ptr<Comm> comm;
+  RankRows rows{};
+  int up = -1, dn = -1;  // nearest non-empty ranks above / below (-1: none)
+  std::vector<size_t> gather_off, gather_cnt;  // owned rows of every rank, in doubles / W nc
+  int s_lo = 0, s_hi = 0;
+  DBuf<double> ur, urs, zs_up, zs_dn, zr_up, zr_dn;
   int stage_nc = 0, stage_max_iters = 0;
   double stage_tol = 0;
   SolvePlan plan{};
@@ -124,6 +132,8 @@ struct ffb_ctx {
   DBuf<int> csr_rp, csr_ci, csr_perm, csr_iperm, csr_bad;
   DBuf<double> csr_v, csr_b, csr_x, csr_r, csr_z, csr_p, csr_Ap, csr_diag, csr_part, csr_AB;
   DBuf<CgCtl> cgctl;
+  DBuf<int> a_f2v, a_v2f, a_rp;  // assemble(): the CSR pattern of the last system
+  DBuf<double> a_g;
   // literal loop, CG subdomain mode: reference-order vectors + per-subdomain control blocks
   DBuf<double> b_x, b_b, b_r, b_z, b_p, b_Ap, b_part;
   DBuf<CgCtl> b_ctl;
@@ -150,6 +160,18 @@ struct ffb_ctx {
     if (h_ctl) cudaFreeHost(h_ctl);
     if (own_st) cudaStreamDestroy(own_st);
   }
+};
+
+// SparseCholesky (linsolve.hpp:32-48) on the device: analyze = the reference's RCM ordering
+// (bit-exact, host integer work) and the band width; factorize = band Cholesky of the
+// permuted matrix on the device; solve = permuted forward/backward substitution.
+struct ffb_chol {
+  ffb_ctx* c = nullptr;
+  int n = 0, nc = 3, bw = 0;
+  long long nnz = 0;
+  bool factored = false;
+  DBuf<int> perm, iperm, rp, ci, bad;
+  DBuf<double> v, AB, t, b;
 };
 
 namespace {
@@ -236,6 +258,30 @@ void ensure_rhs(ffb_ctx* c, int nc) {
   c->rhs_nc = nc;
 }
 
+// Row band of `rank`: subdomain rows [j0, j1) = [rank py / world, (rank+1) py / world), the
+// core rows they own, the rows their free rectangles reach into the neighbours' bands, and
+// the rows of this band the neighbours' subdomains cover (SURVEY §8e exchange sets).
+RankRows rank_rows(const Partition& P, int rank, int world) {
+  const int px = P.px, py = P.py;
+  RankRows g{};
+  g.j0 = static_cast<int>(static_cast<long long>(rank) * py / world);
+  g.j1 = static_cast<int>(static_cast<long long>(rank + 1) * py / world);
+  g.y0 = P.ys[g.j0];
+  g.y1 = P.ys[g.j1];
+  g.fa0 = g.fa1 = g.y0;
+  g.fb0 = g.fb1 = g.y1;
+  g.ra0 = g.ra1 = g.y0;
+  g.rb0 = g.rb1 = g.y1;
+  if (g.j1 == g.j0) return g;  // an empty rank (world > py)
+  const Rect top = free_rect(P, g.j0 * px), bot = free_rect(P, (g.j1 - 1) * px);
+  g.fa0 = std::min(top.y0, g.y0);
+  g.fb1 = std::max(bot.y1, g.y1);
+  if (g.j0 > 0) g.ra1 = std::min(free_rect(P, (g.j0 - 1) * px).y1, g.y1);
+  if (g.j1 < py) g.rb0 = std::max(free_rect(P, g.j1 * px).y0, g.y0);
+  if (g.fa1 - g.fa0 > 0 && g.j0 == 0) fail("schwarz: rank rows: free rows above the image");
+  return g;
+}
+
 void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
   if (c->have_part && c->part_px == px && c->part_py == py && c->part_ov == ov &&
       c->part_nc == nc)
@@ -269,9 +315,24 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
   }
   c->plan = solve_plan(kd_max, c->ccl);
   c->subs.assign(np, SubInfo{});
-  // subdomains [s_lo, s_hi) are factored and solved here (all of them on a single GPU)
-  c->s_lo = static_cast<int>(static_cast<long long>(c->shard_rank) * np / c->shard_world);
-  c->s_hi = static_cast<int>(static_cast<long long>(c->shard_rank + 1) * np / c->shard_world);
+  // this rank's band of subdomain rows (all of them on a single GPU): subdomains
+  // [s_lo, s_hi) are factored and solved here
+  {
+    const int rank = c->comm ? c->comm->rank : 0, world = c->comm ? c->comm->world : 1;
+    c->rows = rank_rows(c->decomp, rank, world);
+    c->s_lo = c->rows.j0 * px;
+    c->s_hi = c->rows.j1 * px;
+    c->up = c->dn = -1;
+    c->gather_off.assign(world, 0);
+    c->gather_cnt.assign(world, 0);
+    for (int q = 0; q < world; ++q) {
+      const RankRows gq = rank_rows(c->decomp, q, world);
+      c->gather_off[q] = static_cast<size_t>(gq.y0) * W * nc;
+      c->gather_cnt[q] = static_cast<size_t>(gq.y1 - gq.y0) * W * nc;
+      if (gq.j1 > gq.j0 && q < rank) c->up = q;
+      if (gq.j1 > gq.j0 && q > rank && c->dn < 0) c->dn = q;
+    }
+  }
   long long fac_off = 0, vec_off = 0;
   double fd = 0, ad = 0, sn = 0, ff = 0;
   for (int p = 0; p < np; ++p) {
@@ -438,10 +499,9 @@ void ensure_coarse(ffb_ctx* c, int nc) {
   c->coarse_nc = nc;
 }
 
-// y = A0^-1 Z^T r for the combine kernel (nullptr without a coarse space; in a sharded solve
-// only rank 0 adds it, the all-reduce of z then carries it to every rank)
+// y = A0^-1 Z^T r for the combine kernel (nullptr without a coarse space; single GPU only)
 const double* coarse_term(ffb_ctx* c, int nc, const double* r, const PcgCtl* ctl) {
-  if (!c->coarse || c->shard_rank != 0) return nullptr;
+  if (!c->coarse || (c->comm && c->comm->world > 1)) return nullptr;
   coarse_apply(r, c->W, nc, c->d_xs.p, c->d_ys.p, c->part_px, c->part_py, c->d_ccol.p,
                c->d_crow.p, c->cAinv.p, c->cgv.p, c->cyv.p, ctl, c->st);
   return c->cyv.p;
@@ -488,6 +548,83 @@ struct PcgResult {
 };
 
 // Schwarz-preconditioned CG on the resident system, x warm or zero.
+// rows [a, b) of an interleaved nc-component vector as an exchange slice
+Xfer rows_xfer(double* v, int W, int nc, int a, int b, int peer, int send) {
+  return Xfer{peer, send, v + static_cast<size_t>(a) * W * nc,
+              static_cast<size_t>(std::max(0, b - a)) * W * nc};
+}
+
+// One scalar reduction's completion: world 1 finished it inside the kernel (finish = 1);
+// otherwise all-reduce the unit values and sum them in unit order on every rank.
+void reduce_scalar(ffb_ctx* c, int stage, int nvals) {
+  if (!c->comm || c->comm->world == 1) return;
+  // out of place: ur keeps zeros outside this rank's units, urs receives the sum
+  double* urs = c->urs.ensure(2 * static_cast<size_t>(c->part_py));
+  c->comm->allreduce_sum(c->ur.p, urs, static_cast<size_t>(nvals) * c->part_py, c->st);
+  pcg_scalar(urs, c->part_py, stage, c->ctl.p, c->st);
+}
+
+// z = M^-1 r on the owned rows: r halo -> subdomain solves -> partial sums for the
+// neighbours -> combine (+ r.z) -> z halo (one row), SURVEY §8e steps 1-3
+void precondition(ffb_ctx* c, int nc, const int* flags, int fin) {
+  const bool multi = c->comm && c->comm->world > 1;
+  const RankRows& g = c->rows;
+  const int W = c->W;
+  double* r = c->r.p;
+  double* z = c->z.p;
+  PcgCtl* ctl = c->ctl.p;
+  if (multi) {  // r on the rows my subdomains reach into; mine to the neighbours
+    Xfer x[4];
+    int n = 0;
+    if (c->up >= 0) {
+      x[n++] = rows_xfer(r, W, nc, g.ra0, g.ra1, c->up, 1);
+      x[n++] = rows_xfer(r, W, nc, g.fa0, g.fa1, c->up, 0);
+    }
+    if (c->dn >= 0) {
+      x[n++] = rows_xfer(r, W, nc, g.rb0, g.rb1, c->dn, 1);
+      x[n++] = rows_xfer(r, W, nc, g.fb0, g.fb1, c->dn, 0);
+    }
+    c->comm->exchange(x, n, c->st);
+  }
+  launch_asm(c, nc, r, flags);
+  const double* yc = multi ? nullptr : coarse_term(c, nc, r, ctl);
+  if (multi) {  // this rank's subdomain sums on the neighbours' rows, theirs on mine
+    pcg_zpart(nc, c->d_subs.p, c->d_col.p, c->d_row.p, c->part_px, c->zlocal.p, W, g, c->zs_up.p,
+              c->zs_dn.p, ctl, c->st);
+    Xfer x[4];
+    int n = 0;
+    if (c->up >= 0) {
+      x[n++] = Xfer{c->up, 1, c->zs_up.p, static_cast<size_t>(g.fa1 - g.fa0) * W * nc};
+      x[n++] = Xfer{c->up, 0, c->zr_up.p, static_cast<size_t>(g.ra1 - g.ra0) * W * nc};
+    }
+    if (c->dn >= 0) {
+      x[n++] = Xfer{c->dn, 1, c->zs_dn.p, static_cast<size_t>(g.fb1 - g.fb0) * W * nc};
+      x[n++] = Xfer{c->dn, 0, c->zr_dn.p, static_cast<size_t>(g.rb1 - g.rb0) * W * nc};
+    }
+    c->comm->exchange(x, n, c->st);
+  }
+  pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, c->part_px, c->zlocal.p, r, z, W, g,
+              c->d_ys.p, c->part_py, c->zr_up.p, c->zr_dn.p, ctl, c->part.p, c->ur.p, fin, c->st,
+              yc, c->d_ccol.p, c->d_crow.p);
+  reduce_scalar(c, pcg_stage_rz(), 1);
+  if (multi) {  // one row of z each side for the next operator application
+    Xfer x[4];
+    int n = 0;
+    if (c->up >= 0) {
+      x[n++] = rows_xfer(z, W, nc, g.y0, g.y0 + 1, c->up, 1);
+      x[n++] = rows_xfer(z, W, nc, g.y0 - 1, g.y0, c->up, 0);
+    }
+    if (c->dn >= 0) {
+      x[n++] = rows_xfer(z, W, nc, g.y1 - 1, g.y1, c->dn, 1);
+      x[n++] = rows_xfer(z, W, nc, g.y1, g.y1 + 1, c->dn, 0);
+    }
+    c->comm->exchange(x, n, c->st);
+  }
+}
+
+// Schwarz-preconditioned CG on the resident system, x warm or zero. With a communicator the
+// rank works on its row band (pcg.cu) and x is all-gathered at the end, so every rank holds
+// the whole solution; the iterates are bitwise those of the single-GPU solve.
 PcgResult pcg(ffb_ctx* c, int nc, double tol, int max_iters, bool warm) {
   ensure_coef(c, nc);
   ensure_rhs(c, nc);
@@ -495,36 +632,45 @@ PcgResult pcg(ffb_ctx* c, int nc, double tol, int max_iters, bool warm) {
   ensure_coarse(c, nc);
   const size_t N = c->N;
   const long long nvec = static_cast<long long>(N) * nc;
+  const bool multi = c->comm && c->comm->world > 1;
+  const int fin = multi ? 0 : 1;
+  const RankRows& g = c->rows;
+  const int W = c->W, py = c->part_py;
   double* x = c->x.ensure(3 * N);
   double* r = c->r.ensure(3 * N);
   double* z = c->z.ensure(3 * N);
   double* P0 = c->p0.ensure(3 * N);
   double* P1 = c->p1.ensure(3 * N);
   double* q = c->q.ensure(3 * N);
-  double* part = c->part.ensure(4 * kRedBlocks);
+  c->part.ensure(2 * static_cast<size_t>(std::max(1, g.j1 - g.j0)) * kCU);
+  double* ur = c->ur.ensure(2 * static_cast<size_t>(py));
+  FFB_CUDA(cudaMemsetAsync(ur, 0, 2 * py * sizeof(double), c->st));  // zero off this rank's units
+  const size_t row = static_cast<size_t>(W) * nc;
+  c->zs_up.ensure(std::max(1, g.fa1 - g.fa0) * row);
+  c->zs_dn.ensure(std::max(1, g.fb1 - g.fb0) * row);
+  c->zr_up.ensure(std::max(1, g.ra1 - g.ra0) * row);
+  c->zr_dn.ensure(std::max(1, g.rb1 - g.rb0) * row);
   PcgCtl* ctl = c->ctl.ensure(1);
   if (!c->h_ctl) FFB_CUDA(cudaMallocHost(&c->h_ctl, sizeof(PcgCtl)));
   if (!warm) FFB_CUDA(cudaMemsetAsync(x, 0, nvec * sizeof(double), c->st));
   if (max_iters <= 0) max_iters = static_cast<int>(std::min<long long>(10 * nvec, 1 << 30));
   std::memset(c->h_ctl, 0, sizeof(PcgCtl));
   c->h_ctl->tol = tol;
+  c->h_ctl->max_iters = max_iters;
   FFB_CUDA(cudaMemcpyAsync(ctl, c->h_ctl, sizeof(PcgCtl), cudaMemcpyHostToDevice, c->st));
   const int* flags = &ctl->done;
-  const int px = c->part_px;
-  pcg_init(nc, c->coef.p, c->b.p, x, r, c->W, c->H, ctl, part, c->st);
-  launch_asm(c, nc, r, flags);
-  if (c->shard_world != 1) fail("schwarz.schwarz_solve: sharded context: use the staged solve");
-  pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, px, c->zlocal.p, r, z, c->W, c->H, ctl,
-              part, 0, c->s_hi, 0, c->st, coarse_term(c, nc, r, ctl), c->d_ccol.p, c->d_crow.p);
+  pcg_init(nc, c->coef.p, c->b.p, x, r, W, c->H, g, c->d_ys.p, py, ctl, c->part.p, ur, fin, c->st);
+  reduce_scalar(c, pcg_stage_init(), 2);
+  precondition(c, nc, flags, fin);
   const int chunk = 8;
   for (;;) {
     for (int it = 0; it < chunk; ++it) {
-      pcg_spmv_p(nc, c->coef.p, z, P0, P1, q, c->W, c->H, ctl, part, c->st);
-      pcg_update(nc, x, r, P0, P1, q, nvec, max_iters, ctl, part, c->st);
-      launch_asm(c, nc, r, flags);
-      pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, px, c->zlocal.p, r, z, c->W, c->H,
-                  ctl, part, 0, c->s_hi, 0, c->st, coarse_term(c, nc, r, ctl), c->d_ccol.p,
-                  c->d_crow.p);
+      pcg_spmv_p(nc, c->coef.p, z, P0, P1, q, W, c->H, g, c->d_ys.p, py, ctl, c->part.p, ur, fin,
+                 c->st);
+      reduce_scalar(c, pcg_stage_pap(), 1);
+      pcg_update(nc, x, r, P0, P1, q, W, g, c->d_ys.p, py, ctl, c->part.p, ur, fin, c->st);
+      reduce_scalar(c, pcg_stage_rr(), 1);
+      precondition(c, nc, flags, fin);
     }
     FFB_CUDA(cudaMemcpyAsync(c->h_ctl, ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, c->st));
     sync(c);
@@ -538,6 +684,8 @@ PcgResult pcg(ffb_ctx* c, int nc, double tol, int max_iters, bool warm) {
     FFB_CUDA(cudaMemsetAsync(x, 0, nvec * sizeof(double), c->st));
     return {0, 0.0};
   }
+  if (multi)  // every rank's owned rows of x to every rank
+    c->comm->allgather_rows(x, c->gather_off.data(), c->gather_cnt.data(), c->st);
   if (!(h.res <= tol)) {
     char buf[160];
     std::snprintf(buf, sizeof buf,
@@ -579,7 +727,7 @@ void run_dev(ffb_ctx* c, int W, int H, const double* f0, const double* f1,
   const double alpha_th = std::isnan(cfg->alpha_th) ? cfg->alpha0 / 100.0 : cfg->alpha_th;
   double* eh = c->eta_hist.ensure(FFB_MAX_SOLVES);
   double* eta = c->eta.ensure(c->ntri);
-  double* blockmax = c->part.ensure(4 * kRedBlocks);
+  double* blockmax = c->red.ensure(4 * kRedBlocks);
   unsigned* counter = c->counter.ensure(1);
   FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
   double ms_factor = 0, ms_pcg = 0, ms_adapt = 0, ms_factor0 = 0;
@@ -912,7 +1060,7 @@ int ffb_error_indicator(ffb_ctx* c, int W, int H, const double* t10, const doubl
     unsigned* counter = c->counter.ensure(1);
     FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
     error_indicator(c->t10.p, c->alpha.p, c->lambda.p, u, W, H, nc, e, em,
-                    c->part.ensure(4 * kRedBlocks), counter, c->st);
+                    c->red.ensure(4 * kRedBlocks), counter, c->st);
     if (eta) download(eta, e, c->ntri, c->st);
     download(eta_max, em, 1, c->st);
     sync(c);
@@ -1013,146 +1161,66 @@ int ffb_pcg_solve(ffb_ctx* c, int nc, double tol, int max_iters, int warm, doubl
   });
 }
 
-// ---- multi-GPU staged solve -----------------------------------------------------------
-int ffb_shard_range(int n_parts, int rank, int world, int* lo, int* hi) {
+// ---- multi-GPU: communicators (comm.hpp) --------------------------------------------
+int ffb_comm_nccl_id(unsigned char* id128) {
   return guard([&] {
-    if (world < 1 || rank < 0 || rank >= world) fail("schwarz: invalid shard rank/world");
-    *lo = static_cast<int>(static_cast<long long>(rank) * n_parts / world);
-    *hi = static_cast<int>(static_cast<long long>(rank + 1) * n_parts / world);
+    if (!id128) fail("schwarz.comm: null id buffer");
+    nccl_unique_id(id128);
   });
 }
 
-int ffb_set_shard(ffb_ctx* c, int rank, int world) {
+int ffb_comm_init_nccl(ffb_ctx* c, int rank, int world, const unsigned char* id128) {
   return guard([&] {
     check_ctx(c);
-    if (world < 1 || rank < 0 || rank >= world) fail("schwarz: invalid shard rank/world");
-    c->shard_rank = rank;
-    c->shard_world = world;
+    if (world < 1 || rank < 0 || rank >= world) fail("schwarz.comm: invalid rank/world");
+    c->comm = world == 1 ? nullptr : make_nccl_comm(rank, world, id128);
+    c->have_part = false;  // the row band changes with the communicator
+    c->factor_key_a = c->factor_key_t = -1;
+    c->fact_valid = 0;
+  });
+}
+
+int ffb_comm_local_hub(int world, ffb_local_hub** hub) {
+  return guard([&] {
+    if (!hub) fail("schwarz.comm: null hub pointer");
+    *hub = reinterpret_cast<ffb_local_hub*>(local_hub_create(world));
+  });
+}
+
+int ffb_comm_local_hub_destroy(ffb_local_hub* hub) {
+  return guard([&] { local_hub_destroy(reinterpret_cast<LocalHub*>(hub)); });
+}
+
+int ffb_comm_init_local(ffb_ctx* c, ffb_local_hub* hub, int rank) {
+  return guard([&] {
+    check_ctx(c);
+    c->comm = make_local_comm(reinterpret_cast<LocalHub*>(hub), rank);
     c->have_part = false;
     c->factor_key_a = c->factor_key_t = -1;
+    c->fact_valid = 0;
   });
 }
 
-int ffb_pcg_begin(ffb_ctx* c, int nc, double tol, int max_iters, int warm, const double* u3) {
+int ffb_comm_info(ffb_ctx* c, int* rank, int* world, int* rows) {
   return guard([&] {
     check_ctx(c);
-    if (nc != 2 && nc != 3) fail("assembly.assemble: components must be 2 or 3");
-    if (!c->alpha.p) fail("assembly.assemble: no regularization set");
-    if (!c->have_part) fail("schwarz.schwarz_solve: no partition set");
-    ensure_coef(c, nc);
-    ensure_rhs(c, nc);
-    ensure_factor(c, nc);
-    ensure_coarse(c, nc);
-    const size_t N = c->N;
-    const long long nvec = static_cast<long long>(N) * nc;
-    double* x = c->x.ensure(3 * N);
-    double* r = c->r.ensure(3 * N);
-    double* z = c->z.ensure(3 * N);
-    c->p0.ensure(3 * N);
-    c->p1.ensure(3 * N);
-    c->q.ensure(3 * N);
-    double* part = c->part.ensure(4 * kRedBlocks);
-    PcgCtl* ctl = c->ctl.ensure(1);
-    if (!c->h_ctl) FFB_CUDA(cudaMallocHost(&c->h_ctl, sizeof(PcgCtl)));
-    if (warm && u3) {
-      double* w = c->work.ensure(3 * N);
-      upload(w, u3, 3 * N, c->st);
-      planes_to_inter(w, x, static_cast<long long>(N), nc, c->st);
-    } else if (!warm) {
-      FFB_CUDA(cudaMemsetAsync(x, 0, nvec * sizeof(double), c->st));
-    }
-    c->stage_max_iters =
-        max_iters > 0 ? max_iters : static_cast<int>(std::min<long long>(10 * nvec, 1 << 30));
-    c->stage_nc = nc;
-    c->stage_tol = tol;
-    std::memset(c->h_ctl, 0, sizeof(PcgCtl));
-    c->h_ctl->tol = tol;
-    FFB_CUDA(cudaMemcpyAsync(ctl, c->h_ctl, sizeof(PcgCtl), cudaMemcpyHostToDevice, c->st));
-    pcg_init(nc, c->coef.p, c->b.p, x, r, c->W, c->H, ctl, part, c->st);
-    launch_asm(c, nc, r, &ctl->done);
-    pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, c->part_px, c->zlocal.p, r, z, c->W, c->H,
-                ctl, part, c->s_lo, c->s_hi, 1, c->st, coarse_term(c, nc, r, ctl), c->d_ccol.p,
-                c->d_crow.p);
-  });
-}
-
-int ffb_pcg_stage(ffb_ctx* c, int stage) {
-  return guard([&] {
-    check_ctx(c);
-    if (!c->stage_nc) fail("linsolve.cg: no staged solve in progress");
-    const int nc = c->stage_nc;
-    const long long nvec = static_cast<long long>(c->N) * nc;
-    PcgCtl* ctl = c->ctl.p;
-    double* part = c->part.p;
-    if (stage == 0) {  // A: p, q = A p, x/r update, own subdomain solves, partial z
-      pcg_spmv_p(nc, c->coef.p, c->z.p, c->p0.p, c->p1.p, c->q.p, c->W, c->H, ctl, part, c->st);
-      pcg_update(nc, c->x.p, c->r.p, c->p0.p, c->p1.p, c->q.p, nvec, c->stage_max_iters, ctl, part,
-                 c->st);
-      launch_asm(c, nc, c->r.p, &ctl->done);
-      pcg_combine(nc, c->d_subs.p, c->d_col.p, c->d_row.p, c->part_px, c->zlocal.p, c->r.p, c->z.p,
-                  c->W, c->H, ctl, part, c->s_lo, c->s_hi, 1, c->st,
-                  coarse_term(c, nc, c->r.p, ctl), c->d_ccol.p, c->d_crow.p);
-    } else if (stage == 1) {  // B: r.z of the all-reduced z
-      pcg_rz(c->r.p, c->z.p, nvec, ctl, part, c->st);
-    } else {
-      fail("linsolve.cg: unknown stage");
+    if (rank) *rank = c->comm ? c->comm->rank : 0;
+    if (world) *world = c->comm ? c->comm->world : 1;
+    if (rows) {
+      if (!c->have_part) fail("schwarz.comm: no partition set");
+      const RankRows& g = c->rows;
+      const int v[12] = {g.y0, g.y1, g.j0, g.j1, g.fa0, g.fa1, g.fb0, g.fb1, g.ra0, g.ra1, g.rb0, g.rb1};
+      std::memcpy(rows, v, sizeof v);
     }
   });
 }
 
-int ffb_pcg_status(ffb_ctx* c, int* done, int* iters, double* residual, int* err) {
+int ffb_comm_rows(int W, int H, int px, int py, int ov, int rank, int world, int* rows) {
   return guard([&] {
-    check_ctx(c);
-    if (!c->stage_nc) fail("linsolve.cg: no staged solve in progress");
-    FFB_CUDA(cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(PcgCtl), cudaMemcpyDeviceToHost, c->st));
-    sync(c);
-    if (c->time_asm) harvest_asm_events(c);
-    if (done) *done = c->h_ctl->done;
-    if (iters) *iters = c->h_ctl->iters;
-    if (residual) *residual = c->h_ctl->res;
-    if (err) *err = c->h_ctl->err;
-  });
-}
-
-int ffb_pcg_end(ffb_ctx* c, double* u3, int* iters, double* residual) {
-  return guard([&] {
-    check_ctx(c);
-    if (!c->stage_nc) fail("linsolve.cg: no staged solve in progress");
-    const int nc = c->stage_nc;
-    c->stage_nc = 0;
-    FFB_CUDA(cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(PcgCtl), cudaMemcpyDeviceToHost, c->st));
-    sync(c);
-    const PcgCtl& h = *c->h_ctl;
-    if (h.err)
-      fail("linsolve.cg: indefinite matrix detected at iteration " + std::to_string(h.err_it));
-    if (h.zero_rhs)
-      FFB_CUDA(cudaMemsetAsync(c->x.p, 0, static_cast<long long>(c->N) * nc * sizeof(double), c->st));
-    else if (!(h.res <= c->stage_tol)) {
-      char buf[160];
-      std::snprintf(buf, sizeof buf,
-                    "linsolve.cg: no convergence after %d iterations, relative residual %f",
-                    h.iters, h.res);
-      fail(buf);
-    }
-    if (u3) {
-      double* w = c->work.ensure(3 * c->N);
-      inter_to_planes(c->x.p, w, static_cast<long long>(c->N), nc, c->st);
-      download(u3, w, 3 * c->N, c->st);
-      sync(c);
-    }
-    if (iters) *iters = h.zero_rhs ? 0 : h.iters;
-    if (residual) *residual = h.zero_rhs ? 0.0 : h.res;
-  });
-}
-
-int ffb_device_buffer(ffb_ctx* c, int which, void** ptr, long long* n_doubles) {
-  return guard([&] {
-    check_ctx(c);
-    double* bufs[5] = {c->z.p, c->r.p, c->x.p, c->p0.p, c->p1.p};
-    if (which < 0 || which > 4) fail("ffb: unknown device buffer");
-    if (!bufs[which]) fail("ffb: buffer not allocated yet");
-    *ptr = bufs[which];
-    *n_doubles = static_cast<long long>(c->N) * (c->stage_nc ? c->stage_nc : 3);
+    if (world < 1 || rank < 0 || rank >= world) fail("schwarz.comm: invalid rank/world");
+    const RankRows g = rank_rows(build_partition(W, H, px, py, ov), rank, world);
+    const int v[12] = {g.y0, g.y1, g.j0, g.j1, g.fa0, g.fa1, g.fb0, g.fb1, g.ra0, g.ra1, g.rb0, g.rb1};
+    std::memcpy(rows, v, sizeof v);
   });
 }
 
@@ -1165,7 +1233,8 @@ int ffb_schwarz_run(ffb_ctx* c, const ffb_schwarz_options* o, double* u3, ffb_sc
     if (nc != 2 && nc != 3) fail("assembly.assemble: components must be 2 or 3");
     if (!c->alpha.p) fail("assembly.assemble: no regularization set");
     if (!c->have_part) fail("schwarz.schwarz_solve: no partition set");
-    if (c->shard_world != 1) fail("schwarz.schwarz_solve: sharded context");
+    if (c->comm && c->comm->world > 1)
+      fail("schwarz.schwarz_solve: the literal loop runs on one GPU (no communicator)");
     if (n_iters < 0) fail("schwarz.schwarz_solve: n_iters must be >= 0");
     if (o->method != FFB_SOLVE_CHOLESKY && o->method != FFB_SOLVE_CG)
       fail("schwarz.schwarz_solve: unknown solver method");
@@ -1185,7 +1254,7 @@ int ffb_schwarz_run(ffb_ctx* c, const ffb_schwarz_options* o, double* u3, ffb_sc
     double* inc = c->incs.ensure(std::max(n_iters, 1));
     double* em = c->eta_hist.ensure(std::max(n_iters, FFB_MAX_SOLVES));
     double* eta = c->eta.ensure(c->ntri);
-    double* blockmax = c->part.ensure(4 * kRedBlocks);
+    double* blockmax = c->red.ensure(4 * kRedBlocks);
     unsigned* counter = c->counter.ensure(1);
     // CG mode: persistent warm start x_prev (schwarz.cpp:250-253), reference-order vectors
     const int maxch = ras_cg_chunks(max_n);
@@ -1332,7 +1401,7 @@ int ffb_energy(ffb_ctx* c, int W, int H, const double* t10, const double* alpha,
     double* out = c->eta_hist.ensure(FFB_MAX_SOLVES);
     unsigned* counter = c->counter.ensure(1);
     FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
-    energy(c->t10.p, c->alpha.p, c->lambda.p, u, W, H, nc, out, c->part.ensure(4 * kRedBlocks),
+    energy(c->t10.p, c->alpha.p, c->lambda.p, u, W, H, nc, out, c->red.ensure(4 * kRedBlocks),
            counter, c->st);
     download(e, out, 1, c->st);
     sync(c);
@@ -1351,7 +1420,7 @@ int ffb_energy_resident(ffb_ctx* c, int nc, double* e) {
     unsigned* counter = c->counter.ensure(1);
     FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
     energy(c->t10.p, c->alpha.p, c->lambda.p, u, c->W, c->H, nc, out,
-           c->part.ensure(4 * kRedBlocks), counter, c->st);
+           c->red.ensure(4 * kRedBlocks), counter, c->st);
     download(e, out, 1, c->st);
     sync(c);
   });
@@ -1369,7 +1438,7 @@ int ffb_adapt(ffb_ctx* c, int nc, double kappa, double eta_thr, double alpha_th,
     FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
     double* eta = c->eta.ensure(c->ntri);
     error_indicator(c->t10.p, c->alpha.p, c->lambda.p, u3, c->W, c->H, nc, eta, em,
-                    c->part.ensure(4 * kRedBlocks), counter, c->st);
+                    c->red.ensure(4 * kRedBlocks), counter, c->st);
     update_alpha(c->alpha.p, c->alpha.p, eta, em, c->ntri, kappa, eta_thr, alpha_th, c->st);
     c->alpha_version++;
     if (eta_max) download(eta_max, em, 1, c->st);
@@ -1476,6 +1545,93 @@ void run_cg(ffb_ctx* c, const CsrDev& A, const double* b, const double* warm_h, 
 }  // namespace
 
 extern "C" {
+
+// assemble (assembly.hpp:59-61, assembly.cpp:32-166) as an explicit CSR SparseSystem: the
+// pattern (free vertices, row lengths) is host integer work as in the reference, the values
+// and the eliminated right-hand side come from the device coefficient planes (bitwise).
+// Call with row_ptr == NULL for n and nnz, then with arrays of n+1 / nnz / nnz / n and
+// vert_to_free[W*H] / free_to_vert[n/nc] (either may be NULL).
+int ffb_assemble_system(ffb_ctx* c, int W, int H, const double* t10, const double* alpha,
+                        const double* lambda, int nc, int n_dir, const int* dir_vertices,
+                        const double* dir_values, int* n_out, long long* nnz_out, int* row_ptr,
+                        int* cols, double* vals, double* rhs, int* vert_to_free,
+                        int* free_to_vert) {
+  return guard([&] {
+    if (nc != 2 && nc != 3) fail("assembly.assemble: components must be 2 or 3");
+    check_dims(W, H, "mesh.build_pixel_mesh");
+    const int nv = W * H;
+    std::vector<int> v2f(nv, 0);
+    std::vector<double> g;
+    if (n_dir > 0) {
+      g.assign(static_cast<size_t>(nv) * nc, 0.0);
+      for (int k = 0; k < n_dir; ++k) {
+        const int v = dir_vertices[k];
+        if (v < 0 || v >= nv) fail("assembly.assemble: Dirichlet vertex out of range");
+        v2f[v] = -1;
+        for (int cc = 0; cc < nc; ++cc) g[static_cast<size_t>(v) * nc + cc] = dir_values[k * nc + cc];
+      }
+    }
+    std::vector<int> f2v;
+    for (int v = 0; v < nv; ++v) {
+      if (v2f[v] == 0) {
+        v2f[v] = static_cast<int>(f2v.size());
+        f2v.push_back(v);
+      } else {
+        v2f[v] = -1;
+      }
+    }
+    const int nf = static_cast<int>(f2v.size());
+    std::vector<int> rp(static_cast<size_t>(nf) * nc + 1, 0);
+    for (int f = 0; f < nf; ++f) {
+      const int v = f2v[f], x = v % W, y = v / W;
+      const int nb[6][2] = {{x - 1, y - 1}, {x, y - 1}, {x - 1, y}, {x + 1, y}, {x, y + 1}, {x + 1, y + 1}};
+      int cnt = 0;
+      for (const auto& q : nb)
+        if (q[0] >= 0 && q[0] < W && q[1] >= 0 && q[1] < H && v2f[q[1] * W + q[0]] >= 0) ++cnt;
+      for (int cc = 0; cc < nc; ++cc) rp[f * nc + cc + 1] = cnt + nc;
+    }
+    for (size_t r = 0; r + 1 < rp.size(); ++r) rp[r + 1] += rp[r];
+    *n_out = nf * nc;
+    *nnz_out = rp.back();
+    if (!row_ptr) return;
+    check_ctx(c);
+    set_problem(c, W, H);
+    const size_t N = c->N;
+    upload(c->t10.ensure(10 * N), t10, 10 * N, c->st);
+    c->terms_version++;
+    ensure_reg(c);
+    upload(c->alpha.p, alpha, c->ntri, c->st);
+    upload(c->lambda.p, lambda, c->ntri, c->st);
+    c->alpha_version++;
+    c->fact_valid = 0;
+    c->coef.ensure(kCoefPlanes * N);
+    build_coef(c->t10.p, c->alpha.p, c->lambda.p, W, H, nc, c->coef.p, nullptr, c->st);
+    c->coef_key_a = c->alpha_version, c->coef_key_t = c->terms_version, c->coef_nc = nc;
+    int* d_f2v = c->a_f2v.ensure(std::max(nf, 1));
+    int* d_v2f = c->a_v2f.ensure(nv);
+    int* d_rp = c->a_rp.ensure(rp.size());
+    double* d_g = c->a_g.ensure(std::max<size_t>(g.size(), 1));
+    if (nf) FFB_CUDA(cudaMemcpyAsync(d_f2v, f2v.data(), nf * sizeof(int), cudaMemcpyHostToDevice, c->st));
+    FFB_CUDA(cudaMemcpyAsync(d_v2f, v2f.data(), nv * sizeof(int), cudaMemcpyHostToDevice, c->st));
+    FFB_CUDA(cudaMemcpyAsync(d_rp, rp.data(), rp.size() * sizeof(int), cudaMemcpyHostToDevice, c->st));
+    if (!g.empty()) upload(d_g, g.data(), g.size(), c->st);
+    const long long nnz = rp.back();
+    int* d_cols = c->csr_ci.ensure(std::max<long long>(nnz, 1));
+    double* d_vals = c->csr_v.ensure(std::max<long long>(nnz, 1));
+    double* d_rhs = c->csr_b.ensure(std::max(nf * nc, 1));
+    csr_fill(c->coef.p, c->t10.p, W, H, nc, nf, d_f2v, d_v2f, d_rp, g.empty() ? nullptr : d_g,
+             d_cols, d_vals, d_rhs, c->st);
+    std::copy(rp.begin(), rp.end(), row_ptr);
+    if (nnz) {
+      FFB_CUDA(cudaMemcpyAsync(cols, d_cols, nnz * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+      download(vals, d_vals, nnz, c->st);
+    }
+    if (nf) download(rhs, d_rhs, static_cast<size_t>(nf) * nc, c->st);
+    sync(c);
+    if (vert_to_free) std::copy(v2f.begin(), v2f.end(), vert_to_free);
+    if (free_to_vert) std::copy(f2v.begin(), f2v.end(), free_to_vert);
+  });
+}
 
 int ffb_csr_spmv(ffb_ctx* c, int n, const int* row_ptr, const int* cols, const double* vals,
                  const double* x, double* y) {
@@ -1590,6 +1746,126 @@ int ffb_csr_solve(ffb_ctx* c, int n, int components, const int* row_ptr, const i
     if (iters) *iters = 0;
     download(x, xd, n, c->st);
     sync(c);
+  });
+}
+
+int ffb_chol_create(ffb_ctx* c, ffb_chol** out) {
+  return guard([&] {
+    check_ctx(c);
+    if (!out) fail("linsolve.cholesky: null output");
+    auto h = std::make_unique<ffb_chol>();
+    h->c = c;
+    *out = h.release();
+  });
+}
+
+int ffb_chol_destroy(ffb_chol* h) {
+  return guard([&] {
+    if (!h) return;
+    cudaSetDevice(h->c->device);
+    delete h;
+  });
+}
+
+int ffb_chol_analyze(ffb_chol* h, int n, int components, const int* row_ptr, const int* cols) {
+  return guard([&] {
+    if (!h) fail("linsolve.cholesky: null handle");
+    check_ctx(h->c);
+    const std::vector<int> perm = rcm_order(n, components, row_ptr, cols);  // rcm.cpp, bit-exact
+    std::vector<int> iperm(n);
+    for (int k = 0; k < n; ++k) iperm[perm[k]] = k;
+    int bw = 0;
+    for (int r = 0; r < n; ++r)
+      for (int q = row_ptr[r]; q < row_ptr[r + 1]; ++q)
+        bw = std::max(bw, std::abs(iperm[r] - iperm[cols[q]]));
+    cudaStream_t st = h->c->st;
+    h->n = n, h->nc = components, h->bw = bw, h->nnz = n > 0 ? row_ptr[n] : 0;
+    h->factored = false;
+    FFB_CUDA(cudaMemcpyAsync(h->perm.ensure(std::max(n, 1)), perm.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
+    FFB_CUDA(cudaMemcpyAsync(h->iperm.ensure(std::max(n, 1)), iperm.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
+    FFB_CUDA(cudaMemcpyAsync(h->rp.ensure(n + 1), row_ptr, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (h->nnz)
+      FFB_CUDA(cudaMemcpyAsync(h->ci.ensure(h->nnz), cols, h->nnz * sizeof(int), cudaMemcpyHostToDevice, st));
+    FFB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int ffb_chol_factorize(ffb_chol* h, int n, const double* vals) {
+  return guard([&] {
+    if (!h || !h->perm.p) fail("linsolve.cholesky: factorize before analyze");
+    check_ctx(h->c);
+    if (n != h->n) fail("linsolve.cholesky: matrix size changed since analyze");
+    cudaStream_t st = h->c->st;
+    if (n == 0) {
+      h->factored = true;
+      return;
+    }
+    upload(h->v.ensure(std::max<long long>(h->nnz, 1)), vals, h->nnz, st);
+    const size_t nab = static_cast<size_t>(n) * (h->bw + 1);
+    double* AB = h->AB.ensure(nab);
+    FFB_CUDA(cudaMemsetAsync(AB, 0, nab * sizeof(double), st));
+    const CsrDev A{n, h->rp.p, h->ci.p, h->v.p};
+    band_scatter(A, h->iperm.p, h->bw, AB, st);
+    int* bad = h->bad.ensure(1);
+    FFB_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(int), st));
+    band_cholesky(n, h->bw, AB, bad, st);
+    int bad_h = -1;
+    FFB_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FFB_CUDA(cudaStreamSynchronize(st));
+    h->factored = false;
+    if (bad_h >= 0) {
+      int u = 0;
+      FFB_CUDA(cudaMemcpy(&u, h->perm.p + bad_h, sizeof(int), cudaMemcpyDeviceToHost));
+      fail("linsolve.cholesky: breakdown at pivot " + std::to_string(bad_h) + " (unknown " +
+           std::to_string(u) + "): matrix is not positive definite");
+    }
+    h->factored = true;
+  });
+}
+
+int ffb_chol_solve(ffb_chol* h, int n, const double* b, double* x) {
+  return guard([&] {
+    if (!h || !h->factored) fail("linsolve.cholesky: solve before factorize");
+    check_ctx(h->c);
+    if (n != h->n) fail("linsolve.cholesky: rhs size mismatch");
+    if (n == 0) return;
+    cudaStream_t st = h->c->st;
+    double* db = h->b.ensure(n);
+    double* t = h->t.ensure(n);
+    upload(db, b, n, st);
+    gather(n, h->perm.p, db, t, st);
+    band_solve(n, h->bw, h->AB.p, t, st);
+    scatter(n, h->perm.p, t, db, false, st);
+    download(x, db, n, st);
+    FFB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int ffb_chol_info(ffb_chol* h, int* bandwidth, long long* factor_nonzeros) {
+  return guard([&] {
+    if (!h) fail("linsolve.cholesky: null handle");
+    if (bandwidth) *bandwidth = h->bw;
+    if (factor_nonzeros) {  // stored lower band including the diagonal
+      long long s = 0;
+      for (int i = 0; i < h->n; ++i) s += std::min(i, h->bw) + 1;
+      *factor_nonzeros = s;
+    }
+  });
+}
+
+// the caller's Partition (flat format of include/flowfem_b200.h): must be the grid
+// build_partition(W, H, px, py, ov) makes — the device layout follows that grid
+int ffb_set_partition_flat(ffb_ctx* c, const int* flat, long len) {
+  return guard([&] {
+    check_ctx(c);
+    if (!c->W) fail("schwarz.schwarz_solve: no problem set");
+    if (!flat || len < 6) fail("schwarz.schwarz_solve: bad partition");
+    if (flat[0] != c->W || flat[1] != c->H)
+      fail("schwarz.schwarz_solve: partition does not match the mesh");
+    const std::vector<int> want = flatten(build_partition(flat[0], flat[1], flat[2], flat[3], flat[4]));
+    if (static_cast<long>(want.size()) != len || !std::equal(want.begin(), want.end(), flat))
+      fail("schwarz.schwarz_solve: only partitions made by build_partition are supported");
+    ensure_partition(c, flat[2], flat[3], flat[4], c->part_nc ? c->part_nc : 3);
   });
 }
 

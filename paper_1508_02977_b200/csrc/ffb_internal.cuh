@@ -59,6 +59,10 @@ void build_rhs(const double* t10, int W, int H, int nc, double* b, cudaStream_t 
 void apply_op(const double* coef, int W, int H, int nc, const double* x, double* y,
               cudaStream_t st);
 void planes_to_inter(const double* p3, double* x, long long N, int nc, cudaStream_t st);
+// assemble()'s CSR rows of the free vertices (pattern from the host, values on the device)
+void csr_fill(const double* coef, const double* t10, int W, int H, int nc, int n_free,
+              const int* free_to_vert, const int* vert_to_free, const int* row_ptr,
+              const double* g, int* cols, double* vals, double* rhs, cudaStream_t st);
 void inter_to_planes(const double* x, double* p3, long long N, int nc, cudaStream_t st);
 
 // ---- subdomain factor / solve (band.cu) -----------------------------------------------
@@ -133,17 +137,49 @@ struct PcgCtl {
   int err;     // 1: indefinite (pAp <= 0)
   int err_it;
   int zero_rhs;
-  int pad[2];
+  int max_iters;
+  int pad;
   unsigned counter[4];
 };
 
+// Row-band geometry of one rank (capi.cpp rank_rows): the reduction units are subdomain
+// rows; rank r owns subdomain rows [j0, j1) and the pixel rows [y0, y1) of their cores.
+constexpr int kCU = 296;  // CTAs per reduction unit (2 x 148 SMs), fixed for any world size
+struct RankRows {
+  int y0, y1;    // owned pixel rows
+  int j0, j1;    // owned subdomain rows (reduction units)
+  int fa0, fa1;  // rows above y0 that my subdomains' free rectangles cover
+  int fb0, fb1;  // rows below y1 that my subdomains cover
+  int ra0, ra1;  // my rows covered by the subdomains of the rank above
+  int rb0, rb1;  // my rows covered by the subdomains of the rank below
+};
+
+// part >= 2 * (j1 - j0) * kCU doubles; ur: 2 * py doubles (unit values, zero outside the
+// rank's units); finish = 1 when world == 1 (the last CTA completes the scalar update),
+// else the caller all-reduces ur and runs pcg_scalar.
 void pcg_init(int nc, const double* coef, const double* b, const double* x, double* r, int W,
-              int H, PcgCtl* ctl, double* part, cudaStream_t st);
+              int H, const RankRows& g, const int* ys, int py, PcgCtl* ctl, double* part,
+              double* ur, int finish, cudaStream_t st);
+void pcg_zpart(int nc, const SubInfo* subs, const AxisMap* colmap, const AxisMap* rowmap, int px,
+               const double* zlocal, int W, const RankRows& g, double* send_up, double* send_dn,
+               const PcgCtl* ctl, cudaStream_t st);
 void pcg_combine(int nc, const SubInfo* subs, const AxisMap* colmap, const AxisMap* rowmap,
-                 int px, const double* zlocal, const double* r, double* z, int W, int H,
-                 PcgCtl* ctl, double* part, int s_lo, int s_hi, int partial, cudaStream_t st,
-                 const double* yc = nullptr, const int* ccol = nullptr,
+                 int px, const double* zlocal, const double* r, double* z, int W,
+                 const RankRows& g, const int* ys, int py, const double* recv_up,
+                 const double* recv_dn, PcgCtl* ctl, double* part, double* ur, int finish,
+                 cudaStream_t st, const double* yc = nullptr, const int* ccol = nullptr,
                  const int* crow = nullptr);
+void pcg_spmv_p(int nc, const double* coef, const double* z, double* P0, double* P1, double* q,
+                int W, int H, const RankRows& g, const int* ys, int py, PcgCtl* ctl, double* part,
+                double* ur, int finish, cudaStream_t st);
+void pcg_update(int nc, double* x, double* r, const double* P0, const double* P1,
+                const double* q, int W, const RankRows& g, const int* ys, int py, PcgCtl* ctl,
+                double* part, double* ur, int finish, cudaStream_t st);
+void pcg_scalar(const double* ur, int py, int stage, PcgCtl* ctl, cudaStream_t st);
+int pcg_stage_init();
+int pcg_stage_pap();
+int pcg_stage_rr();
+int pcg_stage_rz();
 
 // ---- two-level coarse space (coarse.cu) ---------------------------------------------------
 // xs[px+1], ys[py+1]: core cuts; ccol[W] + crow[H]: coarse node of the core of pixel (x,y);

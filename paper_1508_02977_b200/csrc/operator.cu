@@ -176,6 +176,61 @@ __global__ void k_fill(double* __restrict__ p, double v, long long n) {
     p[i] = v;
 }
 
+// assemble()'s CSR SparseSystem (assembly.cpp:32-166) from the coefficient planes: one thread
+// per free vertex writes its nc rows in the reference's column order — the vertex's mesh
+// neighbours ascending (v-W-1, v-W, v-1, own nc x nc block, v+1, v+W, v+W+1; the diagonal
+// pair couples with exactly 0.0, mesh.cpp:172-186) — and eliminates constrained neighbours
+// into the right-hand side in the same order (assembly.cpp:150-160). Bitwise equal to the
+// reference (same values as the matrix-free operator, same subtraction order).
+__global__ void k_csr_fill(const double* __restrict__ coef, const double* __restrict__ t10,
+                           int W, int H, int nc, int n_free, const int* __restrict__ free_to_vert,
+                           const int* __restrict__ vert_to_free, const int* __restrict__ row_ptr,
+                           const double* __restrict__ g, int* __restrict__ cols,
+                           double* __restrict__ vals, double* __restrict__ rhs) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n_free) return;
+  const size_t n = static_cast<size_t>(W) * H;
+  const int v = free_to_vert[f];
+  const int x = v % W, y = v / W;
+  const double wv = lumped(x, y, W, H);
+  const int plane[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+  // neighbours ascending: 0 v-W-1, 1 v-W, 2 v-1, (self), 3 v+1, 4 v+W, 5 v+W+1
+  const bool has[6] = {x > 0 && y > 0, y > 0, x > 0, x < W - 1, y < H - 1, x < W - 1 && y < H - 1};
+  const int nbv[6] = {v - W - 1, v - W, v - 1, v + 1, v + W, v + W + 1};
+  for (int c = 0; c < nc; ++c) {
+    const int k = c < 2 ? 0 : 1;
+    const double st[6] = {0.0, has[1] ? coef[(8 + k) * n + v - W] : 0.0,
+                          has[2] ? coef[(6 + k) * n + v - 1] : 0.0,
+                          has[3] ? coef[(6 + k) * n + v] : 0.0,
+                          has[4] ? coef[(8 + k) * n + v] : 0.0, 0.0};
+    const int row = f * nc + c;
+    int q = row_ptr[row];
+    double r = wv * t10[(6 + c) * n + v];
+    for (int a = 0; a < 7; ++a) {
+      if (a == 3) {  // the vertex's own block
+        for (int c2 = 0; c2 < nc; ++c2) {
+          cols[q] = f * nc + c2;
+          vals[q] = coef[plane[c][c2] * n + v];
+          ++q;
+        }
+        continue;
+      }
+      const int e = a < 3 ? a : a - 1;
+      if (!has[e]) continue;
+      const int w = nbv[e];
+      const int fw = vert_to_free[w];
+      if (fw >= 0) {
+        cols[q] = fw * nc + c;
+        vals[q] = st[e];
+        ++q;
+      } else {
+        r -= st[e] * g[static_cast<size_t>(w) * nc + c];
+      }
+    }
+    rhs[row] = r;
+  }
+}
+
 constexpr int kT = 128;
 
 }  // namespace
@@ -212,6 +267,15 @@ void planes_to_inter(const double* p3, double* x, long long N, int nc, cudaStrea
 
 void inter_to_planes(const double* x, double* p3, long long N, int nc, cudaStream_t st) {
   k_inter_to_planes<<<(N + 255) / 256, 256, 0, st>>>(x, p3, N, nc);
+  FFB_LAUNCHED();
+}
+
+void csr_fill(const double* coef, const double* t10, int W, int H, int nc, int n_free,
+              const int* free_to_vert, const int* vert_to_free, const int* row_ptr,
+              const double* g, int* cols, double* vals, double* rhs, cudaStream_t st) {
+  if (n_free <= 0) return;
+  k_csr_fill<<<(n_free + 127) / 128, 128, 0, st>>>(coef, t10, W, H, nc, n_free, free_to_vert,
+                                                   vert_to_free, row_ptr, g, cols, vals, rhs);
   FFB_LAUNCHED();
 }
 

@@ -6,14 +6,29 @@
 // by the symmetric additive Schwarz operator M^-1 = sum_i R_i^T A_i^-1 R_i (the
 // reference's RAS is nonsymmetric and cannot precondition CG).
 //
-// Four kernels per iteration, no host round trip: spmv_p (p = z + beta p fused into the
-// matrix-free operator, p.Ap), update (x, r, r.r), asm (band solves, band.cu), combine
-// (z = sum of subdomain solutions in ascending subdomain order, r.z). Scalars live in a
-// device control block; every reduction writes per-CTA partials and the last CTA to
-// finish sums them in a fixed order, so results are bitwise reproducible run to run.
+// Per iteration: spmv_p (p = z + beta p fused into the matrix-free operator, p.Ap), update
+// (x, r, r.r), asm (band solves, band.cu), combine (z = sum of the subdomain solutions, r.z).
+//
+// Multi-GPU layout (one rank per GPU, capi.cpp): rank r owns a band of subdomain ROWS
+// [j0, j1) and the pixel rows [y0, y1) of their cores. Every kernel works on the owned rows;
+// the halos a rank needs are neighbour rows exchanged between the kernels (r on the rows its
+// subdomains' free rectangles reach into, p/z on one row, and the partial sums of z on the
+// rows its subdomains cover in the neighbour's band).
+//
+// Reductions are WORLD-INDEPENDENT: the reduction unit is a subdomain row j (its core rows,
+// full width) processed by a fixed number kCU of CTAs with a fixed thread -> pixel map; the
+// unit's value is the sum of its CTAs' partials in CTA order (computed by the last CTA to
+// finish), and the global value the sum of the units in j order (k_scalar, after an
+// all-reduce of the unit values when world > 1: every unit is non-zero on exactly one rank,
+// so the all-reduce is exact). The z combine sums the subdomains covering a pixel row-pair
+// by row-pair, (z_{j,i} + z_{j,i+1}) + (z_{j+1,i} + z_{j+1,i+1}), so a row-pair computed on
+// the neighbouring rank enters the same expression. Hence every scalar, iterate and the
+// iteration count are bitwise identical for any number of GPUs, and run to run.
 // Once converged (or failed) every kernel returns at entry, so the host may enqueue
 // several iterations ahead and only reads the control block between chunks.
 #include "ffb_internal.cuh"
+
+#include <algorithm>
 
 namespace ffb {
 
@@ -42,11 +57,89 @@ __device__ __forceinline__ bool arrive_last(unsigned* counter) {
   return t == gridDim.x - 1;
 }
 
-// fixed-order sum of gridDim.x partials by one block
-__device__ __forceinline__ double final_sum(const double* part, int nparts, double* sm) {
-  double v = 0.0;
-  for (int i = threadIdx.x; i < nparts; i += T) v += __ldcg(part + i);
-  return block_sum(v, sm);
+enum Stage { kStInit = 0, kStPap, kStRr, kStRz };
+
+// the scalar recurrences of cg_solve (linsolve.cpp:314-357) once a reduction is complete;
+// s2 only for kStInit (r.r next to b.b)
+__device__ void apply_stage(PcgCtl* ctl, int stage, double s, double s2) {
+  switch (stage) {
+    case kStInit:
+      ctl->bb = s;
+      ctl->rr = s2;
+      ctl->normb = sqrt(s);
+      ctl->k = 0;
+      ctl->iters = 0;
+      ctl->err = 0;
+      if (s == 0.0) {  // linsolve.cpp:321-324
+        ctl->zero_rhs = 1;
+        ctl->res = 0.0;
+        ctl->done = 1;
+      } else {
+        ctl->res = sqrt(s2) / ctl->normb;
+        ctl->done = ctl->res <= ctl->tol ? 1 : 0;
+      }
+      break;
+    case kStPap:
+      ctl->pAp = s;
+      break;
+    case kStRr:
+      ctl->rr = s;
+      ctl->res = sqrt(s) / ctl->normb;
+      ctl->iters = ctl->k;
+      if (ctl->res <= ctl->tol || ctl->k >= ctl->max_iters) ctl->done = 1;
+      break;
+    case kStRz:
+      ctl->rz_old = ctl->rz;
+      ctl->rz = s;
+      ctl->k += 1;
+      break;
+  }
+}
+
+// Last CTA of a reduction kernel: unit values ur[j] (j in the rank's units) as the CTA-order
+// sum of part[], then, if `finish` (world == 1), the j-order total and the scalar update.
+// part2/ur2 carry a second simultaneous reduction (k_init) or are null.
+__device__ void finish_units(const RankRows& g, int py, const double* part, double* ur,
+                             const double* part2, double* ur2, int finish, PcgCtl* ctl,
+                             int stage) {
+  const int nu = g.j1 - g.j0;
+  for (int u = threadIdx.x; u < nu; u += blockDim.x) {
+    double a = 0.0, b = 0.0;
+    for (int c = 0; c < kCU; ++c) {
+      a += __ldcg(part + u * kCU + c);
+      if (part2) b += __ldcg(part2 + u * kCU + c);
+    }
+    ur[g.j0 + u] = a;
+    if (ur2) ur2[g.j0 + u] = b;
+  }
+  if (!finish) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int j = 0; j < py; ++j) {
+      a += ur[j];
+      if (ur2) b += ur2[j];
+    }
+    apply_stage(ctl, stage, a, b);
+  }
+}
+
+// (unit, CTA-in-unit) of this block; the unit's pixels are its core rows, full width
+struct UnitRange {
+  long long v0;  // first pixel
+  int n;         // pixels
+  int c;         // CTA index within the unit
+  int u;         // unit index relative to j0
+};
+__device__ __forceinline__ UnitRange unit_of_block(const RankRows& g, const int* __restrict__ ys,
+                                                   int W) {
+  UnitRange r;
+  r.u = blockIdx.x / kCU;
+  r.c = blockIdx.x - r.u * kCU;
+  const int j = g.j0 + r.u;
+  r.v0 = static_cast<long long>(ys[j]) * W;
+  r.n = (ys[j + 1] - ys[j]) * W;
+  return r;
 }
 
 struct Vtx {
@@ -96,17 +189,20 @@ __device__ __forceinline__ void load3(const double* __restrict__ a, long long v,
   for (int c = 0; c < NC; ++c) o[c] = a[v * NC + c];
 }
 
-// r = b - A x ; b.b ; r.r   (linsolve.cpp:314-327)
+// r = b - A x ; b.b ; r.r   (linsolve.cpp:314-327), on the owned rows
 template <int NC>
 __global__ void __launch_bounds__(T) k_init(const double* __restrict__ coef,
                                             const double* __restrict__ b,
                                             const double* __restrict__ x, double* __restrict__ r,
-                                            int W, int H, PcgCtl* ctl, double* part) {
+                                            int W, int H, RankRows g, const int* __restrict__ ys,
+                                            int py, PcgCtl* ctl, double* part, double* ur,
+                                            int finish) {
   __shared__ double sm[32];
   const size_t n = static_cast<size_t>(W) * H;
+  const UnitRange ur_ = unit_of_block(g, ys, W);
   double bb = 0.0, rr = 0.0;
-  for (long long v = static_cast<long long>(blockIdx.x) * T + threadIdx.x;
-       v < static_cast<long long>(n); v += static_cast<long long>(gridDim.x) * T) {
+  for (int i = ur_.c * T + threadIdx.x; i < ur_.n; i += kCU * T) {
+    const long long v = ur_.v0 + i;
     Vtx q{static_cast<int>(v % W), static_cast<int>(v / W), v};
     double pc[3], pd[3] = {0, 0, 0}, pl[3] = {0, 0, 0}, pr[3] = {0, 0, 0}, pu[3] = {0, 0, 0};
     load3<NC>(x, v, pc);
@@ -128,54 +224,89 @@ __global__ void __launch_bounds__(T) k_init(const double* __restrict__ coef,
   bb = block_sum(bb, sm);
   rr = block_sum(rr, sm);
   __shared__ bool last;
+  double* part2 = part + static_cast<long long>(gridDim.x);
   if (threadIdx.x == 0) {
     part[blockIdx.x] = bb;
-    part[gridDim.x + blockIdx.x] = rr;
+    part2[blockIdx.x] = rr;
     last = arrive_last(&ctl->counter[0]);
   }
   __syncthreads();
   if (!last) return;
-  const double BB = final_sum(part, gridDim.x, sm);
-  const double RR = final_sum(part + gridDim.x, gridDim.x, sm);
-  if (threadIdx.x == 0) {
-    ctl->counter[0] = 0;
-    ctl->bb = BB;
-    ctl->rr = RR;
-    ctl->normb = sqrt(BB);
-    ctl->k = 0;
-    ctl->iters = 0;
-    ctl->err = 0;
-    if (BB == 0.0) {  // linsolve.cpp:321-324
-      ctl->zero_rhs = 1;
-      ctl->res = 0.0;
-      ctl->done = 1;
-    } else {
-      ctl->res = sqrt(RR) / ctl->normb;
-      ctl->done = ctl->res <= ctl->tol ? 1 : 0;
-    }
+  if (threadIdx.x == 0) ctl->counter[0] = 0;
+  finish_units(g, py, part, ur, part2, ur + py, finish, ctl, kStInit);
+}
+
+// S_j(v) = sum over the column-subdomains i of row j covering pixel (x, y), ascending i
+template <int NC>
+__device__ __forceinline__ void row_pair_sum(const SubInfo* __restrict__ subs, int px, int j,
+                                             int ly, const AxisMap& cm,
+                                             const double* __restrict__ zlocal, double* acc) {
+  bool first = true;
+#pragma unroll
+  for (int ii = 0; ii < 2; ++ii) {
+    const int i = ii ? cm.p1 : cm.p0;
+    if (i < 0) continue;
+    const int lx = ii ? cm.l1 : cm.l0;
+    const SubInfo& s = subs[j * px + i];
+    const long long vl = s.xfast ? static_cast<long long>(ly) * s.fw + lx
+                                 : static_cast<long long>(lx) * s.fh + ly;
+    const double* zl = zlocal + s.vec_off + vl * NC;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = first ? zl[c] : acc[c] + zl[c];
+    first = false;
   }
 }
 
-// combine: z = sum_i R_i^T z_i (ascending subdomain id), r.z; k++
-// With a shard [s_lo, s_hi) (multi-GPU) only this rank's subdomains contribute and the
-// result is a partial z that the host all-reduces before k_rz forms r.z.
+// The partial sums of this rank's subdomains on the neighbours' rows it covers: rows
+// [fa0, fa1) above (covered by subdomain row j0 only) and [fb0, fb1) below (row j1 - 1 only),
+// sent to rank - 1 / rank + 1 before their combine.
+template <int NC>
+__global__ void __launch_bounds__(T)
+    k_zpart(const SubInfo* __restrict__ subs, const AxisMap* __restrict__ colmap,
+            const AxisMap* __restrict__ rowmap, int px, const double* __restrict__ zlocal, int W,
+            RankRows g, double* __restrict__ send_up, double* __restrict__ send_dn,
+            const PcgCtl* ctl) {
+  if (ctl->done | ctl->err) return;
+  const int na = (g.fa1 - g.fa0) * W, nb = (g.fb1 - g.fb0) * W;
+  for (int k = blockIdx.x * T + threadIdx.x; k < na + nb; k += gridDim.x * T) {
+    const bool up = k < na;
+    const int kk = up ? k : k - na;
+    const int y = (up ? g.fa0 : g.fb0) + kk / W, x = kk % W;
+    const int j = up ? g.j0 : g.j1 - 1;
+    const AxisMap rm = rowmap[y];
+    const int ly = rm.p0 == j ? rm.l0 : rm.l1;
+    double acc[3];
+    row_pair_sum<NC>(subs, px, j, ly, colmap[x], zlocal, acc);
+    double* out = (up ? send_up : send_dn) + static_cast<long long>(kk) * NC;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) out[c] = acc[c];
+  }
+}
+
+// combine on the owned rows: z = S_j0 (+ S_j1) over the (<= 2) subdomain rows covering the
+// pixel, ascending j; an S of a subdomain row owned by a neighbour comes from its k_zpart
+// (recv_up: rows [ra0, ra1) from rank - 1; recv_dn: rows [rb0, rb1) from rank + 1). r.z.
+// Two-level (world == 1 only): + the core's coarse value yc (coarse.cu).
 template <int NC>
 __global__ void __launch_bounds__(T) k_combine(const SubInfo* __restrict__ subs,
                                                const AxisMap* __restrict__ colmap,
                                                const AxisMap* __restrict__ rowmap, int px,
                                                const double* __restrict__ zlocal,
                                                const double* __restrict__ r,
-                                               double* __restrict__ z, int W, int H,
-                                               PcgCtl* ctl, double* part, int s_lo, int s_hi,
-                                               int partial, const double* __restrict__ yc,
+                                               double* __restrict__ z, int W, RankRows g,
+                                               const int* __restrict__ ys, int py,
+                                               const double* __restrict__ recv_up,
+                                               const double* __restrict__ recv_dn, PcgCtl* ctl,
+                                               double* part, double* ur, int finish,
+                                               const double* __restrict__ yc,
                                                const int* __restrict__ ccol,
                                                const int* __restrict__ crow) {
   if (ctl->done | ctl->err) return;
   __shared__ double sm[32];
-  const size_t n = static_cast<size_t>(W) * H;
+  const UnitRange ur_ = unit_of_block(g, ys, W);
   double rz = 0.0;
-  for (long long v = static_cast<long long>(blockIdx.x) * T + threadIdx.x;
-       v < static_cast<long long>(n); v += static_cast<long long>(gridDim.x) * T) {
+  for (int i = ur_.c * T + threadIdx.x; i < ur_.n; i += kCU * T) {
+    const long long v = ur_.v0 + i;
     const int x = static_cast<int>(v % W), y = static_cast<int>(v / W);
     const AxisMap cm = colmap[x], rm = rowmap[y];
     double acc[3] = {0.0, 0.0, 0.0};
@@ -183,21 +314,20 @@ __global__ void __launch_bounds__(T) k_combine(const SubInfo* __restrict__ subs,
     for (int jj = 0; jj < 2; ++jj) {
       const int j = jj ? rm.p1 : rm.p0;
       if (j < 0) continue;
-      const int ly = jj ? rm.l1 : rm.l0;
+      double s[3];
+      if (j < g.j0) {
+        const double* f = recv_up + (static_cast<long long>(y - g.ra0) * W + x) * NC;
 #pragma unroll
-      for (int ii = 0; ii < 2; ++ii) {
-        const int i = ii ? cm.p1 : cm.p0;
-        if (i < 0) continue;
-        const int lx = ii ? cm.l1 : cm.l0;
-        const int sid = j * px + i;
-        if (sid < s_lo || sid >= s_hi) continue;
-        const SubInfo& s = subs[sid];
-        const long long vl = s.xfast ? static_cast<long long>(ly) * s.fw + lx
-                                     : static_cast<long long>(lx) * s.fh + ly;
-        const double* zl = zlocal + s.vec_off + vl * NC;
+        for (int c = 0; c < NC; ++c) s[c] = f[c];
+      } else if (j >= g.j1) {
+        const double* f = recv_dn + (static_cast<long long>(y - g.rb0) * W + x) * NC;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) acc[c] += zl[c];
+        for (int c = 0; c < NC; ++c) s[c] = f[c];
+      } else {
+        row_pair_sum<NC>(subs, px, j, jj ? rm.l1 : rm.l0, cm, zlocal, s);
       }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) acc[c] = jj ? acc[c] + s[c] : s[c];
     }
     if (yc) {  // two-level: + Z A0^-1 Z^T r (coarse.cu), the core's coarse value
       const double* yv = yc + static_cast<long long>(ccol[x] + crow[y]) * NC;
@@ -210,7 +340,6 @@ __global__ void __launch_bounds__(T) k_combine(const SubInfo* __restrict__ subs,
       rz += r[v * NC + c] * acc[c];
     }
   }
-  if (partial) return;
   rz = block_sum(rz, sm);
   __shared__ bool last;
   if (threadIdx.x == 0) {
@@ -219,48 +348,20 @@ __global__ void __launch_bounds__(T) k_combine(const SubInfo* __restrict__ subs,
   }
   __syncthreads();
   if (!last) return;
-  const double RZ = final_sum(part, gridDim.x, sm);
-  if (threadIdx.x == 0) {
-    ctl->counter[1] = 0;
-    ctl->rz_old = ctl->rz;
-    ctl->rz = RZ;
-    ctl->k += 1;
-  }
+  if (threadIdx.x == 0) ctl->counter[1] = 0;
+  finish_units(g, py, part, ur, nullptr, nullptr, finish, ctl, kStRz);
 }
 
-// r.z of the all-reduced z (multi-GPU stage B); k++
-__global__ void __launch_bounds__(T) k_rz(const double* __restrict__ r,
-                                          const double* __restrict__ z, long long nvec,
-                                          PcgCtl* ctl, double* part) {
-  if (ctl->done | ctl->err) return;
-  __shared__ double sm[32];
-  double rz = 0.0;
-  for (long long i = static_cast<long long>(blockIdx.x) * T + threadIdx.x; i < nvec;
-       i += static_cast<long long>(gridDim.x) * T)
-    rz += r[i] * z[i];
-  rz = block_sum(rz, sm);
-  __shared__ bool last;
-  if (threadIdx.x == 0) {
-    part[blockIdx.x] = rz;
-    last = arrive_last(&ctl->counter[1]);
-  }
-  __syncthreads();
-  if (!last) return;
-  const double RZ = final_sum(part, gridDim.x, sm);
-  if (threadIdx.x == 0) {
-    ctl->counter[1] = 0;
-    ctl->rz_old = ctl->rz;
-    ctl->rz = RZ;
-    ctl->k += 1;
-  }
-}
-
-// p = z + beta p (beta = rz/rz_old, p = z on the first iteration); q = A p; p.q
+// p = z + beta p (beta = rz/rz_old, p = z on the first iteration); q = A p; p.q on the owned
+// rows. p is also written on the (<= 1) halo row on each side, so the next iteration's
+// stencil finds its old value there.
 template <int NC>
 __global__ void __launch_bounds__(T) k_spmv_p(const double* __restrict__ coef,
                                               const double* __restrict__ z, double* __restrict__ P0,
                                               double* __restrict__ P1, double* __restrict__ qv,
-                                              int W, int H, PcgCtl* ctl, double* part) {
+                                              int W, int H, RankRows g,
+                                              const int* __restrict__ ys, int py, PcgCtl* ctl,
+                                              double* part, double* ur, int finish) {
   if (ctl->done | ctl->err) return;
   __shared__ double sm[32];
   const int k = ctl->k;
@@ -268,15 +369,16 @@ __global__ void __launch_bounds__(T) k_spmv_p(const double* __restrict__ coef,
   const double* __restrict__ pold = (k & 1) ? P1 : P0;
   double* __restrict__ pnew = (k & 1) ? P0 : P1;
   const size_t n = static_cast<size_t>(W) * H;
-  double pq = 0.0;
-  for (long long v = static_cast<long long>(blockIdx.x) * T + threadIdx.x;
-       v < static_cast<long long>(n); v += static_cast<long long>(gridDim.x) * T) {
-    Vtx q{static_cast<int>(v % W), static_cast<int>(v / W), v};
-    auto pn = [&](long long w, double* o) {
+  auto pn = [&](long long w, double* o) {
 #pragma unroll
-      for (int c = 0; c < NC; ++c)
-        o[c] = k == 1 ? z[w * NC + c] : z[w * NC + c] + beta * pold[w * NC + c];
-    };
+    for (int c = 0; c < NC; ++c)
+      o[c] = k == 1 ? z[w * NC + c] : z[w * NC + c] + beta * pold[w * NC + c];
+  };
+  const UnitRange ur_ = unit_of_block(g, ys, W);
+  double pq = 0.0;
+  for (int i = ur_.c * T + threadIdx.x; i < ur_.n; i += kCU * T) {
+    const long long v = ur_.v0 + i;
+    Vtx q{static_cast<int>(v % W), static_cast<int>(v / W), v};
     double pc[3], pd[3] = {0, 0, 0}, pl[3] = {0, 0, 0}, pr[3] = {0, 0, 0}, pu[3] = {0, 0, 0};
     pn(v, pc);
     if (q.y > 0) pn(v - W, pd);
@@ -292,6 +394,16 @@ __global__ void __launch_bounds__(T) k_spmv_p(const double* __restrict__ coef,
       pq += pc[c] * ap[c];
     }
   }
+  // halo rows of p (outside the owned band, inside the image)
+  const int hu = g.y0 > 0 ? 1 : 0, hd = g.y1 < H ? 1 : 0;
+  for (int i = blockIdx.x * T + threadIdx.x; i < (hu + hd) * W; i += gridDim.x * T) {
+    const int y = (i < hu * W) ? g.y0 - 1 : g.y1;
+    const long long v = static_cast<long long>(y) * W + (i % W);
+    double pc[3];
+    pn(v, pc);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) pnew[v * NC + c] = pc[c];
+  }
   pq = block_sum(pq, sm);
   __shared__ bool last;
   if (threadIdx.x == 0) {
@@ -300,20 +412,18 @@ __global__ void __launch_bounds__(T) k_spmv_p(const double* __restrict__ coef,
   }
   __syncthreads();
   if (!last) return;
-  const double PQ = final_sum(part, gridDim.x, sm);
-  if (threadIdx.x == 0) {
-    ctl->counter[2] = 0;
-    ctl->pAp = PQ;
-  }
+  if (threadIdx.x == 0) ctl->counter[2] = 0;
+  finish_units(g, py, part, ur, nullptr, nullptr, finish, ctl, kStPap);
 }
 
-// x += alpha p ; r -= alpha q ; r.r ; convergence test (linsolve.cpp:335-349)
+// x += alpha p ; r -= alpha q ; r.r ; convergence test (linsolve.cpp:335-349), owned rows
 template <int NC>
 __global__ void __launch_bounds__(T) k_update(double* __restrict__ x, double* __restrict__ r,
                                               const double* __restrict__ P0,
                                               const double* __restrict__ P1,
-                                              const double* __restrict__ qv, long long nvec,
-                                              int max_iters, PcgCtl* ctl, double* part) {
+                                              const double* __restrict__ qv, int W, RankRows g,
+                                              const int* __restrict__ ys, int py, PcgCtl* ctl,
+                                              double* part, double* ur, int finish) {
   if (ctl->done | ctl->err) return;
   __shared__ double sm[32];
   const int k = ctl->k;
@@ -327,13 +437,18 @@ __global__ void __launch_bounds__(T) k_update(double* __restrict__ x, double* __
   }
   const double alpha = ctl->rz / pAp;
   const double* __restrict__ p = (k & 1) ? P0 : P1;
+  const UnitRange ur_ = unit_of_block(g, ys, W);
   double rr = 0.0;
-  for (long long i = static_cast<long long>(blockIdx.x) * T + threadIdx.x; i < nvec;
-       i += static_cast<long long>(gridDim.x) * T) {
-    x[i] += alpha * p[i];
-    const double ri = r[i] - alpha * qv[i];
-    r[i] = ri;
-    rr += ri * ri;
+  for (int i = ur_.c * T + threadIdx.x; i < ur_.n; i += kCU * T) {
+    const long long v = ur_.v0 + i;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const long long e = v * NC + c;
+      x[e] += alpha * p[e];
+      const double ri = r[e] - alpha * qv[e];
+      r[e] = ri;
+      rr += ri * ri;
+    }
   }
   rr = block_sum(rr, sm);
   __shared__ bool last;
@@ -343,63 +458,94 @@ __global__ void __launch_bounds__(T) k_update(double* __restrict__ x, double* __
   }
   __syncthreads();
   if (!last) return;
-  const double RR = final_sum(part, gridDim.x, sm);
-  if (threadIdx.x == 0) {
-    ctl->counter[3] = 0;
-    ctl->rr = RR;
-    ctl->res = sqrt(RR) / ctl->normb;
-    ctl->iters = k;
-    if (ctl->res <= ctl->tol || k >= max_iters) ctl->done = 1;
+  if (threadIdx.x == 0) ctl->counter[3] = 0;
+  finish_units(g, py, part, ur, nullptr, nullptr, finish, ctl, kStRr);
+}
+
+// after the all-reduce of the unit values (world > 1): the j-order total, the scalar update
+__global__ void k_scalar(const double* __restrict__ ur, int py, int stage, PcgCtl* ctl) {
+  if (ctl->done | ctl->err) return;
+  double a = 0.0, b = 0.0;
+  for (int j = 0; j < py; ++j) {
+    a += ur[j];
+    if (stage == kStInit) b += ur[py + j];
   }
+  apply_stage(ctl, stage, a, b);
 }
 
 }  // namespace
 
+static int grid_of(const RankRows& g) { return (g.j1 - g.j0) * kCU; }
+
 void pcg_init(int nc, const double* coef, const double* b, const double* x, double* r, int W,
-              int H, PcgCtl* ctl, double* part, cudaStream_t st) {
+              int H, const RankRows& g, const int* ys, int py, PcgCtl* ctl, double* part,
+              double* ur, int finish, cudaStream_t st) {
+  if (grid_of(g) == 0) return;
   if (nc == 3)
-    k_init<3><<<kRedBlocks, T, 0, st>>>(coef, b, x, r, W, H, ctl, part);
+    k_init<3><<<grid_of(g), T, 0, st>>>(coef, b, x, r, W, H, g, ys, py, ctl, part, ur, finish);
   else
-    k_init<2><<<kRedBlocks, T, 0, st>>>(coef, b, x, r, W, H, ctl, part);
+    k_init<2><<<grid_of(g), T, 0, st>>>(coef, b, x, r, W, H, g, ys, py, ctl, part, ur, finish);
+  FFB_LAUNCHED();
+}
+
+void pcg_zpart(int nc, const SubInfo* subs, const AxisMap* colmap, const AxisMap* rowmap, int px,
+               const double* zlocal, int W, const RankRows& g, double* send_up, double* send_dn,
+               const PcgCtl* ctl, cudaStream_t st) {
+  const int n = (g.fa1 - g.fa0 + g.fb1 - g.fb0) * W;
+  if (n <= 0) return;
+  const int grid = std::min((n + T - 1) / T, 4 * 148);
+  if (nc == 3)
+    k_zpart<3><<<grid, T, 0, st>>>(subs, colmap, rowmap, px, zlocal, W, g, send_up, send_dn, ctl);
+  else
+    k_zpart<2><<<grid, T, 0, st>>>(subs, colmap, rowmap, px, zlocal, W, g, send_up, send_dn, ctl);
   FFB_LAUNCHED();
 }
 
 void pcg_combine(int nc, const SubInfo* subs, const AxisMap* colmap, const AxisMap* rowmap,
-                 int px, const double* zlocal, const double* r, double* z, int W, int H,
-                 PcgCtl* ctl, double* part, int s_lo, int s_hi, int partial, cudaStream_t st,
-                 const double* yc, const int* ccol, const int* crow) {
+                 int px, const double* zlocal, const double* r, double* z, int W,
+                 const RankRows& g, const int* ys, int py, const double* recv_up,
+                 const double* recv_dn, PcgCtl* ctl, double* part, double* ur, int finish,
+                 cudaStream_t st, const double* yc, const int* ccol, const int* crow) {
+  if (grid_of(g) == 0) return;
   if (nc == 3)
-    k_combine<3><<<kRedBlocks, T, 0, st>>>(subs, colmap, rowmap, px, zlocal, r, z, W, H, ctl, part,
-                                           s_lo, s_hi, partial, yc, ccol, crow);
+    k_combine<3><<<grid_of(g), T, 0, st>>>(subs, colmap, rowmap, px, zlocal, r, z, W, g, ys, py,
+                                           recv_up, recv_dn, ctl, part, ur, finish, yc, ccol, crow);
   else
-    k_combine<2><<<kRedBlocks, T, 0, st>>>(subs, colmap, rowmap, px, zlocal, r, z, W, H, ctl, part,
-                                           s_lo, s_hi, partial, yc, ccol, crow);
-  FFB_LAUNCHED();
-}
-
-void pcg_rz(const double* r, const double* z, long long nvec, PcgCtl* ctl, double* part,
-            cudaStream_t st) {
-  k_rz<<<kRedBlocks, T, 0, st>>>(r, z, nvec, ctl, part);
+    k_combine<2><<<grid_of(g), T, 0, st>>>(subs, colmap, rowmap, px, zlocal, r, z, W, g, ys, py,
+                                           recv_up, recv_dn, ctl, part, ur, finish, yc, ccol, crow);
   FFB_LAUNCHED();
 }
 
 void pcg_spmv_p(int nc, const double* coef, const double* z, double* P0, double* P1, double* q,
-                int W, int H, PcgCtl* ctl, double* part, cudaStream_t st) {
+                int W, int H, const RankRows& g, const int* ys, int py, PcgCtl* ctl, double* part,
+                double* ur, int finish, cudaStream_t st) {
+  if (grid_of(g) == 0) return;
   if (nc == 3)
-    k_spmv_p<3><<<kRedBlocks, T, 0, st>>>(coef, z, P0, P1, q, W, H, ctl, part);
+    k_spmv_p<3><<<grid_of(g), T, 0, st>>>(coef, z, P0, P1, q, W, H, g, ys, py, ctl, part, ur, finish);
   else
-    k_spmv_p<2><<<kRedBlocks, T, 0, st>>>(coef, z, P0, P1, q, W, H, ctl, part);
+    k_spmv_p<2><<<grid_of(g), T, 0, st>>>(coef, z, P0, P1, q, W, H, g, ys, py, ctl, part, ur, finish);
   FFB_LAUNCHED();
 }
 
 void pcg_update(int nc, double* x, double* r, const double* P0, const double* P1,
-                const double* q, long long nvec, int max_iters, PcgCtl* ctl, double* part,
-                cudaStream_t st) {
+                const double* q, int W, const RankRows& g, const int* ys, int py, PcgCtl* ctl,
+                double* part, double* ur, int finish, cudaStream_t st) {
+  if (grid_of(g) == 0) return;
   if (nc == 3)
-    k_update<3><<<kRedBlocks, T, 0, st>>>(x, r, P0, P1, q, nvec, max_iters, ctl, part);
+    k_update<3><<<grid_of(g), T, 0, st>>>(x, r, P0, P1, q, W, g, ys, py, ctl, part, ur, finish);
   else
-    k_update<2><<<kRedBlocks, T, 0, st>>>(x, r, P0, P1, q, nvec, max_iters, ctl, part);
+    k_update<2><<<grid_of(g), T, 0, st>>>(x, r, P0, P1, q, W, g, ys, py, ctl, part, ur, finish);
   FFB_LAUNCHED();
 }
+
+void pcg_scalar(const double* ur, int py, int stage, PcgCtl* ctl, cudaStream_t st) {
+  k_scalar<<<1, 1, 0, st>>>(ur, py, stage, ctl);
+  FFB_LAUNCHED();
+}
+
+int pcg_stage_init() { return kStInit; }
+int pcg_stage_pap() { return kStPap; }
+int pcg_stage_rr() { return kStRr; }
+int pcg_stage_rz() { return kStRz; }
 
 }  // namespace ffb

@@ -6,7 +6,7 @@
 #include "flowfem_b200.hpp"
 
 int main() {
-  namespace ff = flowfem_b200;
+  namespace ff = flowfem;
   const auto s = ff::choose_split(96, 80, 4);
   if (s.parts_x != 2 || s.parts_y != 2) return 1;
   const auto all = ff::enumerate_splits(640, 480, 12);

@@ -58,3 +58,25 @@ def test_cpp_shim_compiles_and_runs(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, (out.returncode, out.stderr)
     assert "shim ok" in out.stdout
+
+
+def test_cpp_mesh_equals_reference(tmp_path):
+    """build_pixel_mesh / p1_gradients of the C++ drop-in (include/flowfem_b200.hpp) produce the
+    same arrays, byte for byte, as the reference's mesh.cpp (compiled from /root/reference in
+    the build container; skipped where the reference is absent)."""
+    import subprocess
+    ref = "/root/reference/proj"
+    if not os.path.isdir(ref):
+        pytest.skip("reference sources not present")
+    src = os.path.join(ROOT, "tests", "cpp", "mesh_dump.cpp")
+    ours, theirs = tmp_path / "ours", tmp_path / "theirs"
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), src, "-o",
+                    str(ours)], check=True, capture_output=True)
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ref, "include"), src,
+                    os.path.join(ref, "src", "mesh.cpp"), "-o", str(theirs)], check=True,
+                   capture_output=True)
+    for W, H in ((2, 2), (5, 3), (17, 11), (64, 40)):
+        a, b = tmp_path / f"a{W}", tmp_path / f"b{H}"
+        subprocess.run([str(ours), str(W), str(H), str(a)], check=True)
+        subprocess.run([str(theirs), str(W), str(H), str(b)], check=True)
+        assert a.read_bytes() == b.read_bytes(), (W, H)
