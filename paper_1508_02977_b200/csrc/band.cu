@@ -948,7 +948,7 @@ __global__ void __launch_bounds__(kFT, 1)
   const int chain = mid ? 0 : cid & 1;
   const SubInfo s = subs[sub];
   const int tid = threadIdx.x;
-  const int kd = s.kd, L = s.L, m = mid_line(L);
+  const int kd = s.kd, L = s.L, m = s.m;
   // lines [lo, hi] of this subdomain whose operator changed since the last factorisation
   // (all of them on a full refactorisation): chain 0 restarts at lo, chain 1 at hi, and the
   // untouched prefix of each chain keeps its inverses (D_l depends on lines <= l only)
@@ -1105,17 +1105,21 @@ __device__ __forceinline__ int chunk_end(int r0, int rhi, long long cap) {
   return r1;
 }
 
-// Lines visited by (phase, chain): forward 0: 0..m-1, forward 1: L-1..m+1;
-// backward c: m first (the middle, computed by both chains), then m-1..0 / m+1..L-1.
-__device__ __forceinline__ int chain_len(int phase, int chain, int L) {
-  const int m = mid_line(L);
-  const int len = chain == 0 ? m : L - 1 - m;
-  return phase == 0 ? len : len + 1;
+// Lines visited by (phase, chain): forward 0: 0..m-1, forward 1: L-1..m+1; backward: the
+// middle m first, then m-1..0 / m+1..L-1. The middle is solved by every chain with a forward
+// part (a chain without one — an unbalanced split, m = 0 or m = L-1 — does nothing) and
+// written by mid_writer(s).
+__device__ __forceinline__ int chain_len(int phase, int chain, const SubInfo& s) {
+  const int len0 = s.m, len1 = s.L - 1 - s.m;
+  const int len = chain == 0 ? len0 : len1;
+  if (phase == 0) return len;
+  if (len > 0) return len + 1;
+  return (chain == 0 && len1 == 0) ? 1 : 0;  // L == 1: chain 0 solves the single line
 }
-__device__ __forceinline__ int chain_line(int phase, int chain, int L, int t) {
-  const int m = mid_line(L);
-  if (phase == 0) return chain == 0 ? t : L - 1 - t;
-  return chain == 0 ? m - t : m + t;
+__device__ __forceinline__ int mid_writer(const SubInfo& s) { return (s.m > 0 || s.L == 1) ? 0 : 1; }
+__device__ __forceinline__ int chain_line(int phase, int chain, const SubInfo& s, int t) {
+  if (phase == 0) return chain == 0 ? t : s.L - 1 - t;
+  return chain == 0 ? s.m - t : s.m + t;
 }
 
 // wait with cluster-scope acquire: pairs with remote release-arrivals from the other CTAs
@@ -1160,24 +1164,28 @@ __device__ __forceinline__ void compute_bar() {
 // Warp 15 is a producer that streams the CTA's share of every line through the shared-memory
 // ring (cp.async.bulk, full/empty mbarriers) independently of the compute warps, so the bulk
 // copy engine keeps running across the per-line reductions.
-template <int MAXM>
+template <int MAXM, bool PERSIST>
 __global__ void __launch_bounds__(kST, 1)
     k_line_solve(const SubInfo* __restrict__ subs, const double* __restrict__ fac,
                  const double* __restrict__ coef, size_t N, const double* __restrict__ r,
                  double* __restrict__ ylocal, double* __restrict__ zlocal, int W, int nc,
                  int stages, int cap, int kd_max, int rc, int phase,
                  const int* __restrict__ flags,
-                 const double* __restrict__ rlocal) {
+                 const double* __restrict__ rlocal, const int2* __restrict__ tasks,
+                 const int* __restrict__ task_ptr) {
   if (flags && (flags[0] | flags[1])) return;  // PCG converged or failed (grid-uniform)
   const int C = static_cast<int>(cl_size()), crank = static_cast<int>(cl_rank());
-  const int cid = blockIdx.x / C;  // (subdomain, chain)
-  const int sub = cid >> 1, chain = cid & 1;
-  const SubInfo s = subs[sub];
+  // the (subdomain, chain) tasks of this CTA: one per cluster, or — the balanced schedule
+  // (C == 1, capi.cpp balance_chains) — the list task_ptr[b] .. task_ptr[b+1], streamed
+  // back to back through the same ring
+  const int tk0 = PERSIST ? task_ptr[blockIdx.x] : 0;
+  const int tk1 = PERSIST ? task_ptr[blockIdx.x + 1] : 1;
+  auto task = [&](int tk) {
+    if (PERSIST) return tasks[tk];
+    const int cid = blockIdx.x / C;
+    return make_int2(cid >> 1, cid & 1);
+  };
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int kd = s.kd, L = s.L, m = mid_line(L);
-  const int nl = chain_len(phase, chain, L);
-  const int rlo = row_lo(crank, C, kd, rc), rhi = row_lo(crank + 1, C, kd, rc);
-  const double* F = fac + s.fac_off;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + 8;
@@ -1194,11 +1202,6 @@ __global__ void __launch_bounds__(kST, 1)
   double* xbuf = yrow + kd_max;                                  // 2 x kd_max (line parity)
   double* red = xbuf + 2 * kd_max;                               // 2 x C x kd_max slots
   double* dcorr = red + 2 * static_cast<size_t>(C) * kd_max;     // kd_max: D_ii w_i
-  double* yl = ylocal + s.vec_off;
-  double* zl = zlocal + s.vec_off;
-  const double* rl = rlocal ? rlocal + s.vec_off : nullptr;  // per-subdomain rhs (RAS mode)
-  if (nl == 0) return;  // cluster-uniform
-
   if (tid == 0) {
     for (int q = 0; q < stages; ++q) {
       mbar_init(&full[q], 1);
@@ -1212,32 +1215,31 @@ __global__ void __launch_bounds__(kST, 1)
     }
     fence_barrier_init();
   }
-  // chunk boundaries of this CTA's rows, the same for every line: cb[0] = rlo < ... <
-  // cb[nch] = rhi, each chunk's packed rows fitting one ring stage
-  int* cb = reinterpret_cast<int*>(smem_raw + 256);
-  int* rlos = reinterpret_cast<int*>(smem_raw + 192);  // row_lo(c) for c = 0..C
-  if (tid <= C) rlos[tid] = row_lo(tid, C, kd, rc);
-  if (tid == 0) {
-    int n = 0, r = rlo;
-    cb[0] = rlo;
-    while (r < rhi && n < kMaxChunks) cb[++n] = r = chunk_end(r, rhi, cap);
-    if (r < rhi) __trap();  // ring stages too small for this line width
-    cb[kMaxChunks] = n;
-  }
+  int* rlos = reinterpret_cast<int*>(smem_raw + 192);  // row_lo(c) for c = 0..C (C > 1)
+  if (C > 1 && tid <= C) rlos[tid] = row_lo(tid, C, subs[task(tk0).x].kd, rc);
   for (int j = tid; j < 2 * kd_max; j += kST) xbuf[j] = 0.0;
   if (C > 1) cl_sync(); else __syncthreads();  // barriers initialised cluster-wide
-  const int nch = cb[kMaxChunks];
 
   // ------------------------------------------------------------------ producer warp
+  // Row chunks of a line: the CTA's rows [rlo, rhi) cut into runs whose packed rows fit one
+  // ring stage (chunk_end), computed on the fly by the producer and the consumers alike.
   if (warp == kCW) {
-    if (rlo >= rhi) return;
-    int q = 0, t_i = 0, r_i = 0;  // r_i: chunk index within the line
+    int q = 0;  // ring slots used so far (continues across tasks)
     int line_of[8];  // line of the chunk last placed in each stage
 #pragma unroll
     for (int k = 0; k < 8; ++k) line_of[k] = -1;
-    auto issue_until = [&](int t_sync) {
-      // place chunks in FIFO order while they belong to lines <= t_sync + 1 and the stage's
-      // previous occupant belongs to a line the consumers finish before barrier t_sync
+    for (int tk = tk0; tk < tk1; ++tk) {
+      const int2 tc = task(tk);
+      const SubInfo s = subs[tc.x];
+      const int chain = tc.y, kd = s.kd, nl = chain_len(phase, chain, s);
+      const int rlo = row_lo(crank, C, kd, rc), rhi = row_lo(crank + 1, C, kd, rc);
+      if (nl == 0 || rlo >= rhi) continue;
+      const double* F = fac + s.fac_off;
+      int t_i = 0, r_a = rlo;  // next chunk: line step t_i, first row r_a
+      // place chunks in FIFO order; with C > 1 only while they belong to lines <= t_sync + 1
+      // and the stage's previous occupant belongs to a line the consumers finish before
+      // barrier t_sync (the gating is moot for one CTA per chain)
+      const int t_sync = 1 << 30;
       while (t_i < nl) {
         if (C > 1 && t_i > t_sync + 1) break;
         const int st = q % stages;
@@ -1247,8 +1249,9 @@ __global__ void __launch_bounds__(kST, 1)
           if (k == st) prev_line = line_of[k];
         if (C > 1 && prev_line > t_sync) break;
         if (q >= stages) mbar_wait(&empty[st], ((q / stages) - 1) & 1);
-        const int l = chain_line(phase, chain, L, t_i);
-        const int o0 = prow_off32(cb[r_i]), o1 = prow_off32(cb[r_i + 1]);
+        const int l = chain_line(phase, chain, s, t_i);
+        const int r_b = chunk_end(r_a, rhi, cap);
+        const int o0 = prow_off32(r_a), o1 = prow_off32(r_b);
         if (lane == 0) {
           if (dbg & 4) {
             mbar_arrive(&full[st]);
@@ -1264,14 +1267,31 @@ __global__ void __launch_bounds__(kST, 1)
         for (int k = 0; k < 8; ++k)
           if (k == st) line_of[k] = t_i;
         ++q;
-        if (++r_i == nch) r_i = 0, ++t_i;
+        r_a = r_b;
+        if (r_a == rhi) r_a = rlo, ++t_i;
       }
-    };
-    issue_until(1 << 30);  // gated by the empty barriers only
+    }
     return;
   }
 
   // ------------------------------------------------------------------ compute warps
+  int c_seq = 0;  // ring slots consumed (continues across tasks)
+  PROF_DECL
+  for (int tk = tk0; tk < tk1; ++tk) {
+  const int2 tc = task(tk);
+  const SubInfo s = subs[tc.x];
+  const int chain = tc.y;
+  const int kd = s.kd, L = s.L, m = s.m;
+  const int nl = chain_len(phase, chain, s);
+  if (nl == 0) continue;  // cluster-uniform
+  const int rlo = row_lo(crank, C, kd, rc), rhi = row_lo(crank + 1, C, kd, rc);
+  double* yl = ylocal + s.vec_off;
+  double* zl = zlocal + s.vec_off;
+  const double* rl = rlocal ? rlocal + s.vec_off : nullptr;  // per-subdomain rhs (RAS mode)
+  if (PERSIST && tk > tk0) {  // x of "line -1" is zero for every task (one CTA per chain)
+    for (int j = tid; j < 2 * kd_max; j += kCT) xbuf[j] = 0.0;
+    compute_bar();
+  }
   // operand of line step t, prefetched into registers one step ahead. Forward:
   // w = r_l - b_prev o y_prev; backward middle: w = r_m - b_m y_{m-1} - b_{m+1} y_{m+1};
   // backward chain: w = b_next o x_next and x_l = y_l - Dinv_l w.
@@ -1282,7 +1302,7 @@ __global__ void __launch_bounds__(kST, 1)
     for (int q = 0; q < PS; ++q) {
       pf_r[q] = pf_b[q] = pf_y[q] = 0.0;
       if (t >= nl) continue;
-      const int l = chain_line(phase, chain, L, t);
+      const int l = chain_line(phase, chain, s, t);
       const int j = tid + kCT * q;
       if (j < kd) {
         if (phase == 0) {
@@ -1303,11 +1323,8 @@ __global__ void __launch_bounds__(kST, 1)
     }
   };
   prefetch(0);
-  PROF_DECL
-
-  int c_seq = 0;
   for (int t = 0; t < nl; ++t) {
-    const int l = chain_line(phase, chain, L, t);
+    const int l = chain_line(phase, chain, s, t);
     const int par = t & 1;
     const bool subtract = phase == 1 && t > 0;  // x_l = y_l - Dinv_l w
     const double* xprev = xbuf + (par ^ 1) * kd_max;  // x of line t-1 (zeros at t = 0)
@@ -1351,8 +1368,8 @@ __global__ void __launch_bounds__(kST, 1)
       wreg[mm].y = j + 1 < kd ? wv[j + 1] : 0.0;
       cacc[mm].x = cacc[mm].y = 0.0;
     }
-    for (int ci = 0; ci < nch; ++ci) {
-      const int r0 = cb[ci], r1 = cb[ci + 1];
+    for (int r0 = rlo, r1 = rlo; r0 < rhi; r0 = r1) {
+      r1 = chunk_end(r0, rhi, cap);
       const int st = c_seq % stages;
       mbar_wait(&full[st], (c_seq / stages) & 1);
       PROF_MARK(1);
@@ -1490,7 +1507,7 @@ __global__ void __launch_bounds__(kST, 1)
         if (phase == 0) {
           yl[k] = v;
           if (L == 1) zl[k] = v;
-        } else if (chain == 0) {
+        } else if (chain == mid_writer(s)) {
           zl[k] = v;  // middle line, written once
         }
       } else {
@@ -1509,6 +1526,7 @@ __global__ void __launch_bounds__(kST, 1)
   // arrivals means no remote store into this CTA's shared memory is still in flight
   if (C > 1 && !(dbg & 2)) mbar_wait_cluster(&x_bar[(nl - 1) & 1], ((nl - 1) >> 1) & 1);
   if (C > 1 && (dbg & 2)) cl_sync();
+  }  // tasks
   PROF_FLUSH(16);
 }
 
@@ -1597,8 +1615,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   const int sub = cid >> 1, chain = cid & 1;
   const SubInfo s = subs[sub];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int kd = s.kd, L = s.L, m = mid_line(L);
-  const int nl = chain_len(phase, chain, L);
+  const int kd = s.kd, L = s.L, m = s.m;
+  const int nl = chain_len(phase, chain, s);
   if (nl == 0) return;  // cluster-uniform
   const int nt = (kd + 31) >> 5, kdp = nt * 32;
   const int ci = C == 1 ? 0 : (C == 2 ? 1 : (C == 4 ? 2 : 3));
@@ -1700,12 +1718,12 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   // own region, after its own reads of line t - 2), line step t + 1 into L2; lane 0 only
   auto issue_tile = [&](int t) {
     if (!has_tile || t >= nl || (dbg & 4)) return;
-    const double* Fl = F + static_cast<long long>(chain_line(phase, chain, L, t)) * s.line_sz;
+    const double* Fl = F + static_cast<long long>(chain_line(phase, chain, s, t)) * s.line_sz;
     fence_proxy_async();
     bulk_g2s(stage + static_cast<size_t>(t & 1) * stage_doubles + my_off, Fl + my_src,
              static_cast<uint32_t>(my_sz) * 8u, &full[t & 1]);
     if (t + 1 < nl)
-      bulk_prefetch_l2(F + static_cast<long long>(chain_line(phase, chain, L, t + 1)) * s.line_sz + my_src,
+      bulk_prefetch_l2(F + static_cast<long long>(chain_line(phase, chain, s, t + 1)) * s.line_sz + my_src,
                        static_cast<uint32_t>(my_sz) * 8u);
   };
   if (tid == 0 && !(dbg & 4)) {
@@ -1720,7 +1738,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   if (tid < kdp) {
     double w = 0.0;
     if (tid < kd) {
-      const int l = chain_line(phase, chain, L, 0);
+      const int l = chain_line(phase, chain, s, 0);
       w = r_at(l, tid);
       if (phase == 1) {
         if (m > 0) w -= b_at(m, tid) * yl[static_cast<long long>(m - 1) * kd + tid];
@@ -1740,12 +1758,12 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       if ((q == 0 ? ob0 : ob1) < 0 || i >= kd) continue;
       double b = 0.0, rr = 0.0, y = 0.0;
       if (tw < nl) {
-        const int l = chain_line(phase, chain, L, tw);
+        const int l = chain_line(phase, chain, s, tw);
         b = b_at(phase == 0 ? (chain == 0 ? l : l + 1) : (chain == 0 ? l + 1 : l), i);
         if (phase == 0) rr = r_at(l, i);
       }
       if (phase == 1 && ty >= 1 && ty < nl)
-        y = yl[static_cast<long long>(chain_line(phase, chain, L, ty)) * kd + i];
+        y = yl[static_cast<long long>(chain_line(phase, chain, s, ty)) * kd + i];
       if (q == 0) pb0 = b, pr0 = rr, py0 = y; else pb1 = b, pr1 = rr, py1 = y;
     }
   };
@@ -1754,7 +1772,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   PROF_DECL
 
   for (int t = 0; t < nl; ++t) {
-    const int l = chain_line(phase, chain, L, t);
+    const int l = chain_line(phase, chain, s, t);
     const uint32_t par = t & 1;
     if (t > 0) mbar_wait_g(&w_bar[par], ((t - 1) >> 1) & 1);  // operand of line t, all owners
     const double* wt = wv + par * kdp_max;
@@ -1930,7 +1948,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         if (phase == 0) {
           yl[e] = v;
           if (L == 1) zl[e] = v;
-        } else if (t > 0 || chain == 0) {
+        } else if (t > 0 || chain == mid_writer(s)) {
           zl[e] = v;  // (t == 0: the middle line, written once)
         }
       }
@@ -2261,7 +2279,8 @@ template <int M>
 static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
                            const double* fac, const double* coef, size_t N, const double* r,
                            double* ylocal, double* zlocal, int W, int nc, const int* flags,
-                           const double* rlocal, cudaStream_t st) {
+                           const double* rlocal, cudaStream_t st, const int2* tasks,
+                           const int* task_ptr, int nseg) {
   for (int phase = 0; phase <= 1; ++phase) {
     if (pl.tile) {
       set_tile_tables();
@@ -2269,9 +2288,16 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
                      fac, coef, N, r, ylocal, zlocal, W, nc, (pl.maxm) * 32, pl.stage_doubles,
                      phase, flags, rlocal);
     } else {
-      launch_cluster(k_line_solve<M>, 2 * nsub * pl.C, kST, pl.smem, pl.C, st, d_subs, fac, coef,
-                     N, r, ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, pl.row_cost,
-                     phase, flags, rlocal);
+      // balanced schedule (one CTA per chain): `nseg` persistent CTAs, each streaming its
+      // task list; else one cluster per (subdomain, chain)
+      if (tasks)
+        launch_cluster(k_line_solve<M, true>, nseg, kST, pl.smem, 1, st, d_subs, fac, coef, N, r,
+                       ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, pl.row_cost, phase,
+                       flags, rlocal, tasks, task_ptr);
+      else
+        launch_cluster(k_line_solve<M, false>, 2 * nsub * pl.C, kST, pl.smem, pl.C, st, d_subs,
+                       fac, coef, N, r, ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max,
+                       pl.row_cost, phase, flags, rlocal, tasks, task_ptr);
     }
     FFB_LAUNCHED();
   }
@@ -2279,18 +2305,25 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
 
 void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,
                 const double* coef, size_t N, const double* r, double* ylocal, double* zlocal,
-                int W, int nc, const int* flags, cudaStream_t st, const double* rlocal) {
+                int W, int nc, const int* flags, cudaStream_t st, const double* rlocal,
+                const int2* tasks, const int* task_ptr, int nseg) {
+  if (pl.tile || pl.C != 1) tasks = nullptr, task_ptr = nullptr;  // balanced: ring, C == 1
   if (nsub <= 0) return;  // a rank without subdomains (world > parts)
   if (pl.maxm <= 4)
-    launch_solve_m<4>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st);
+    launch_solve_m<4>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
+                      tasks, task_ptr, nseg);
   else if (pl.maxm <= 8)
-    launch_solve_m<8>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st);
+    launch_solve_m<8>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
+                      tasks, task_ptr, nseg);
   else if (pl.maxm <= 14)
-    launch_solve_m<14>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st);
+    launch_solve_m<14>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
+                      tasks, task_ptr, nseg);
   else if (pl.maxm <= 20)
-    launch_solve_m<20>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st);
+    launch_solve_m<20>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
+                      tasks, task_ptr, nseg);
   else if (pl.maxm <= 26)
-    launch_solve_m<26>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st);
+    launch_solve_m<26>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
+                      tasks, task_ptr, nseg);
   else
     fail("linsolve.cholesky: subdomain line too wide (kd > 832)");
 }

@@ -113,6 +113,10 @@ struct ffb_ctx {
   int up = -1, dn = -1;  // nearest non-empty ranks above / below (-1: none)
   std::vector<size_t> gather_off, gather_cnt;  // owned rows of every rank, in doubles / W nc
   int s_lo = 0, s_hi = 0;
+  // balanced schedule of the ring solve (balance_chains): per persistent CTA a task list
+  int nseg = 0;
+  DBuf<int2> d_tasks;
+  DBuf<int> d_task_ptr;
   DBuf<double> ur, urs, zs_up, zs_dn, zr_up, zr_dn;
   int stage_nc = 0, stage_max_iters = 0;
   double stage_tol = 0;
@@ -282,6 +286,59 @@ RankRows rank_rows(const Partition& P, int rank, int world) {
   return g;
 }
 
+// Balanced twisted splits for the ring solve with one CTA per chain (c3-c5 shapes). Every
+// chain is a sequential pass over its lines, so with 2 chains per subdomain and one CTA per SM
+// the launch runs in ceil(2 nsub / #SMs) rounds and the last one is partly empty (c4: 512
+// chains on 148 SMs = 3.46 rounds, 86% occupancy). Instead, the rank's subdomains' line steps
+// (L_i - 1 each, the middle line apart) are laid end to end and cut into #SMs equal segments;
+// a subdomain a cut falls into is split there (its middle line m_i = the cut), the others run
+// as one chain (m_i = L_i - 1), and each segment becomes the task list of one persistent CTA.
+// The factor follows the same m_i. Used when every segment is longer than any subdomain, so a
+// subdomain is cut at most once; FFB_NO_BALANCE=1 keeps the middle split.
+void balance_chains(ffb_ctx* c) {
+  c->nseg = 0;
+  if (c->plan.tile || c->ccl != 1 || std::getenv("FFB_NO_BALANCE")) return;
+  int nsm = 0;
+  FFB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+  long long T = 0;
+  int nmax = 0;
+  for (int p = c->s_lo; p < c->s_hi; ++p) {
+    T += c->subs[p].L - 1;
+    nmax = std::max(nmax, c->subs[p].L - 1);
+  }
+  if (nsm < 1 || T < static_cast<long long>(nsm) * (nmax + 2)) return;
+  auto cut = [&](int k) { return (static_cast<long long>(k) * T + nsm / 2) / nsm; };
+  std::vector<int2> tasks;
+  std::vector<int> ptr(nsm + 1, 0);
+  int seg = 0;
+  long long g = 0, next = cut(1);
+  for (int p = c->s_lo; p < c->s_hi; ++p) {
+    SubInfo& s = c->subs[p];
+    const int n = s.L - 1, rel = p - c->s_lo;
+    if (n > 0 && next > g && next < g + n) {  // split: chain 0 ends this segment
+      s.m = static_cast<int>(next - g);
+      tasks.push_back(make_int2(rel, 0));
+      ptr[++seg] = static_cast<int>(tasks.size());
+      next = cut(seg + 1);
+      tasks.push_back(make_int2(rel, 1));   // chain 1 opens the next one
+    } else {
+      s.m = n;  // one chain: lines 0..L-2, the last line closes it
+      tasks.push_back(make_int2(rel, 0));
+      if (seg < nsm - 1 && next == g + n) {
+        ptr[++seg] = static_cast<int>(tasks.size());
+        next = cut(seg + 1);
+      }
+    }
+    g += n;
+  }
+  while (seg < nsm) ptr[++seg] = static_cast<int>(tasks.size());
+  c->nseg = nsm;
+  FFB_CUDA(cudaMemcpyAsync(c->d_tasks.ensure(tasks.size()), tasks.data(), tasks.size() * sizeof(int2),
+                           cudaMemcpyHostToDevice, c->st));
+  FFB_CUDA(cudaMemcpyAsync(c->d_task_ptr.ensure(ptr.size()), ptr.data(), ptr.size() * sizeof(int),
+                           cudaMemcpyHostToDevice, c->st));
+}
+
 void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
   if (c->have_part && c->part_px == px && c->part_py == py && c->part_ov == ov &&
       c->part_nc == nc)
@@ -325,12 +382,13 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
     c->up = c->dn = -1;
     c->gather_off.assign(world, 0);
     c->gather_cnt.assign(world, 0);
+    const bool live = c->rows.j1 > c->rows.j0;  // a rank without subdomains exchanges nothing
     for (int q = 0; q < world; ++q) {
       const RankRows gq = rank_rows(c->decomp, q, world);
       c->gather_off[q] = static_cast<size_t>(gq.y0) * W * nc;
       c->gather_cnt[q] = static_cast<size_t>(gq.y1 - gq.y0) * W * nc;
-      if (gq.j1 > gq.j0 && q < rank) c->up = q;
-      if (gq.j1 > gq.j0 && q > rank && c->dn < 0) c->dn = q;
+      if (live && gq.j1 > gq.j0 && q < rank) c->up = q;
+      if (live && gq.j1 > gq.j0 && q > rank && c->dn < 0) c->dn = q;
     }
   }
   long long fac_off = 0, vec_off = 0;
@@ -347,6 +405,7 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
     if (n > (1LL << 30)) fail("schwarz: subdomain too large");
     s.n = static_cast<int>(n);
     s.line_sz = packed_line_size(s.kd);
+    s.m = (s.L - 1) / 2;  // the middle line (balance_chains may move it)
     s.fac_off = fac_off;
     s.vec_off = vec_off;
     if (p < c->s_lo || p >= c->s_hi) continue;  // another rank's subdomain: no storage here
@@ -359,6 +418,7 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
   }
   c->factor_doubles = fd;
   c->factor_flops = ff;
+  balance_chains(c);
   c->apply_doubles = ad;
   c->sum_n = sn;
   // free-rectangle membership along each axis (free rect of part (i,j) = X_i x Y_j)
@@ -524,7 +584,8 @@ void launch_asm(ffb_ctx* c, int nc, const double* rvec, const int* flags) {
     FFB_CUDA(cudaEventRecord(ev->a, c->st));
   }
   line_solve(c->d_subs.p + c->s_lo, c->s_hi - c->s_lo, c->plan, solve_factor(c), c->coef.p, c->N, rvec,
-             c->ylocal.p, c->zlocal.p, c->W, nc, flags, c->st);
+             c->ylocal.p, c->zlocal.p, c->W, nc, flags, c->st, nullptr,
+             c->nseg ? c->d_tasks.p : nullptr, c->d_task_ptr.p, c->nseg);
   if (ev) FFB_CUDA(cudaEventRecord(ev->b, c->st));
 }
 
@@ -1323,12 +1384,14 @@ int ffb_schwarz_run(ffb_ctx* c, const ffb_schwarz_options* o, double* u3, ffb_sc
       } else {
         ensure_factor(c, nc);  // refactors iff alpha changed (schwarz.cpp:238-241)
         line_solve(c->d_subs.p, np, c->plan, solve_factor(c), c->coef.p, N, nullptr, c->ylocal.p,
-                   c->zlocal.p, c->W, nc, nullptr, c->st, rl);
+                   c->zlocal.p, c->W, nc, nullptr, c->st, rl, c->nseg ? c->d_tasks.p : nullptr,
+                   c->d_task_ptr.p, c->nseg);
         // x += A^-1 (rhs - A x): one step of iterative refinement (schwarz.cpp:242-247)
         vec_copy(xl, c->zlocal.p, vec_len, c->st);
         ras_residual(c->d_subs.p, np, c->coef.p, N, c->W, nc, rl, xl, rl, c->st);
         line_solve(c->d_subs.p, np, c->plan, solve_factor(c), c->coef.p, N, nullptr, c->ylocal.p,
-                   c->zlocal.p, c->W, nc, nullptr, c->st, rl);
+                   c->zlocal.p, c->W, nc, nullptr, c->st, rl, c->nseg ? c->d_tasks.p : nullptr,
+                   c->d_task_ptr.p, c->nseg);
         dl = c->zlocal.p;
       }
       ras_compose(c->own_col.p, c->own_row.p, c->d_subs.p, c->part_px, xl, dl, G, Gn, c->W, c->H,

@@ -138,7 +138,7 @@ struct LocalHub {
       arrived = 0;
       ++gen;
       cv.notify_all();
-    } else if (!cv.wait_for(lk, std::chrono::seconds(600), [&] { return gen != g; })) {
+    } else if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g; })) {
       fail("schwarz.comm: a rank of the in-process communicator did not arrive (failed?)");
     }
   }

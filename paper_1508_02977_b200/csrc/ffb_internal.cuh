@@ -76,7 +76,7 @@ struct SubInfo {
   int L;                 // slow extent (number of lines)
   int kd;                // unknowns per line, nc*S
   int n;                 // L*kd scalar unknowns
-  int pad_;
+  int m;                 // twisted split: chain 0 lines 0..m-1, chain 1 L-1..m+1, middle m
   long long line_sz;     // doubles per line of the packed factor (packed_line_size(kd))
   long long fac_off;     // offset (doubles) of the subdomain's factor
   long long vec_off;     // offset (doubles) into the per-subdomain vectors
@@ -102,7 +102,8 @@ SolvePlan solve_plan(int kd_max, int C);
 void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,
                 const double* coef, size_t N, const double* r, double* ylocal, double* zlocal,
                 int W, int nc, const int* flags, cudaStream_t st,
-                const double* rlocal = nullptr);
+                const double* rlocal = nullptr, const int2* tasks = nullptr,
+                const int* task_ptr = nullptr, int nseg = 0);
 
 // ---- literal Schwarz iteration (ras.cu) ---------------------------------------------------
 void ras_rhs(const SubInfo* d_subs, int nsub, const double* coef, const double* b,

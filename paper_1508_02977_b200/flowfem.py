@@ -518,6 +518,68 @@ def solve(sys: SparseSystem, cfg: SolverConfig = SolverConfig(),
     return x
 
 
+def assemble(terms: DataTerms, reg: RegField, components: int = 3, dirichlet_vertices=None,
+             dirichlet_values=None, ctx: Context | None = None) -> SparseSystem:
+    """assemble (assembly.hpp:59-61, assembly.cpp:32-166) as an explicit CSR system, with an
+    optional Dirichlet set (vertex ids, values (n, components)) eliminated into the rhs;
+    values from the device operator, bitwise equal to the reference's."""
+    ctx = ctx or default_context()
+    t = terms.planes
+    _, H, W = t.shape
+    lib = ctx.lib
+    nd = 0 if dirichlet_vertices is None else len(dirichlet_vertices)
+    dv = np.ascontiguousarray(dirichlet_vertices, dtype=np.int32) if nd else None
+    dval = _f64(np.asarray(dirichlet_values).reshape(nd, components)) if nd else None
+    n, nnz = C.c_int(), C.c_longlong()
+    args = [ctx.handle, W, H, _p(t), _p(_f64(reg.alpha)), _p(_f64(reg.lambda_)), components, nd,
+            _ip(dv) if nd else None, _p(dval) if nd else None, C.byref(n), C.byref(nnz)]
+    _check(lib.ffb_assemble_system(*args, None, None, None, None, None, None))
+    rp = np.zeros(n.value + 1, dtype=np.int32)
+    cols = np.zeros(nnz.value, dtype=np.int32)
+    vals = np.zeros(nnz.value)
+    rhs = np.zeros(n.value)
+    _check(lib.ffb_assemble_system(*args, _ip(rp), _ip(cols), _p(vals), _p(rhs), None, None))
+    return SparseSystem(rp, cols, vals, rhs, components)
+
+
+class SparseCholesky:
+    """SparseCholesky (linsolve.hpp:32-48) on the device: analyze = the reference's RCM order
+    (bit-exact) + band width, factorize = band Cholesky of the permuted matrix, solve."""
+
+    def __init__(self, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(self.ctx.lib.ffb_chol_create(self.ctx.handle, C.byref(h)))
+        self._h = h
+        self.n = 0
+
+    def analyze(self, sys: SparseSystem):
+        _check(self.ctx.lib.ffb_chol_analyze(self._h, sys.n, sys.components, _ip(sys.row_ptr),
+                                             _ip(sys.cols)))
+        self.n = sys.n
+
+    def factorize(self, sys: SparseSystem, workers: int = 1):
+        _check(self.ctx.lib.ffb_chol_factorize(self._h, sys.n, _p(sys.vals)))
+
+    def solve(self, b) -> np.ndarray:
+        b = _f64(b)
+        x = np.zeros(self.n)
+        _check(self.ctx.lib.ffb_chol_solve(self._h, len(b), _p(b), _p(x)))
+        return x
+
+    def bandwidth(self) -> int:
+        bw = C.c_int()
+        _check(self.ctx.lib.ffb_chol_info(self._h, C.byref(bw), None))
+        return bw.value
+
+    def __del__(self):
+        try:
+            if self._h:
+                self.ctx.lib.ffb_chol_destroy(self._h)
+        except Exception:
+            pass
+
+
 @dataclass
 class IndicatorField:
     eta: np.ndarray

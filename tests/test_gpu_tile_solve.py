@@ -85,3 +85,25 @@ def test_tile_solve_deterministic(port):
     u2, it2, _, k2 = solve(t, a, l, 4, 4, 2, 3)
     assert k1 == k2 == 1 and it1 == it2
     assert np.array_equal(u1, u2)  # fixed-order reductions: bitwise run to run
+
+
+def test_balanced_chain_schedule_matches_middle_split(ctx, monkeypatch):
+    """Balanced twisted splits (capi.cpp balance_chains: the subdomains' line steps cut into
+    one segment per SM, persistent CTAs streaming their task lists) give the same solution
+    as the middle split (FFB_NO_BALANCE=1) to rounding, on a 16x16 partition large enough to
+    balance (1600x900: 256 subdomains of ~104 lines), and converge to the true residual."""
+    import numpy as np
+    from conftest import rel_l2
+    rng = np.random.default_rng(3)
+    H, W = 900, 1600
+    yy, xx = np.mgrid[0:H, 0:W].astype(float)
+    f0 = 120 + 50 * np.sin(xx / 9.0) * np.cos(yy / 7.0) + rng.normal(0, 3, (H, W))
+    f1 = 120 + 50 * np.sin((xx - 0.8) / 9.0) * np.cos((yy - 0.5) / 7.0) + rng.normal(0, 3, (H, W))
+    cfg = ff.RunConfig(sigma=1.5, parts=256, overlap=4, adapt_iters=1, cg_tolerance=1e-10)
+    a = ff.run_on_frames(f0, f1, cfg, ff.Context(0))
+    monkeypatch.setenv("FFB_NO_BALANCE", "1")
+    b = ff.run_on_frames(f0, f1, cfg, ff.Context(0))
+    for c in range(3):
+        assert rel_l2(a.flow.planes()[c], b.flow.planes()[c]) < 1e-8
+    assert max(a.stats.residual) <= 1e-10
+    assert abs(sum(a.stats.iters) - sum(b.stats.iters)) <= 2

@@ -66,8 +66,9 @@ class EmuRank:
         live = [q for q in range(self.world)
                 if par.rank_rows(W, H, self.px, self.py, cfg.overlap, q, self.world)["j1"] >
                 par.rank_rows(W, H, self.px, self.py, cfg.overlap, q, self.world)["j0"]]
-        self.up = max([q for q in live if q < self.rank], default=-1)
-        self.dn = min([q for q in live if q > self.rank], default=-1)
+        me = self.g["j1"] > self.g["j0"]  # a rank without subdomains exchanges nothing
+        self.up = max([q for q in live if q < self.rank], default=-1) if me else -1
+        self.dn = min([q for q in live if q > self.rank], default=-1) if me else -1
         self.ys = np.array(self.P.ys if hasattr(self.P, "ys") else
                            [self.P.parts[j * self.px].core.y0 for j in range(self.py)] + [H])
         self.x = np.zeros((H, W, 3))
