@@ -1122,6 +1122,12 @@ __device__ __forceinline__ int chain_line(int phase, int chain, const SubInfo& s
   return chain == 0 ? s.m - t : s.m + t;
 }
 
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // wait with cluster-scope acquire: pairs with remote release-arrivals from the other CTAs
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -1169,21 +1175,28 @@ __global__ void __launch_bounds__(kST, 1)
     k_line_solve(const SubInfo* __restrict__ subs, const double* __restrict__ fac,
                  const double* __restrict__ coef, size_t N, const double* __restrict__ r,
                  double* __restrict__ ylocal, double* __restrict__ zlocal, int W, int nc,
-                 int stages, int cap, int kd_max, int rc, int phase,
+                 int stages, int cap, int kd_max, int rc, int phase_arg,
                  const int* __restrict__ flags,
-                 const double* __restrict__ rlocal, const int2* __restrict__ tasks,
-                 const int* __restrict__ task_ptr) {
+                 const double* __restrict__ rlocal, int* __restrict__ qsync, int nsub_all) {
   if (flags && (flags[0] | flags[1])) return;  // PCG converged or failed (grid-uniform)
   const int C = static_cast<int>(cl_size()), crank = static_cast<int>(cl_rank());
-  // the (subdomain, chain) tasks of this CTA: one per cluster, or — the balanced schedule
-  // (C == 1, capi.cpp balance_chains) — the list task_ptr[b] .. task_ptr[b+1], streamed
-  // back to back through the same ring
-  const int tk0 = PERSIST ? task_ptr[blockIdx.x] : 0;
-  const int tk1 = PERSIST ? task_ptr[blockIdx.x + 1] : 1;
-  auto task = [&](int tk) {
-    if (PERSIST) return tasks[tk];
-    const int cid = blockIdx.x / C;
-    return make_int2(cid >> 1, cid & 1);
+  // Tasks (phase, subdomain, chain). One per cluster; or (PERSIST, one CTA per chain, one CTA
+  // per SM) a dynamic queue of the whole application — the forward chains of every
+  // subdomain, then the backward chains — so the chains fill the SMs without the partly
+  // empty last round of a one-chain-per-CTA launch (c4: 512 chains on 148 SMs per sweep).
+  // qsync[0] is the queue head, qsync[1 + sub] counts the finished forward chains of sub: a
+  // backward task waits for them (release/acquire through global memory; the forward tasks
+  // were all dequeued earlier, so they are running or done).
+  const int ntask = PERSIST ? 4 * nsub_all : 1;
+  auto decode = [&](int tk, int& ph, int& sub, int& chain) {
+    if (!PERSIST) {
+      const int cid = blockIdx.x / C;
+      ph = phase_arg, sub = cid >> 1, chain = cid & 1;
+      return;
+    }
+    ph = tk >= 2 * nsub_all ? 1 : 0;
+    const int c2 = tk - ph * 2 * nsub_all;
+    sub = c2 >> 1, chain = c2 & 1;
   };
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1192,6 +1205,9 @@ __global__ void __launch_bounds__(kST, 1)
   const int dbg = g_solve_dbg;
   uint64_t* red_bar = empty + 8;  // [2]: partial sums for my rows have arrived (line parity)
   uint64_t* x_bar = red_bar + 2;  // [2]: the other CTAs' x of the line have arrived
+  uint64_t* tbar = x_bar + 2;     // [4] PERSIST: task id k published by the producer
+  uint64_t* tfree = tbar + 4;     // [4] PERSIST: the consumers have read task slot k
+  int* task_ids = reinterpret_cast<int*>(smem_raw + 240);  // [4]
   double* stage0 = reinterpret_cast<double*>(smem_raw + kSolveHdr);
   // column-partial slots: one per compute warp, or 8 (two-round reduction) for wide lines
   // where the 7 kd doubles buy ring capacity (must match solve_plan)
@@ -1213,10 +1229,14 @@ __global__ void __launch_bounds__(kST, 1)
       mbar_init(&red_bar[q], 1);  // armed with the expected bytes by this CTA each use
       mbar_init(&x_bar[q], 1);
     }
+    for (int q = 0; q < 4; ++q) {
+      mbar_init(&tbar[q], 1);
+      mbar_init(&tfree[q], 1);
+    }
     fence_barrier_init();
   }
-  int* rlos = reinterpret_cast<int*>(smem_raw + 192);  // row_lo(c) for c = 0..C (C > 1)
-  if (C > 1 && tid <= C) rlos[tid] = row_lo(tid, C, subs[task(tk0).x].kd, rc);
+  int* rlos = reinterpret_cast<int*>(smem_raw + 256);  // row_lo(c) for c = 0..C (C > 1)
+  if (C > 1 && tid <= C) rlos[tid] = row_lo(tid, C, subs[(blockIdx.x / C) >> 1].kd, rc);
   for (int j = tid; j < 2 * kd_max; j += kST) xbuf[j] = 0.0;
   if (C > 1) cl_sync(); else __syncthreads();  // barriers initialised cluster-wide
 
@@ -1228,10 +1248,22 @@ __global__ void __launch_bounds__(kST, 1)
     int line_of[8];  // line of the chunk last placed in each stage
 #pragma unroll
     for (int k = 0; k < 8; ++k) line_of[k] = -1;
-    for (int tk = tk0; tk < tk1; ++tk) {
-      const int2 tc = task(tk);
-      const SubInfo s = subs[tc.x];
-      const int chain = tc.y, kd = s.kd, nl = chain_len(phase, chain, s);
+    for (int kk = 0;; ++kk) {
+      int tk = kk;
+      if (PERSIST) {  // dequeue and publish the next task to the compute warps
+        if (lane == 0) {
+          if (kk >= 4) mbar_wait(&tfree[kk & 3], ((kk >> 2) - 1) & 1);
+          tk = atomicAdd(qsync, 1);
+          task_ids[kk & 3] = tk;
+          mbar_arrive(&tbar[kk & 3]);
+        }
+        tk = __shfl_sync(0xffffffffu, tk, 0);
+      }
+      if (tk >= ntask) break;
+      int phase, sub, chain;
+      decode(tk, phase, sub, chain);
+      const SubInfo s = subs[sub];
+      const int kd = s.kd, nl = chain_len(phase, chain, s);
       const int rlo = row_lo(crank, C, kd, rc), rhi = row_lo(crank + 1, C, kd, rc);
       if (nl == 0 || rlo >= rhi) continue;
       const double* F = fac + s.fac_off;
@@ -1277,10 +1309,18 @@ __global__ void __launch_bounds__(kST, 1)
   // ------------------------------------------------------------------ compute warps
   int c_seq = 0;  // ring slots consumed (continues across tasks)
   PROF_DECL
-  for (int tk = tk0; tk < tk1; ++tk) {
-  const int2 tc = task(tk);
-  const SubInfo s = subs[tc.x];
-  const int chain = tc.y;
+  for (int kk = 0;; ++kk) {
+  int tk = kk;
+  if (PERSIST) {
+    mbar_wait(&tbar[kk & 3], (kk >> 2) & 1);
+    tk = task_ids[kk & 3];
+    compute_bar();  // every compute thread has read the slot
+    if (tid == 0) mbar_arrive(&tfree[kk & 3]);
+  }
+  if (tk >= ntask) break;
+  int phase, sub, chain;
+  decode(tk, phase, sub, chain);
+  const SubInfo s = subs[sub];
   const int kd = s.kd, L = s.L, m = s.m;
   const int nl = chain_len(phase, chain, s);
   if (nl == 0) continue;  // cluster-uniform
@@ -1288,8 +1328,15 @@ __global__ void __launch_bounds__(kST, 1)
   double* yl = ylocal + s.vec_off;
   double* zl = zlocal + s.vec_off;
   const double* rl = rlocal ? rlocal + s.vec_off : nullptr;  // per-subdomain rhs (RAS mode)
-  if (PERSIST && tk > tk0) {  // x of "line -1" is zero for every task (one CTA per chain)
+  if (PERSIST && kk > 0) {  // x of "line -1" is zero for every task (one CTA per chain)
     for (int j = tid; j < 2 * kd_max; j += kCT) xbuf[j] = 0.0;
+    compute_bar();
+  }
+  if (PERSIST && phase == 1) {  // both forward chains of this subdomain are done
+    if (tid == 0) {
+      const int need = (s.m > 0 ? 1 : 0) + (s.L - 1 - s.m > 0 ? 1 : 0);
+      while (ld_acquire_gpu(qsync + 1 + sub) < need) __nanosleep(100);
+    }
     compute_bar();
   }
   // operand of line step t, prefetched into registers one step ahead. Forward:
@@ -1310,16 +1357,16 @@ __global__ void __launch_bounds__(kST, 1)
           if (t > 0) pf_b[q] = bcoef(s, coef, N, W, nc, chain == 0 ? l : l + 1, j);
         } else if (t == 0) {  // middle line: both neighbours from the forward sweep
           double w = rl ? rl[static_cast<long long>(l) * kd + j] : r[gidx(s, l, j, W, nc)];
-          if (m > 0) w -= bcoef(s, coef, N, W, nc, m, j) * yl[static_cast<long long>(m - 1) * kd + j];
+          if (m > 0) w -= bcoef(s, coef, N, W, nc, m, j) * __ldcg(yl + static_cast<long long>(m - 1) * kd + j);
           if (m < L - 1)
-            w -= bcoef(s, coef, N, W, nc, m + 1, j) * yl[static_cast<long long>(m + 1) * kd + j];
+            w -= bcoef(s, coef, N, W, nc, m + 1, j) * __ldcg(yl + static_cast<long long>(m + 1) * kd + j);
           pf_r[q] = w;
         } else {
           pf_b[q] = bcoef(s, coef, N, W, nc, chain == 0 ? l + 1 : l, j);
         }
       }
       const int jo = rlo + tid + kCT * q;  // owned row
-      if (phase == 1 && t > 0 && jo < rhi) pf_y[q] = yl[static_cast<long long>(l) * kd + jo];
+      if (phase == 1 && t > 0 && jo < rhi) pf_y[q] = __ldcg(yl + static_cast<long long>(l) * kd + jo);
     }
   };
   prefetch(0);
@@ -1526,6 +1573,11 @@ __global__ void __launch_bounds__(kST, 1)
   // arrivals means no remote store into this CTA's shared memory is still in flight
   if (C > 1 && !(dbg & 2)) mbar_wait_cluster(&x_bar[(nl - 1) & 1], ((nl - 1) >> 1) & 1);
   if (C > 1 && (dbg & 2)) cl_sync();
+  if (PERSIST && phase == 0) {  // publish this forward chain (y of its lines) to the queue
+    __threadfence();
+    compute_bar();
+    if (tid == 0) atomicAdd(qsync + 1 + sub, 1);
+  }
   }  // tasks
   PROF_FLUSH(16);
 }
@@ -2279,8 +2331,7 @@ template <int M>
 static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
                            const double* fac, const double* coef, size_t N, const double* r,
                            double* ylocal, double* zlocal, int W, int nc, const int* flags,
-                           const double* rlocal, cudaStream_t st, const int2* tasks,
-                           const int* task_ptr, int nseg) {
+                           const double* rlocal, cudaStream_t st, int* qsync, int n_cta) {
   for (int phase = 0; phase <= 1; ++phase) {
     if (pl.tile) {
       set_tile_tables();
@@ -2288,16 +2339,19 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
                      fac, coef, N, r, ylocal, zlocal, W, nc, (pl.maxm) * 32, pl.stage_doubles,
                      phase, flags, rlocal);
     } else {
-      // balanced schedule (one CTA per chain): `nseg` persistent CTAs, each streaming its
-      // task list; else one cluster per (subdomain, chain)
-      if (tasks)
-        launch_cluster(k_line_solve<M, true>, nseg, kST, pl.smem, 1, st, d_subs, fac, coef, N, r,
-                       ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, pl.row_cost, phase,
-                       flags, rlocal, tasks, task_ptr);
-      else
+      // one CTA per chain: n_cta persistent CTAs pull the chains of both sweeps from a queue;
+      // else one cluster per (subdomain, chain), one launch per sweep
+      if (qsync) {  // one launch for both sweeps (the dynamic queue holds them in order)
+        if (phase == 1) break;
+        FFB_CUDA(cudaMemsetAsync(qsync, 0, (nsub + 1) * sizeof(int), st));
+        launch_cluster(k_line_solve<M, true>, n_cta, kST, pl.smem, 1, st, d_subs, fac, coef, N, r,
+                       ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max, pl.row_cost, 0,
+                       flags, rlocal, qsync, nsub);
+      } else {
         launch_cluster(k_line_solve<M, false>, 2 * nsub * pl.C, kST, pl.smem, pl.C, st, d_subs,
                        fac, coef, N, r, ylocal, zlocal, W, nc, pl.stages, pl.cap, pl.kd_max,
-                       pl.row_cost, phase, flags, rlocal, tasks, task_ptr);
+                       pl.row_cost, phase, flags, rlocal, nullptr, nsub);
+      }
     }
     FFB_LAUNCHED();
   }
@@ -2306,24 +2360,24 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
 void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,
                 const double* coef, size_t N, const double* r, double* ylocal, double* zlocal,
                 int W, int nc, const int* flags, cudaStream_t st, const double* rlocal,
-                const int2* tasks, const int* task_ptr, int nseg) {
-  if (pl.tile || pl.C != 1) tasks = nullptr, task_ptr = nullptr;  // balanced: ring, C == 1
+                int* qsync, int n_cta) {
+  if (pl.tile || pl.C != 1) qsync = nullptr;  // the task queue: ring kernel, one CTA per chain
   if (nsub <= 0) return;  // a rank without subdomains (world > parts)
   if (pl.maxm <= 4)
     launch_solve_m<4>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
-                      tasks, task_ptr, nseg);
+                      qsync, n_cta);
   else if (pl.maxm <= 8)
     launch_solve_m<8>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
-                      tasks, task_ptr, nseg);
+                      qsync, n_cta);
   else if (pl.maxm <= 14)
     launch_solve_m<14>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
-                      tasks, task_ptr, nseg);
+                      qsync, n_cta);
   else if (pl.maxm <= 20)
     launch_solve_m<20>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
-                      tasks, task_ptr, nseg);
+                      qsync, n_cta);
   else if (pl.maxm <= 26)
     launch_solve_m<26>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
-                      tasks, task_ptr, nseg);
+                      qsync, n_cta);
   else
     fail("linsolve.cholesky: subdomain line too wide (kd > 832)");
 }

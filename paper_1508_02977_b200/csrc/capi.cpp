@@ -113,10 +113,9 @@ struct ffb_ctx {
   int up = -1, dn = -1;  // nearest non-empty ranks above / below (-1: none)
   std::vector<size_t> gather_off, gather_cnt;  // owned rows of every rank, in doubles / W nc
   int s_lo = 0, s_hi = 0;
-  // balanced schedule of the ring solve (balance_chains): per persistent CTA a task list
-  int nseg = 0;
-  DBuf<int2> d_tasks;
-  DBuf<int> d_task_ptr;
+  // persistent ring solve (balance_chains): CTAs, and the task queue + forward-done counters
+  int n_cta = 0;
+  DBuf<int> qsync;
   DBuf<double> ur, urs, zs_up, zs_dn, zr_up, zr_dn;
   int stage_nc = 0, stage_max_iters = 0;
   double stage_tol = 0;
@@ -286,57 +285,20 @@ RankRows rank_rows(const Partition& P, int rank, int world) {
   return g;
 }
 
-// Balanced twisted splits for the ring solve with one CTA per chain (c3-c5 shapes). Every
-// chain is a sequential pass over its lines, so with 2 chains per subdomain and one CTA per SM
-// the launch runs in ceil(2 nsub / #SMs) rounds and the last one is partly empty (c4: 512
-// chains on 148 SMs = 3.46 rounds, 86% occupancy). Instead, the rank's subdomains' line steps
-// (L_i - 1 each, the middle line apart) are laid end to end and cut into #SMs equal segments;
-// a subdomain a cut falls into is split there (its middle line m_i = the cut), the others run
-// as one chain (m_i = L_i - 1), and each segment becomes the task list of one persistent CTA.
-// The factor follows the same m_i. Used when every segment is longer than any subdomain, so a
-// subdomain is cut at most once; FFB_NO_BALANCE=1 keeps the middle split.
+// Persistent ring solve with one CTA per chain (band.cu k_line_solve<M, true>): when the
+// rank has more chains than SMs, one CTA per SM pulls the forward chains of every subdomain
+// and then the backward chains from a queue, so the SMs stay busy through what would be a
+// partly empty last round of one-chain-per-CTA launches (c4: 512 chains per sweep on 148 SMs
+// = 3.46 rounds). FFB_NO_BALANCE=1 keeps the two launches per application.
 void balance_chains(ffb_ctx* c) {
-  c->nseg = 0;
+  c->n_cta = 0;
   if (c->plan.tile || c->ccl != 1 || std::getenv("FFB_NO_BALANCE")) return;
   int nsm = 0;
   FFB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
-  long long T = 0;
-  int nmax = 0;
-  for (int p = c->s_lo; p < c->s_hi; ++p) {
-    T += c->subs[p].L - 1;
-    nmax = std::max(nmax, c->subs[p].L - 1);
-  }
-  if (nsm < 1 || T < static_cast<long long>(nsm) * (nmax + 2)) return;
-  auto cut = [&](int k) { return (static_cast<long long>(k) * T + nsm / 2) / nsm; };
-  std::vector<int2> tasks;
-  std::vector<int> ptr(nsm + 1, 0);
-  int seg = 0;
-  long long g = 0, next = cut(1);
-  for (int p = c->s_lo; p < c->s_hi; ++p) {
-    SubInfo& s = c->subs[p];
-    const int n = s.L - 1, rel = p - c->s_lo;
-    if (n > 0 && next > g && next < g + n) {  // split: chain 0 ends this segment
-      s.m = static_cast<int>(next - g);
-      tasks.push_back(make_int2(rel, 0));
-      ptr[++seg] = static_cast<int>(tasks.size());
-      next = cut(seg + 1);
-      tasks.push_back(make_int2(rel, 1));   // chain 1 opens the next one
-    } else {
-      s.m = n;  // one chain: lines 0..L-2, the last line closes it
-      tasks.push_back(make_int2(rel, 0));
-      if (seg < nsm - 1 && next == g + n) {
-        ptr[++seg] = static_cast<int>(tasks.size());
-        next = cut(seg + 1);
-      }
-    }
-    g += n;
-  }
-  while (seg < nsm) ptr[++seg] = static_cast<int>(tasks.size());
-  c->nseg = nsm;
-  FFB_CUDA(cudaMemcpyAsync(c->d_tasks.ensure(tasks.size()), tasks.data(), tasks.size() * sizeof(int2),
-                           cudaMemcpyHostToDevice, c->st));
-  FFB_CUDA(cudaMemcpyAsync(c->d_task_ptr.ensure(ptr.size()), ptr.data(), ptr.size() * sizeof(int),
-                           cudaMemcpyHostToDevice, c->st));
+  const int nsub = c->s_hi - c->s_lo;
+  if (nsm < 1 || 2 * nsub <= nsm) return;
+  c->n_cta = nsm;
+  c->qsync.ensure(nsub + 1);
 }
 
 void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
@@ -405,7 +367,7 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
     if (n > (1LL << 30)) fail("schwarz: subdomain too large");
     s.n = static_cast<int>(n);
     s.line_sz = packed_line_size(s.kd);
-    s.m = (s.L - 1) / 2;  // the middle line (balance_chains may move it)
+    s.m = (s.L - 1) / 2;  // the middle line of the twisted factorisation
     s.fac_off = fac_off;
     s.vec_off = vec_off;
     if (p < c->s_lo || p >= c->s_hi) continue;  // another rank's subdomain: no storage here
@@ -585,7 +547,7 @@ void launch_asm(ffb_ctx* c, int nc, const double* rvec, const int* flags) {
   }
   line_solve(c->d_subs.p + c->s_lo, c->s_hi - c->s_lo, c->plan, solve_factor(c), c->coef.p, c->N, rvec,
              c->ylocal.p, c->zlocal.p, c->W, nc, flags, c->st, nullptr,
-             c->nseg ? c->d_tasks.p : nullptr, c->d_task_ptr.p, c->nseg);
+             c->n_cta ? c->qsync.p : nullptr, c->n_cta);
   if (ev) FFB_CUDA(cudaEventRecord(ev->b, c->st));
 }
 
@@ -1384,14 +1346,14 @@ int ffb_schwarz_run(ffb_ctx* c, const ffb_schwarz_options* o, double* u3, ffb_sc
       } else {
         ensure_factor(c, nc);  // refactors iff alpha changed (schwarz.cpp:238-241)
         line_solve(c->d_subs.p, np, c->plan, solve_factor(c), c->coef.p, N, nullptr, c->ylocal.p,
-                   c->zlocal.p, c->W, nc, nullptr, c->st, rl, c->nseg ? c->d_tasks.p : nullptr,
-                   c->d_task_ptr.p, c->nseg);
+                   c->zlocal.p, c->W, nc, nullptr, c->st, rl, c->n_cta ? c->qsync.p : nullptr,
+                   c->n_cta);
         // x += A^-1 (rhs - A x): one step of iterative refinement (schwarz.cpp:242-247)
         vec_copy(xl, c->zlocal.p, vec_len, c->st);
         ras_residual(c->d_subs.p, np, c->coef.p, N, c->W, nc, rl, xl, rl, c->st);
         line_solve(c->d_subs.p, np, c->plan, solve_factor(c), c->coef.p, N, nullptr, c->ylocal.p,
-                   c->zlocal.p, c->W, nc, nullptr, c->st, rl, c->nseg ? c->d_tasks.p : nullptr,
-                   c->d_task_ptr.p, c->nseg);
+                   c->zlocal.p, c->W, nc, nullptr, c->st, rl, c->n_cta ? c->qsync.p : nullptr,
+                   c->n_cta);
         dl = c->zlocal.p;
       }
       ras_compose(c->own_col.p, c->own_row.p, c->d_subs.p, c->part_px, xl, dl, G, Gn, c->W, c->H,

@@ -102,8 +102,7 @@ SolvePlan solve_plan(int kd_max, int C);
 void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,
                 const double* coef, size_t N, const double* r, double* ylocal, double* zlocal,
                 int W, int nc, const int* flags, cudaStream_t st,
-                const double* rlocal = nullptr, const int2* tasks = nullptr,
-                const int* task_ptr = nullptr, int nseg = 0);
+                const double* rlocal = nullptr, int* qsync = nullptr, int n_cta = 0);
 
 // ---- literal Schwarz iteration (ras.cu) ---------------------------------------------------
 void ras_rhs(const SubInfo* d_subs, int nsub, const double* coef, const double* b,
