@@ -6,6 +6,7 @@ import collections
 import sys
 
 src, out_csv, out_txt = sys.argv[1:4]
+what = sys.argv[4] if len(sys.argv) > 4 else "python bench.py --steps 2 --warmup 3 --no-cpu-baseline (c2)"
 rows = [r for r in csv.reader(open(src)) if len(r) > 10]
 h = rows[0]
 ik, iv, iid, im = h.index("Kernel Name"), h.index("Metric Value"), h.index("ID"), h.index("Metric Name")
@@ -17,8 +18,7 @@ for r in rows[1:]:
     launches.append((int(r[iid]), name, float(r[iv].replace(",", ""))))
 unit_ns = 1.0  # ncu reports ns for gpu__time_duration.sum in --csv
 with open(out_csv, "w") as f:
-    f.write("# ncu --metrics gpu__time_duration.sum --clock-control none: python bench.py --steps 2 "
-            "--warmup 3 --no-cpu-baseline (c2), every launch (warm-up + timed steps)\n")
+    f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none: {what}, every launch\n")
     f.write("id,kernel,duration_ns\n")
     for i, n, v in launches:
         f.write(f"{i},{n},{v * unit_ns:.0f}\n")
