@@ -29,7 +29,7 @@ for _, n, v in launches:
     cnt[n] += 1
 s = sum(tot.values())
 with open(out_txt, "w") as f:
-    f.write(f"per-kernel totals of {out_csv} (5 steps: 3 warm-up + 2 timed; cold-cache serialised ncu times)\n")
+    f.write(f"per-kernel totals of {out_csv} ({what}; cold-cache serialised ncu times)\n")
     f.write(f"{'kernel':40s} {'launches':>9s} {'total ms':>10s} {'share':>7s}\n")
     for n, v in sorted(tot.items(), key=lambda x: -x[1]):
         f.write(f"{n[:40]:40s} {cnt[n]:9d} {v / 1e6:10.2f} {100 * v / s:6.1f}%\n")
