@@ -2112,7 +2112,8 @@ void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
     const char* e = std::getenv("FFB_LOOKAHEAD");
     return e ? std::atoi(e) : 1;
   }();
-  const size_t smem = (nb * (nb + 1) + 2 * nb * (nb + 2) + 2 * nb + static_cast<size_t>(nb) * (kdp + 8)) *
+  const int ldl = nb == 32 ? li_stride<32>() : li_stride<16>();
+  const size_t smem = (nb * (nb + 1) + 2 * nb * ldl + 2 * nb + static_cast<size_t>(nb) * (kdp + 8)) *
                       sizeof(double);
   if (smem > 227 * 1024) fail("linsolve.cholesky: subdomain line too wide for shared memory");
   // Factor clusters of 4 CTAs regardless of how many SMs that asks for: the hardware runs the

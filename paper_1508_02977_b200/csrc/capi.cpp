@@ -325,14 +325,6 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
     const int v = std::atoi(e);
     if (v == 16 || v == 32) c->nbf = v;
   }
-  // CTAs per subdomain (one thread-block cluster): enough that ~128 SMs take part
-  c->ccl = 1;
-  while (c->ccl < 8 && 2 * np * c->ccl * 2 <= 160) c->ccl *= 2;  // 2 chains per subdomain
-  if (const char* e = std::getenv("FFB_CLUSTER")) {
-    const int v = std::atoi(e);
-    if (v == 1 || v == 2 || v == 4 || v == 8) c->ccl = v;
-  }
-  c->plan = solve_plan(kd_max, c->ccl);
   c->subs.assign(np, SubInfo{});
   // this rank's band of subdomain rows (all of them on a single GPU): subdomains
   // [s_lo, s_hi) are factored and solved here
@@ -352,6 +344,18 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
       if (live && gq.j1 > gq.j0 && q < rank) c->up = q;
       if (live && gq.j1 > gq.j0 && q > rank && c->dn < 0) c->dn = q;
     }
+  }
+  // CTAs per subdomain solve (one thread-block cluster), from THIS rank's subdomains: enough
+  // that ~128 SMs take part (2 chains per subdomain)
+  {
+    const int nown = std::max(1, c->s_hi - c->s_lo);
+    c->ccl = 1;
+    while (c->ccl < 8 && 2 * nown * c->ccl * 2 <= 160) c->ccl *= 2;
+    if (const char* e = std::getenv("FFB_CLUSTER")) {
+      const int v = std::atoi(e);
+      if (v == 1 || v == 2 || v == 4 || v == 8) c->ccl = v;
+    }
+    c->plan = solve_plan(kd_max, c->ccl);
   }
   long long fac_off = 0, vec_off = 0;
   double fd = 0, ad = 0, sn = 0, ff = 0;

@@ -14,10 +14,14 @@
 
 namespace ffb {
 
-// row stride of the L^-1 tiles (even: rows stay 16-byte aligned for paired loads)
+// row stride of the L^-1 tiles: even (rows stay 16-byte aligned for paired loads) and
+// = 4 mod 16 doubles, so the DMMA fragment loads — lanes (g, t4) reading Li[(g + ..) LDL + t4 + ..]
+// as 64-bit loads served per half-warp — put the half-warp's 4 rows on disjoint 32-byte bank
+// groups (NB + 2 had rows 16 bytes apart: ncu counted 6.3e9 excessive shared wavefronts per
+// c4 factorisation, all on these loads)
 template <int NB>
 __host__ __device__ constexpr int li_stride() {
-  return NB + 2;
+  return NB + 4;
 }
 
 // a usable pivot: positive and finite (false for NaN)
