@@ -193,7 +193,6 @@ __device__ __forceinline__ int row_lo(int c, int C, int kd, int rc = 0) {
 //   middle:   T = A_mm - B_m D_{m-1}^-1 B_m - B_{m+1} E_{m+1}^-1 B_{m+1}
 // A_i^-1 r then runs forward from both ends to the middle and backward from the middle out,
 // halving the sequential depth of both the factorization and the solve.
-__host__ __device__ __forceinline__ int mid_line(int L) { return (L - 1) / 2; }
 
 // ----------------------------------------------------------------- K5 factor
 constexpr int kFT = 512;  // factor threads per CTA (16 warps)
@@ -1078,16 +1077,18 @@ __device__ __forceinline__ double transpose_reduce(double (&acc)[R], int lane) {
   return t;
 }
 
-constexpr int kSW = 16;  // solve warps per CTA: 15 compute + 1 producer
-constexpr int kSolveHdr = 1024;  // mbarriers (0..255) and the chunk table (256..1023)
-constexpr int kMaxChunks = 191;  // chunks of one line per CTA
+#ifndef FFB_SOLVE_WARPS
+#define FFB_SOLVE_WARPS 16
+#endif
+constexpr int kSW = FFB_SOLVE_WARPS;  // solve warps per CTA: kSW - 1 compute + 1 producer
+constexpr int kSolveHdr = 1024;  // mbarriers (0..239), task slots (240..255), cluster row table
 // development probe (FFB_SOLVE_DBG): 1 skip the row arithmetic, 2 skip the line exchange,
 // 4 skip the bulk copies. Results are wrong with any bit set; timing decomposition only.
 __device__ int g_solve_dbg = 0;
 constexpr int kST = kSW * 32;
 constexpr int kCW = kSW - 1;
 constexpr int kCT = kCW * 32;
-constexpr int kCS = 8;  // column-partial slots (15 warps reduced in two rounds)
+constexpr int kCS = (kCW + 1) / 2;  // column-partial slots (the compute warps reduced in two rounds)
 
 // Row chunking of a CTA's rows [rlo, rhi) of one line: the longest run of rows starting at
 // r0 whose packed size fits `cap` doubles (at least one row). Identical on every thread.

@@ -91,6 +91,7 @@ struct ffb_ctx {
   long long ntri = 0;
   DBuf<double> t10, alpha, lambda, coef, b, x, r, z, p0, p1, q, eta, part, tmp, work, frames;
   DBuf<double> eta_hist;
+  DBuf<double> xprev;  // the previous pass's solution (FFB_EXTRAP)
   DBuf<double> red;  // reduction scratch of the indicator / energy / compose kernels
   DBuf<int> bad_diag;
   DBuf<unsigned> counter;
@@ -758,6 +759,12 @@ void run_dev(ffb_ctx* c, int W, int H, const double* f0, const double* f1,
   unsigned* counter = c->counter.ensure(1);
   FFB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), c->st));
   double ms_factor = 0, ms_pcg = 0, ms_adapt = 0, ms_factor0 = 0;
+  // Warm start of pass p >= 2: x_{p-1} + theta (x_{p-1} - x_{p-2}), theta = 0.75 — the
+  // solution moves the same way from pass to pass as alpha keeps shrinking in the same places
+  // (measured: c4 400 -> 378 PCG iterations per chain, c3 260 -> 242; theta 0.5 / 1.0 / 1.5,
+  // profiles/r2_warm_start.txt). Each pass still converges to tol, so the result is the same
+  // to the solve tolerance. FFB_EXTRAP=theta overrides, FFB_EXTRAP=-1 warm-starts plainly.
+  const double extrap = std::getenv("FFB_EXTRAP") ? std::atof(std::getenv("FFB_EXTRAP")) : 0.75;
   long long total_it = 0;
   c->asm_ms_total = 0;
   c->asm_launches_timed = 0;
@@ -772,6 +779,9 @@ void run_dev(ffb_ctx* c, int W, int H, const double* f0, const double* f1,
     FFB_CUDA(cudaEventRecord(ev[2], c->st));
     ensure_factor(c, nc);
     FFB_CUDA(cudaEventRecord(ev[3], c->st));
+    if (pass > 0 && extrap >= 0.0)  // warm start: the last solution, extrapolated
+      vec_extrapolate(c->x.p, c->xprev.ensure(3 * c->N), static_cast<long long>(c->N) * nc,
+                      pass > 1 ? extrap : 0.0, c->st);
     const PcgResult pr = pcg(c, nc, cfg->tol, cfg->max_iters, pass > 0);
     FFB_CUDA(cudaEventRecord(ev[4], c->st));
     total_it += pr.iters;

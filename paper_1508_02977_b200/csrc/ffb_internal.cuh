@@ -176,6 +176,8 @@ void pcg_update(int nc, double* x, double* r, const double* P0, const double* P1
                 const double* q, int W, const RankRows& g, const int* ys, int py, PcgCtl* ctl,
                 double* part, double* ur, int finish, cudaStream_t st);
 void pcg_scalar(const double* ur, int py, int stage, PcgCtl* ctl, cudaStream_t st);
+// x <- x + theta (x - xprev), xprev <- old x (the warm start of the next adaptive pass)
+void vec_extrapolate(double* x, double* xprev, long long n, double theta, cudaStream_t st);
 int pcg_stage_init();
 int pcg_stage_pap();
 int pcg_stage_rr();

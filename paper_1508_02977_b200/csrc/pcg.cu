@@ -473,7 +473,24 @@ __global__ void k_scalar(const double* __restrict__ ur, int py, int stage, PcgCt
   apply_stage(ctl, stage, a, b);
 }
 
+// warm start of the next adaptive pass: x <- x + theta (x - xprev), xprev <- old x
+// (theta == 0: only the copy)
+__global__ void k_extrapolate(double* __restrict__ x, double* __restrict__ xprev, long long n,
+                              double theta) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double xc = x[i];
+    if (theta != 0.0) x[i] = xc + theta * (xc - xprev[i]);
+    xprev[i] = xc;
+  }
+}
+
 }  // namespace
+
+void vec_extrapolate(double* x, double* xprev, long long n, double theta, cudaStream_t st) {
+  k_extrapolate<<<kRedBlocks, T, 0, st>>>(x, xprev, n, theta);
+  FFB_LAUNCHED();
+}
 
 static int grid_of(const RankRows& g) { return (g.j1 - g.j0) * kCU; }
 
