@@ -275,7 +275,9 @@ int ffb_energy_resident(ffb_ctx* ctx, int nc, double* e);
  * only: the residual on the rows its subdomains reach into (overlap width), the partial
  * subdomain sums of z on the rows it covers in a neighbour's band, and one row of z; the CG
  * scalars are all-reduced as per-subdomain-row values and summed in a fixed order, so the
- * iterates, iteration counts and results are BITWISE identical for every world size. After
+ * iterates, iteration counts and results are BITWISE identical for every world size at equal
+ * subdomain-solve cluster size (each rank sizes its clusters from its own subdomains; a
+ * different size reorders the sums inside the line solves: equal to the solve tolerance). After
  * each solve every rank holds the whole solution. Set a communicator, then call
  * ffb_run_on_frames / ffb_run_on_frames_dev / ffb_pcg_solve on every rank with the same
  * inputs; the call returns when the distributed solve is done. */

@@ -23,7 +23,8 @@
 // so the all-reduce is exact). The z combine sums the subdomains covering a pixel row-pair
 // by row-pair, (z_{j,i} + z_{j,i+1}) + (z_{j+1,i} + z_{j+1,i+1}), so a row-pair computed on
 // the neighbouring rank enters the same expression. Hence every scalar, iterate and the
-// iteration count are bitwise identical for any number of GPUs, and run to run.
+// iteration count are bitwise identical for any number of GPUs (at equal subdomain-solve
+// cluster size, which orders the sums inside the line solves), and run to run.
 // Once converged (or failed) every kernel returns at entry, so the host may enqueue
 // several iterations ahead and only reads the control block between chunks.
 #include "ffb_internal.cuh"

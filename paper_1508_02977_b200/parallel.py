@@ -5,7 +5,8 @@ library factors and solves only that band's subdomains, runs the CG kernels on i
 exchanges with the neighbouring ranks — over NCCL P2P (ncclSend/ncclRecv on NVLink) for the
 overlap halos, ncclAllReduce for the CG reduction units — so a whole multi-pass solve is ONE
 C-ABI call per rank (ffb_run_on_frames_dev). The reductions are organised per subdomain row
-and summed in a fixed order: iterates and results are bitwise identical for any world size.
+and summed in a fixed order: iterates and results are bitwise identical for any world size at
+equal subdomain-solve cluster size (each rank sizes its clusters from its own subdomains).
 
 This module only wires the communicator:
   * ``init_nccl(ctx, rank, world)`` under torch.distributed (rank 0 makes the NCCL unique id,
