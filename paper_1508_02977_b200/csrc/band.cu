@@ -1583,6 +1583,330 @@ __global__ void __launch_bounds__(kST, 1)
   PROF_FLUSH(16);
 }
 
+// ----------------------------------------------------------------- K5b, row-group tiles
+// The ring kernel for one CTA per chain (c3, c4: lines of up to kRtMaxKd unknowns) with the
+// arithmetic cut into tiles. The packed rows stream through the two-stage ring in runs of
+// whole 16-row groups, and the lower triangle is processed as 16x32 tiles (group g, column
+// block J <= g/2), tile k of a line going to compute warp k mod 15. A lane holds 4 rows x 2
+// column pairs of a tile — 8 LDS.128 and 32 DFMA — and a 7-shuffle reduction gives the
+// tile's 16 row partials (T w) and 32 column partials (T^T w, the upper half the packed rows
+// leave out). Off-diagonal tiles need no masking at all. Each warp accumulates into its own
+// kd slot in a fixed tile order; the line's product is the 15 slots summed in warp order
+// (deterministic). Versus the row-batch loop of k_line_solve (every element masked, both
+// partials carried per column pair) this issues ~3x fewer instructions per element.
+constexpr int kRtMaxKd = 448;
+static_assert(kRtMaxKd <= kCT, "one operand element per compute thread");
+
+__device__ __forceinline__ int rt_first_tile(int g) {  // tiles of groups 0..g-1
+  const int h = g >> 1;
+  return (g & 1) ? (h + 1) * (h + 1) : h * (h + 1);
+}
+// end group of the ring chunk that starts at group g0: whole 16-row groups while they fit
+__device__ __forceinline__ int rt_chunk_end(int g0, int ng, int kd, int cap) {
+  const int base = prow_off32(16 * g0);
+  int g1 = g0 + 1;
+  while (g1 < ng && prow_off32(min(16 * (g1 + 1), kd)) - base <= cap) ++g1;
+  return g1;
+}
+
+// tile (rows R0..R0+15, columns C0..C0+31) of the chunk staged at shared address sb whose
+// first row starts at packed offset soff; adds T w into yacc[rows] and T^T w (strictly
+// lower part) into yacc[columns]. MASK: the diagonal tile (j <= i) or rows past the line.
+template <bool MASK>
+__device__ __forceinline__ void rt_tile(uint32_t sb, int soff, int R0, int C0, int kd,
+                                        const double* __restrict__ wv, double* __restrict__ yacc,
+                                        int lane) {
+  const int rg = lane >> 3, cg = lane & 7;
+  const int i0 = R0 + 4 * rg;  // even: rows i0, i0+1 have length i0+2, rows i0+2, i0+3 i0+4
+  const int j0 = C0 + 2 * cg;
+  int o[4];
+  o[0] = prow_off32(i0) - soff + j0;
+  o[1] = o[0] + i0 + 2;
+  o[2] = o[1] + i0 + 2;
+  o[3] = o[2] + i0 + 4;
+  double2 t[4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    // a row past the line reads row 0 of the chunk instead (masked below)
+    const int oa = (MASK && i0 + a >= kd) ? j0 : o[a];
+    const uint32_t ad = sb + 8u * static_cast<uint32_t>(oa);
+    t[a][0] = lds_f64x2(ad);
+    t[a][1] = lds_f64x2(ad + 128u);
+  }
+  double2 wc0 = *reinterpret_cast<const double2*>(wv + j0);
+  double2 wc1 = *reinterpret_cast<const double2*>(wv + j0 + 16);
+  const double2 wr01 = *reinterpret_cast<const double2*>(wv + i0);
+  const double2 wr23 = *reinterpret_cast<const double2*>(wv + i0 + 2);
+  double wr[4] = {wr01.x, wr01.y, wr23.x, wr23.y};
+  double tc[4][4];  // column-part copy (diagonal excluded under MASK)
+  double tr[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    tr[a][0] = t[a][0].x, tr[a][1] = t[a][0].y, tr[a][2] = t[a][1].x, tr[a][3] = t[a][1].y;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tc[a][c] = tr[a][c];
+  }
+  if (MASK) {
+    // slots past the line may hold anything (stale or never written): zero the operand there
+    wc0.x = j0 < kd ? wc0.x : 0.0;
+    wc0.y = j0 + 1 < kd ? wc0.y : 0.0;
+    wc1.x = j0 + 16 < kd ? wc1.x : 0.0;
+    wc1.y = j0 + 17 < kd ? wc1.y : 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = i0 + a;
+      wr[a] = i < kd ? wr[a] : 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int j = j0 + (c & 1) + 16 * (c >> 1);
+        const bool live = i < kd;
+        tc[a][c] = (live && j < i) ? tr[a][c] : 0.0;
+        tr[a][c] = (live && j <= i) ? tr[a][c] : 0.0;
+      }
+    }
+  }
+  double rp[4], cp[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    double v = tr[a][0] * wc0.x;
+    v = fma(tr[a][1], wc0.y, v);
+    v = fma(tr[a][2], wc1.x, v);
+    rp[a] = fma(tr[a][3], wc1.y, v);
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double v = tc[0][c] * wr[0];
+    v = fma(tc[1][c], wr[1], v);
+    v = fma(tc[2][c], wr[2], v);
+    cp[c] = fma(tc[3][c], wr[3], v);
+  }
+  // rows: sum over the 8 lanes of the row group -> lanes 2k, 2k+1 hold row i0 + k
+  const bool b2 = lane & 4, b1 = lane & 2;
+  double k0 = (b2 ? rp[2] : rp[0]) + __shfl_xor_sync(0xffffffffu, b2 ? rp[0] : rp[2], 4);
+  double k1 = (b2 ? rp[3] : rp[1]) + __shfl_xor_sync(0xffffffffu, b2 ? rp[1] : rp[3], 4);
+  double u = (b1 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, b1 ? k0 : k1, 2);
+  u += __shfl_xor_sync(0xffffffffu, u, 1);
+  // columns: sum over the 4 row groups -> lane holds column j0 + 16 h + e
+  const bool h = lane & 16, e = lane & 8;
+  double q0 = (h ? cp[2] : cp[0]) + __shfl_xor_sync(0xffffffffu, h ? cp[0] : cp[2], 16);
+  double q1 = (h ? cp[3] : cp[1]) + __shfl_xor_sync(0xffffffffu, h ? cp[1] : cp[3], 16);
+  const double v = (e ? q1 : q0) + __shfl_xor_sync(0xffffffffu, e ? q0 : q1, 8);
+  const int row = i0 + (cg >> 1);
+  const int col = j0 + (h ? 16 : 0) + (e ? 1 : 0);
+  if (!(lane & 1) && (!MASK || row < kd)) yacc[row] += u;
+  __syncwarp();  // the diagonal tile's rows and columns overlap: rows first, then columns
+  if (!MASK || col < kd) yacc[col] += v;
+  __syncwarp();
+}
+
+template <bool PERSIST>
+__global__ void __launch_bounds__(kST, 1)
+    k_line_solve_rt(const SubInfo* __restrict__ subs, const double* __restrict__ fac,
+                    const double* __restrict__ coef, size_t N, const double* __restrict__ r,
+                    double* __restrict__ ylocal, double* __restrict__ zlocal, int W, int nc,
+                    int cap, int kd_max, int phase_arg, const int* __restrict__ flags,
+                    const double* __restrict__ rlocal, int* __restrict__ qsync, int nsub_all) {
+  if (flags && (flags[0] | flags[1])) return;  // PCG converged or failed (grid-uniform)
+  constexpr int stages = 2;
+  // tasks as in k_line_solve: one chain per CTA, or (PERSIST) the dynamic queue of both sweeps
+  const int ntask = PERSIST ? 4 * nsub_all : 1;
+  auto decode = [&](int tk, int& ph, int& sub, int& chain) {
+    if (!PERSIST) {
+      ph = phase_arg, sub = static_cast<int>(blockIdx.x) >> 1, chain = blockIdx.x & 1;
+      return;
+    }
+    ph = tk >= 2 * nsub_all ? 1 : 0;
+    const int c2 = tk - ph * 2 * nsub_all;
+    sub = c2 >> 1, chain = c2 & 1;
+  };
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + 8;
+  uint64_t* tbar = empty + 8;  // [4] PERSIST: task id k published by the producer
+  uint64_t* tfree = tbar + 4;  // [4] PERSIST: the consumers have read task slot k
+  int* task_ids = reinterpret_cast<int*>(smem_raw + 240);  // [4]
+  double* stage0 = reinterpret_cast<double*>(smem_raw + kSolveHdr);
+  double* yacc = stage0 + static_cast<size_t>(stages) * cap;  // kCW x kd_max
+  double* wv = yacc + static_cast<size_t>(kCW) * kd_max;       // kd_max
+  double* xbuf = wv + kd_max;                                  // 2 x kd_max (line parity)
+  if (tid == 0) {
+    for (int q = 0; q < stages; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], kCW);
+    }
+    for (int q = 0; q < 4; ++q) {
+      mbar_init(&tbar[q], 1);
+      mbar_init(&tfree[q], 1);
+    }
+    fence_barrier_init();
+  }
+  for (int j = tid; j < (kCW + 3) * kd_max; j += kST) yacc[j] = 0.0;  // yacc, wv, xbuf
+  __syncthreads();
+
+  // ------------------------------------------------------------------ producer warp
+  if (warp == kCW) {
+    int q = 0;  // ring slots used so far (continues across tasks)
+    for (int kk = 0;; ++kk) {
+      int tk = kk;
+      if (PERSIST) {
+        if (lane == 0) {
+          if (kk >= 4) mbar_wait(&tfree[kk & 3], ((kk >> 2) - 1) & 1);
+          tk = atomicAdd(qsync, 1);
+          task_ids[kk & 3] = tk;
+          mbar_arrive(&tbar[kk & 3]);
+        }
+        tk = __shfl_sync(0xffffffffu, tk, 0);
+      }
+      if (tk >= ntask) break;
+      int phase, sub, chain;
+      decode(tk, phase, sub, chain);
+      const SubInfo s = subs[sub];
+      const int kd = s.kd, nl = chain_len(phase, chain, s), ng = (kd + 15) >> 4;
+      const double* F = fac + s.fac_off;
+      for (int t = 0; t < nl; ++t) {
+        const int l = chain_line(phase, chain, s, t);
+        for (int g0 = 0, g1; g0 < ng; g0 = g1, ++q) {
+          g1 = rt_chunk_end(g0, ng, kd, cap);
+          const int st = q % stages;
+          if (q >= stages) mbar_wait(&empty[st], ((q / stages) - 1) & 1);
+          const int o0 = prow_off32(16 * g0), o1 = prow_off32(min(16 * g1, kd));
+          if (lane == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(&full[st], static_cast<uint32_t>((o1 - o0) * sizeof(double)));
+            bulk_g2s(stage0 + static_cast<size_t>(st) * cap,
+                     F + static_cast<long long>(l) * s.line_sz + o0,
+                     static_cast<uint32_t>((o1 - o0) * sizeof(double)), &full[st]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ compute warps
+  int c_seq = 0;  // ring slots consumed (continues across tasks)
+  for (int kk = 0;; ++kk) {
+    int tk = kk;
+    if (PERSIST) {
+      mbar_wait(&tbar[kk & 3], (kk >> 2) & 1);
+      tk = task_ids[kk & 3];
+      compute_bar();  // every compute thread has read the slot
+      if (tid == 0) mbar_arrive(&tfree[kk & 3]);
+    }
+    if (tk >= ntask) break;
+    int phase, sub, chain;
+    decode(tk, phase, sub, chain);
+    const SubInfo s = subs[sub];
+    const int kd = s.kd, L = s.L, m = s.m, ng = (kd + 15) >> 4;
+    const int nl = chain_len(phase, chain, s);
+    if (nl == 0) continue;
+    double* yl = ylocal + s.vec_off;
+    double* zl = zlocal + s.vec_off;
+    const double* rl = rlocal ? rlocal + s.vec_off : nullptr;  // per-subdomain rhs (RAS mode)
+    if (PERSIST && kk > 0) {  // x of "line -1" is zero for every task
+      for (int j = tid; j < 2 * kd_max; j += kCT) xbuf[j] = 0.0;
+      compute_bar();
+    }
+    if (PERSIST && phase == 1) {  // both forward chains of this subdomain are done
+      if (tid == 0) {
+        const int need = (s.m > 0 ? 1 : 0) + (s.L - 1 - s.m > 0 ? 1 : 0);
+        while (ld_acquire_gpu(qsync + 1 + sub) < need) __nanosleep(100);
+      }
+      compute_bar();
+    }
+    // operand of line step t (k_line_solve), prefetched one step ahead; thread tid owns j = tid
+    double pf_r = 0.0, pf_b = 0.0, pf_y = 0.0;
+    auto prefetch = [&](int t) {
+      pf_r = pf_b = pf_y = 0.0;
+      const int j = tid;
+      if (t >= nl || j >= kd) return;
+      const int l = chain_line(phase, chain, s, t);
+      if (phase == 0) {
+        pf_r = rl ? rl[static_cast<long long>(l) * kd + j] : r[gidx(s, l, j, W, nc)];
+        if (t > 0) pf_b = bcoef(s, coef, N, W, nc, chain == 0 ? l : l + 1, j);
+      } else if (t == 0) {
+        double w = rl ? rl[static_cast<long long>(l) * kd + j] : r[gidx(s, l, j, W, nc)];
+        if (m > 0) w -= bcoef(s, coef, N, W, nc, m, j) * __ldcg(yl + static_cast<long long>(m - 1) * kd + j);
+        if (m < L - 1)
+          w -= bcoef(s, coef, N, W, nc, m + 1, j) * __ldcg(yl + static_cast<long long>(m + 1) * kd + j);
+        pf_r = w;
+      } else {
+        pf_b = bcoef(s, coef, N, W, nc, chain == 0 ? l + 1 : l, j);
+        pf_y = __ldcg(yl + static_cast<long long>(l) * kd + j);
+      }
+    };
+    prefetch(0);
+    for (int t = 0; t < nl; ++t) {
+      const int l = chain_line(phase, chain, s, t);
+      const int par = t & 1;
+      const bool subtract = phase == 1 && t > 0;  // x_l = y_l - Dinv_l w
+      const double* xprev = xbuf + (par ^ 1) * kd_max;
+      if (tid < kd)
+        wv[tid] = (phase == 0) ? pf_r - pf_b * xprev[tid] : (t == 0 ? pf_r : pf_b * xprev[tid]);
+      const double cur_y = pf_y;
+      prefetch(t + 1);
+      compute_bar();
+      for (int g0 = 0, g1; g0 < ng; g0 = g1, ++c_seq) {
+        g1 = rt_chunk_end(g0, ng, kd, cap);
+        const int st = c_seq % stages;
+        const int soff = prow_off32(16 * g0);
+        const uint32_t sb = smem_u32(stage0 + static_cast<size_t>(st) * cap);
+        const int T0 = rt_first_tile(g0), T1 = rt_first_tile(g1);
+        int tau = T0 + (warp - T0 % kCW + kCW) % kCW;
+        // every warp waits for the stage, tiles or not: a warp may not arrive on empty for the
+        // stage's next use before the producer has refilled it
+        mbar_wait(&full[st], (c_seq / stages) & 1);
+        {
+          double* ya = yacc + static_cast<size_t>(warp) * kd_max;
+          int g = g0;
+          for (; tau < T1; tau += kCW) {
+            while (rt_first_tile(g + 1) <= tau) ++g;
+            const int J = tau - rt_first_tile(g), I = g >> 1;
+            if (J < I && 16 * (g + 1) <= kd)
+              rt_tile<false>(sb, soff, 16 * g, 32 * J, kd, wv, ya, lane);
+            else
+              rt_tile<true>(sb, soff, 16 * g, 32 * J, kd, wv, ya, lane);
+          }
+        }
+        if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
+      }
+      compute_bar();
+      const int j = tid;
+      if (j < kd) {
+        double tv = 0.0;
+#pragma unroll 5
+        for (int w = 0; w < kCW; ++w) {
+          tv += yacc[w * kd_max + j];
+          yacc[w * kd_max + j] = 0.0;
+        }
+        const long long k = static_cast<long long>(l) * kd + j;
+        double v;
+        if (!subtract) {
+          v = tv;
+          if (phase == 0) {
+            yl[k] = v;
+            if (L == 1) zl[k] = v;
+          } else if (chain == mid_writer(s)) {
+            zl[k] = v;  // middle line, written once
+          }
+        } else {
+          v = cur_y - tv;
+          zl[k] = v;
+        }
+        xbuf[par * kd_max + j] = v;
+      }
+      compute_bar();
+    }
+    if (PERSIST && phase == 0) {  // publish this forward chain (y of its lines) to the queue
+      __threadfence();
+      compute_bar();
+      if (tid == 0) atomicAdd(qsync + 1 + sub, 1);
+    }
+  }
+}
+
 // ----------------------------------------------------------------- K6, register-tiled
 // Latency regime (lines whose packed triangle, split over the cluster, fits the register
 // file: c1, c2). A line step of the sweep is a dependent chain — the operand of line t needs
@@ -2298,7 +2622,8 @@ SolvePlan solve_plan(int kd_max, int C) {
   pl.tile = 0;
   const char* force = std::getenv("FFB_SOLVE");
   const bool ring_forced = force && std::string(force) == "ring";
-  if (!ring_forced && nt <= kTileMaxNt && nt * (nt + 1) / 2 <= kTileWarps * C) {
+  const bool rt_forced = force && std::string(force) == "rt" && C == 1 && kd_max <= kRtMaxKd;
+  if (!ring_forced && !rt_forced && nt <= kTileMaxNt && nt * (nt + 1) / 2 <= kTileWarps * C) {
     ensure_tile_tables_host();
     const int ci = C == 1 ? 0 : (C == 2 ? 1 : (C == 4 ? 2 : 3));
     // a stage holds a CTA's tiles of one line: the most over the CTAs and every line width
@@ -2326,6 +2651,20 @@ SolvePlan solve_plan(int kd_max, int C) {
     for (int n = 1; n <= nt; ++n) tables_ok = tables_ok && h_stage[ci][n] > 0;
     if (tables_ok && smem <= 227 * 1024) pl.tile = 1, pl.smem = smem;
   }
+  // row-group tiles (k_line_solve_rt) for one CTA per chain: two ring stages, each holding at
+  // least one 16-row group of the widest line; FFB_SOLVE=ring keeps the row-batch ring,
+  // FFB_SOLVE=rt takes the row-group tiles also where the register-tiled kernel fits
+  pl.rt = 0;
+  if (!pl.tile && !ring_forced && C == 1 && kd_max <= kRtMaxKd) {
+    const size_t fx = kSolveHdr + static_cast<size_t>(kCW + 3) * kd_max * sizeof(double);
+    const long long cap_rt = static_cast<long long>((budget - fx) / (2 * sizeof(double))) & ~1LL;
+    if (cap_rt >= 16LL * (kd_max + 2)) {
+      pl.rt = 1;
+      pl.stages = 2;
+      pl.cap = static_cast<int>(cap_rt);
+      pl.smem = fx + 2 * static_cast<size_t>(cap_rt) * sizeof(double);
+    }
+  }
   return pl;
 }
 
@@ -2343,7 +2682,19 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
     } else {
       // one CTA per chain: n_cta persistent CTAs pull the chains of both sweeps from a queue;
       // else one cluster per (subdomain, chain), one launch per sweep
-      if (qsync) {  // one launch for both sweeps (the dynamic queue holds them in order)
+      if (pl.rt) {
+        if (qsync) {
+          if (phase == 1) break;
+          FFB_CUDA(cudaMemsetAsync(qsync, 0, (nsub + 1) * sizeof(int), st));
+          launch_cluster(k_line_solve_rt<true>, n_cta, kST, pl.smem, 1, st, d_subs, fac, coef, N,
+                         r, ylocal, zlocal, W, nc, pl.cap, pl.kd_max, 0, flags, rlocal, qsync,
+                         nsub);
+        } else {
+          launch_cluster(k_line_solve_rt<false>, 2 * nsub, kST, pl.smem, 1, st, d_subs, fac,
+                         coef, N, r, ylocal, zlocal, W, nc, pl.cap, pl.kd_max, phase, flags,
+                         rlocal, nullptr, nsub);
+        }
+      } else if (qsync) {  // one launch for both sweeps (the dynamic queue holds them in order)
         if (phase == 1) break;
         FFB_CUDA(cudaMemsetAsync(qsync, 0, (nsub + 1) * sizeof(int), st));
         launch_cluster(k_line_solve<M, true>, n_cta, kST, pl.smem, 1, st, d_subs, fac, coef, N, r,

@@ -887,19 +887,21 @@ int ffb_debug_prof(unsigned long long* out64, int reset) {
 }
 
 // development probe: which subdomain-solve kernel the resident partition uses (1 the
-// register-tiled k_line_solve_tile, 0 the shared-memory ring k_line_solve, -1 none yet)
+// register-tiled k_line_solve_tile, 2 the row-group tile ring k_line_solve_rt, 0 the
+// row-batch ring k_line_solve, -1 none yet)
 int ffb_debug_solve_kernel(ffb_ctx* c) {
   if (!c || !c->have_part) return -1;
-  return c->plan.tile ? 1 : 0;
+  return c->plan.tile ? 1 : (c->plan.rt ? 2 : 0);
 }
 
 // development probe (host only, no device needed): the subdomain-solve plan for a widest
-// line of kd_max unknowns on C-CTA clusters — tile (1: register-tiled, 0: ring), its dynamic
+// line of kd_max unknowns on C-CTA clusters — tile (1: register-tiled, 2: row-group tile
+// ring, 0: row-batch ring), its dynamic
 // shared memory and, for the tiled kernel, the per-CTA line stage in doubles
 int ffb_debug_solve_plan(int kd_max, int C, int* tile, long long* smem, int* stage) {
   return guard([&] {
     const SolvePlan pl = solve_plan(kd_max, C);
-    if (tile) *tile = pl.tile;
+    if (tile) *tile = pl.tile ? 1 : (pl.rt ? 2 : 0);
     if (smem) *smem = static_cast<long long>(pl.smem);
     if (stage) *stage = pl.tile ? pl.stage_doubles : 0;
   });

@@ -96,6 +96,7 @@ void changed_lines(const SubInfo* d_subs, int nsub, const double* alpha, const d
                    int W, int H, int2* changed, cudaStream_t st);
 struct SolvePlan {
   int stages, cap, maxm, C, kd_max, tile, row_cost, ncs, stage_doubles;
+  int rt;  // row-group tile ring kernel (k_line_solve_rt)
   size_t smem;
 };
 SolvePlan solve_plan(int kd_max, int C);

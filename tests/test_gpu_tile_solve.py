@@ -75,6 +75,42 @@ def test_tile_solve_matches_ring_and_oracle(monkeypatch, port, H, W, px, py, ov,
         assert rel_l2(u_t[c], ref_u[c]) < 1e-9, c
 
 
+# k_line_solve_rt (row-group tiles, one CTA per chain): (H, W, px, py, ov, nc, FFB_SOLVE)
+RT_CASES = [
+    (40, 32, 1, 1, 0, 3, "rt"),    # kd 96: six 16-row groups, three diagonal tiles
+    (12, 9, 1, 1, 0, 3, "rt"),     # kd 27: one partial group, rows past the line
+    (50, 44, 3, 2, 4, 2, "rt"),    # two components, six subdomains
+    (130, 160, 2, 2, 3, 3, None),  # kd ~200: the default choice at one CTA per chain
+    (149, 160, 1, 1, 0, 3, None),  # kd 447: the widest line, odd, one group split over stages
+]
+
+
+@pytest.mark.parametrize("H,W,px,py,ov,nc,force", RT_CASES)
+def test_row_group_tiles_match_ring_and_oracle(monkeypatch, port, H, W, px, py, ov, nc, force):
+    f0, f1 = rand_pair(H, W, 5 * H + W)
+    t = port.frames_to_terms(f0, f1, 1.0, 2.5)
+    rng = np.random.default_rng(H * W)
+    ntri = 2 * (W - 1) * (H - 1)
+    a = rng.uniform(20, 1000, ntri)
+    l = np.full(ntri, 1000.0)
+    monkeypatch.setenv("FFB_CLUSTER", "1")
+    if force:
+        monkeypatch.setenv("FFB_SOLVE", force)
+    else:
+        monkeypatch.delenv("FFB_SOLVE", raising=False)
+    u_t, it_t, res_t, kind_t = solve(t, a, l, px, py, ov, nc)
+    monkeypatch.setenv("FFB_SOLVE", "ring")
+    u_r, it_r, res_r, kind_r = solve(t, a, l, px, py, ov, nc)
+    assert kind_t == 2, "the row-group tile kernel was not selected"
+    assert kind_r == 0
+    assert res_t <= 1e-12 and res_r <= 1e-12
+    assert abs(it_t - it_r) <= 2
+    ref_u, _, _ = port.cg_solve(t, a, l, nc, 1e-13)
+    for c in range(nc):
+        assert rel_l2(u_t[c], u_r[c]) < 1e-9, c
+        assert rel_l2(u_t[c], ref_u[c]) < 1e-9, c
+
+
 def test_tile_solve_deterministic(port):
     H, W = 96, 80
     f0, f1 = rand_pair(H, W, 3)

@@ -19,16 +19,18 @@ def plan(kd_max, clusters):
     return tile.value, smem.value, stage.value
 
 
-# (kd_max, cluster CTAs per chain, register-tiled?) for the configurations' line widths:
-# c1 198 on 8-CTA clusters, c2 297 on 4, c3/c4 423 on 1, c5 810 on 4
-@pytest.mark.parametrize("kd,clusters,tiled", [(198, 8, 1), (297, 4, 1), (423, 1, 0), (810, 4, 0),
+# (kd_max, cluster CTAs per chain, kernel: 1 register-tiled, 2 row-group tile ring, 0 row-batch
+# ring) for the configurations' line widths: c1 198 on 8-CTA clusters, c2 297 on 4, c3/c4 423
+# on 1, c5 810 on 4
+@pytest.mark.parametrize("kd,clusters,tiled", [(198, 8, 1), (297, 4, 1), (423, 1, 2), (810, 4, 0),
                                                (96, 8, 1), (96, 1, 1), (27, 1, 1), (320, 4, 0),
-                                               (480, 8, 0)])
+                                               (480, 8, 0), (448, 1, 2), (449, 1, 0),
+                                               (161, 1, 2)])
 def test_plan_kernel_choice(kd, clusters, tiled):
     tile, smem, stage = plan(kd, clusters)
     assert tile == tiled
     assert 0 < smem <= SMEM_MAX
-    if tile:
+    if tile == 1:
         # a CTA's share of one line at most a fair share plus one tile, and at least a share
         line = kd * (kd + 1) // 2
         assert line / clusters <= stage <= line / clusters + 2 * 1024 + 64
@@ -46,10 +48,19 @@ def test_plan_every_width_fits():
 @pytest.mark.parametrize("clusters,widest", [(1, 160), (2, 224), (4, 318), (8, 416)])
 def test_plan_switch_point(clusters, widest):
     assert plan(widest, clusters)[0] == 1
-    assert plan(widest + 1, clusters)[0] == 0
+    assert plan(widest + 1, clusters)[0] == (2 if clusters == 1 else 0)
 
 
 def test_plan_ring_override(monkeypatch):
     monkeypatch.setenv("FFB_SOLVE", "ring")
     tile, smem, _ = plan(297, 4)
     assert tile == 0 and 0 < smem <= SMEM_MAX
+    assert plan(423, 1)[0] == 0
+
+
+def test_plan_row_group_tiles_override(monkeypatch):
+    monkeypatch.setenv("FFB_SOLVE", "rt")
+    for kd in (27, 96, 160, 448):
+        tile, smem, _ = plan(kd, 1)
+        assert tile == 2 and 0 < smem <= SMEM_MAX
+    assert plan(198, 8)[0] == 1  # clusters: the override does not apply
