@@ -11,7 +11,7 @@
 template <int NB, int PAIR, int BUSY = 0>
 __global__ void k(const double* D, int kd, double* out, long long* cyc, int reps) {
   __shared__ __align__(16) double LR[NB * (NB + 1)];
-  __shared__ __align__(16) double Li[NB * (NB + 2)];
+  __shared__ __align__(16) double Li[NB * ffb::li_stride<NB>()];
   __shared__ double ir[NB];
   __shared__ int progress;
   __shared__ volatile int done;
@@ -52,7 +52,7 @@ __global__ void k(const double* D, int kd, double* out, long long* cyc, int reps
     }
     long long t1 = clock64();
     if (threadIdx.x == 0) cyc[0] = (t1 - t0) / reps, done = 1;
-    for (int i = threadIdx.x; i < NB * NB; i += 32) out[i] = Li[(i / NB) * (NB + 2) + i % NB];
+    for (int i = threadIdx.x; i < NB * NB; i += 32) out[i] = Li[(i / NB) * ffb::li_stride<NB>() + i % NB];
   }
 }
 
