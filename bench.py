@@ -375,7 +375,7 @@ def main():
         kind = fn(ctx.handle)
     except Exception:
         kind = -1
-    kname = {1: "k_line_solve_tile", 0: "k_line_solve"}.get(kind, "k_line_solve*")
+    kname = {1: "k_line_solve_tile", 2: "k_line_solve_rt", 0: "k_line_solve"}.get(kind, "k_line_solve*")
     achieved = asm_bytes / (s.ms_asm_per_iter * 1e-3) / 1e9 if s.ms_asm_per_iter > 0 else None
     iters_total = s.pcg_iterations
     line = {
