@@ -230,12 +230,10 @@ void frames_to_terms_dev(ffb_ctx* c, const double* f0, const double* f1, double 
   double* tmp = c->tmp.ensure(10 * N);
   smooth_planes(f0, s, tmp, W, H, 1, sigma, c->st);
   smooth_planes(f1, s + N, tmp, W, H, 1, sigma, c->st);
-  double* prod = c->tmp.p;  // 10 N
   double* t10 = c->t10.ensure(10 * N);
-  deriv_products(s, s + N, prod, W, H, c->st);
-  double* tmp2 = c->coef.ensure(10 * N);  // scratch; the coefficients are rebuilt afterwards
+  double* tmp2 = c->coef.ensure(10 * N);  // large-radius path only; coefficients rebuilt after
   c->coef_key_a = c->coef_key_t = -1;
-  smooth_planes(prod, t10, tmp2, W, H, 10, rho, c->st);
+  data_terms(s, s + N, t10, tmp, tmp2, W, H, rho, c->st);
   c->terms_version++;
 }
 
@@ -977,15 +975,15 @@ int ffb_build_data_terms(ffb_ctx* c, int W, int H, const double* fx, const doubl
     check_ctx(c);
     const size_t N = static_cast<size_t>(W) * H;
     double* in4 = c->work.ensure(4 * N);
-    double* prod = c->tmp.ensure(10 * N);
-    double* tmp = c->frames.ensure(20 * N);
+    double* t10 = c->tmp.ensure(10 * N);
+    double* scratch = c->frames.ensure(20 * N);  // large-radius path only
     upload(in4, fx, N, c->st);
     upload(in4 + N, fy, N, c->st);
     upload(in4 + 2 * N, ft, N, c->st);
     upload(in4 + 3 * N, f, N, c->st);
-    products_from4(in4, in4 + N, in4 + 2 * N, in4 + 3 * N, prod, W, H, c->st);
-    smooth_planes(prod, tmp, tmp + 10 * N, W, H, 10, rho, c->st);
-    download(out10, tmp, 10 * N, c->st);
+    data_terms_from4(in4, in4 + N, in4 + 2 * N, in4 + 3 * N, t10, scratch,
+                     scratch + 10 * N, W, H, rho, c->st);
+    download(out10, t10, 10 * N, c->st);
     sync(c);
   });
 }

@@ -40,12 +40,17 @@ Taps make_taps(double sigma);
 // same size; sigma <= 0 copies.
 void smooth_planes(const double* in, double* out, double* tmp, int W, int H, int planes,
                    double sigma, cudaStream_t st);
-void deriv_products(const double* s0, const double* s1, double* prod10, int W, int H,
-                    cudaStream_t st);
+// the ten rho-smoothed data-term planes from the smoothed frames (derivatives + products +
+// smoothing in one tiled kernel); prod and tmp (10 N each) are used only by the
+// large-radius / unsmoothed path
+void data_terms(const double* s0, const double* s1, double* t10, double* prod, double* tmp,
+                int W, int H, double rho, cudaStream_t st);
 void derivatives4(const double* s0, const double* s1, double* fx, double* fy, double* ft,
                   double* f, int W, int H, cudaStream_t st);
-void products_from4(const double* fx, const double* fy, const double* ft, const double* f,
-                    double* prod10, int W, int H, cudaStream_t st);
+// the same from given derivative planes (build_data_terms)
+void data_terms_from4(const double* fx, const double* fy, const double* ft, const double* f,
+                      double* t10, double* prod, double* tmp, int W, int H, double rho,
+                      cudaStream_t st);
 
 // ---- operator (operator.cu) -----------------------------------------------------------
 // Per-vertex coefficient planes (SoA, each N = W*H):
