@@ -1024,10 +1024,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "{\n"
       ".reg .pred P1;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)  // suspend-time hint: sleep in the wait instead of polling
       : "memory");
 }
 
@@ -1626,13 +1626,41 @@ __device__ __forceinline__ int rt_chunk_end(int g0, int ng, int kd, int cap) {
   return g1;
 }
 
+// The chunk and tile schedule of a line depends only on (kd, cap): the compute warps keep it
+// in two small tables in the shared-memory header, rebuilt when a task's kd differs from the
+// previous one's (per chunk and per tile the schedule arithmetic cost ~100 and ~25
+// instructions on every warp — 27% of the kernel's instructions, ncu r3c — against one
+// shared-memory load now).
+//   chunk c: {packed offset of its first row, T0 | T1 << 8 | (T0 mod kCW) << 16}
+//   tile tau: group | column block << 5 | kind << 9 (rt_tile's KIND, 0..3)
+constexpr int kRtTabChunks = 256;  // byte offset of the chunk table in the header (28 x 8 B)
+constexpr int kRtTabTiles = 480;   // byte offset of the tile table (<= 210 x 2 B)
+constexpr int kRtTabCount = 232;   // byte offset of the chunk count
+static_assert(kRtTabChunks + 8 * ((kRtMaxKd + 15) / 16) <= kRtTabTiles, "chunk table");
+static_assert(kRtTabTiles + 2 * (((kRtMaxKd + 15) / 16 + 1) / 2) * (((kRtMaxKd + 15) / 16) / 2 + 1) <=
+                  kSolveHdr, "tile table");
+
 // tile (rows R0..R0+15, columns C0..C0+31) of the chunk staged at shared address sb whose
 // first row starts at packed offset soff; adds T w into yacc[rows] and T^T w (strictly
-// lower part) into yacc[columns]. MASK: the diagonal tile (j <= i) or rows past the line.
-template <bool MASK>
+// lower part) into yacc[columns].
+//   KIND 0: a full off-diagonal tile, nothing masked.
+//   KIND 1: an off-diagonal tile of the line's last, partial row group.
+//   KIND 2: the diagonal tile of an even group (R0 == C0): columns C0..C0+15 triangular
+//           (j <= i), columns C0+16.. above the diagonal (not loaded).
+//   KIND 3: the diagonal tile of an odd group (R0 == C0 + 16): columns C0..C0+15 full,
+//           columns C0+16.. triangular.
+// Rows past the line (KIND != 0): their loads are redirected to row 0 of the chunk (finite
+// data), their operand is zero (so they add +-0 to the column sums) and their row sums are
+// dropped. The triangular half's masks depend on the lane only through d = 4 rg - 2 cg:
+// entry (a, c) is on or below the diagonal iff d + a - c >= 0. Operand slots past the line
+// hold finite values (zero, or an earlier task's), which the zeroed entries cancel.
+template <int KIND>
 __device__ __forceinline__ void rt_tile(uint32_t sb, int soff, int R0, int C0, int kd,
                                         const double* __restrict__ wv, double* __restrict__ yacc,
                                         int lane) {
+  constexpr bool DIAG = KIND >= 2;
+  constexpr bool HALF1 = KIND != 2;  // columns C0+16.. hold entries of the lower triangle
+  constexpr int TH = KIND == 2 ? 0 : 1;  // the triangular half of a diagonal tile
   const int rg = lane >> 3, cg = lane & 7;
   const int i0 = R0 + 4 * rg;  // even: rows i0, i0+1 have length i0+2, rows i0+2, i0+3 i0+4
   const int j0 = C0 + 2 * cg;
@@ -1644,18 +1672,17 @@ __device__ __forceinline__ void rt_tile(uint32_t sb, int soff, int R0, int C0, i
   double2 t[4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    // a row past the line reads row 0 of the chunk instead (masked below)
-    const int oa = (MASK && i0 + a >= kd) ? j0 : o[a];
+    const int oa = (KIND != 0 && i0 + a >= kd) ? j0 : o[a];
     const uint32_t ad = sb + 8u * static_cast<uint32_t>(oa);
     t[a][0] = lds_f64x2(ad);
-    t[a][1] = lds_f64x2(ad + 128u);
+    t[a][1] = HALF1 ? lds_f64x2(ad + 128u) : make_double2(0.0, 0.0);
   }
-  double2 wc0 = *reinterpret_cast<const double2*>(wv + j0);
-  double2 wc1 = *reinterpret_cast<const double2*>(wv + j0 + 16);
+  const double2 wc0 = *reinterpret_cast<const double2*>(wv + j0);
+  const double2 wc1 = HALF1 ? *reinterpret_cast<const double2*>(wv + j0 + 16) : make_double2(0.0, 0.0);
   const double2 wr01 = *reinterpret_cast<const double2*>(wv + i0);
   const double2 wr23 = *reinterpret_cast<const double2*>(wv + i0 + 2);
   double wr[4] = {wr01.x, wr01.y, wr23.x, wr23.y};
-  double tc[4][4];  // column-part copy (diagonal excluded under MASK)
+  double tc[4][4];  // column-part copy (a diagonal tile: without the diagonal)
   double tr[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
@@ -1663,35 +1690,37 @@ __device__ __forceinline__ void rt_tile(uint32_t sb, int soff, int R0, int C0, i
 #pragma unroll
     for (int c = 0; c < 4; ++c) tc[a][c] = tr[a][c];
   }
-  if (MASK) {
-    // slots past the line may hold anything (stale or never written): zero the operand there
-    wc0.x = j0 < kd ? wc0.x : 0.0;
-    wc0.y = j0 + 1 < kd ? wc0.y : 0.0;
-    wc1.x = j0 + 16 < kd ? wc1.x : 0.0;
-    wc1.y = j0 + 17 < kd ? wc1.y : 0.0;
+  if (KIND != 0) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int i = i0 + a;
-      wr[a] = i < kd ? wr[a] : 0.0;
+    for (int a = 0; a < 4; ++a) wr[a] = i0 + a < kd ? wr[a] : 0.0;
+  }
+  if (DIAG) {
+    const int d = 4 * rg - 2 * cg;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int j = j0 + (c & 1) + 16 * (c >> 1);
-        const bool live = i < kd;
-        tc[a][c] = (live && j < i) ? tr[a][c] : 0.0;
-        tr[a][c] = (live && j <= i) ? tr[a][c] : 0.0;
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        tc[a][2 * TH + c] = d + a - c > 0 ? tr[a][2 * TH + c] : 0.0;
+        tr[a][2 * TH + c] = d + a - c >= 0 ? tr[a][2 * TH + c] : 0.0;
       }
-    }
   }
   double rp[4], cp[4];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     double v = tr[a][0] * wc0.x;
     v = fma(tr[a][1], wc0.y, v);
-    v = fma(tr[a][2], wc1.x, v);
-    rp[a] = fma(tr[a][3], wc1.y, v);
+    if (HALF1) {
+      v = fma(tr[a][2], wc1.x, v);
+      v = fma(tr[a][3], wc1.y, v);
+    }
+    rp[a] = v;
   }
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
+    if (!HALF1 && c >= 2) {
+      cp[c] = 0.0;
+      continue;
+    }
     double v = tc[0][c] * wr[0];
     v = fma(tc[1][c], wr[1], v);
     v = fma(tc[2][c], wr[2], v);
@@ -1710,9 +1739,10 @@ __device__ __forceinline__ void rt_tile(uint32_t sb, int soff, int R0, int C0, i
   const double v = (e ? q1 : q0) + __shfl_xor_sync(0xffffffffu, e ? q0 : q1, 8);
   const int row = i0 + (cg >> 1);
   const int col = j0 + (h ? 16 : 0) + (e ? 1 : 0);
-  if (!(lane & 1) && (!MASK || row < kd)) yacc[row] += u;
-  __syncwarp();  // the diagonal tile's rows and columns overlap: rows first, then columns
-  if (!MASK || col < kd) yacc[col] += v;
+  if (!(lane & 1) && (KIND == 0 || row < kd)) yacc[row] += u;
+  // a diagonal tile's rows and columns overlap: rows first, then columns
+  if (DIAG) __syncwarp();
+  if (!DIAG || col < kd) yacc[col] += v;
   __syncwarp();
 }
 
@@ -1747,6 +1777,9 @@ __global__ void __launch_bounds__(kST, 1)
   double* yacc = stage0 + static_cast<size_t>(stages) * cap;  // kCW x kd_max
   double* wv = yacc + static_cast<size_t>(kCW) * kd_max;       // kd_max
   double* xbuf = wv + kd_max;                                  // 2 x kd_max (line parity)
+  int2* chunk_tab = reinterpret_cast<int2*>(smem_raw + kRtTabChunks);
+  unsigned short* tile_tab = reinterpret_cast<unsigned short*>(smem_raw + kRtTabTiles);
+  int* chunk_cnt = reinterpret_cast<int*>(smem_raw + kRtTabCount);
   if (tid == 0) {
     for (int q = 0; q < stages; ++q) {
       mbar_init(&full[q], 1);
@@ -1758,7 +1791,9 @@ __global__ void __launch_bounds__(kST, 1)
     }
     fence_barrier_init();
   }
-  for (int j = tid; j < (kCW + 3) * kd_max; j += kST) yacc[j] = 0.0;  // yacc, wv, xbuf
+  // yacc, wv, xbuf start at zero — and so do the ring stages: a masked tile row reads a finite
+  // stand-in from its stage (rt_tile), which must not be a NaN pattern of never-written memory
+  for (int j = tid; j < stages * cap + (kCW + 3) * kd_max; j += kST) stage0[j] = 0.0;
   __syncthreads();
 
   // ------------------------------------------------------------------ producer warp
@@ -1803,7 +1838,9 @@ __global__ void __launch_bounds__(kST, 1)
   }
 
   // ------------------------------------------------------------------ compute warps
-  int c_seq = 0;  // ring slots consumed (continues across tasks)
+  int c_seq = 0;    // ring slots consumed (continues across tasks)
+  int tab_kd = -1;  // line width the schedule tables hold
+  const uint32_t sb0 = smem_u32(stage0);
   for (int kk = 0;; ++kk) {
     int tk = kk;
     if (PERSIST) {
@@ -1822,6 +1859,43 @@ __global__ void __launch_bounds__(kST, 1)
     double* yl = ylocal + s.vec_off;
     double* zl = zlocal + s.vec_off;
     const double* rl = rlocal ? rlocal + s.vec_off : nullptr;  // per-subdomain rhs (RAS mode)
+    if (kd != tab_kd) {  // (re)build the schedule tables; every compute warp is past the last line
+      tab_kd = kd;
+      const int ntile = rt_first_tile(ng);
+      for (int tau = tid; tau < ntile; tau += kCT) {
+        int g = 0;
+        while (rt_first_tile(g + 1) <= tau) ++g;
+        const int J = tau - rt_first_tile(g), I = g >> 1;
+        const int kind = J == I ? 2 + (g & 1) : (16 * (g + 1) > kd ? 1 : 0);
+        tile_tab[tau] = static_cast<unsigned short>(g | (J << 5) | (kind << 9));
+      }
+      if (tid == 0) {
+        int c = 0;
+        for (int g0 = 0, g1; g0 < ng; g0 = g1, ++c) {
+          g1 = rt_chunk_end(g0, ng, kd, cap);
+          const int T0 = rt_first_tile(g0), T1 = rt_first_tile(g1);
+          chunk_tab[c] = make_int2(prow_off32(16 * g0), T0 | (T1 << 8) | ((T0 % kCW) << 16));
+        }
+        *chunk_cnt = c;
+      }
+      compute_bar();
+    }
+    const int nchunk = *chunk_cnt;
+    // thread tid owns unknown j = tid of every line: its vertex / component, the global index
+    // of its residual entry and of its slow-axis coupling as base + line * stride
+    long long g_base = 0, b_base = 0;
+    int g_stride = 0, b_stride = 0;
+    if (tid < kd) {
+      const int a = tid / nc, cc = tid - a * nc;
+      const long long v0 = static_cast<long long>(s.fy0 + (s.xfast ? 0 : a)) * W + s.fx0 + (s.xfast ? a : 0);
+      g_base = v0 * nc + cc;
+      g_stride = s.xfast ? W * nc : nc;
+      b_base = static_cast<long long>((s.xfast ? 8 : 6) + (cc < 2 ? 0 : 1)) * static_cast<long long>(N) +
+               v0 - (s.xfast ? W : 1);
+      b_stride = s.xfast ? W : 1;
+    }
+    auto gix = [&](int l) { return g_base + static_cast<long long>(l) * g_stride; };
+    auto bco = [&](int l) { return coef[b_base + static_cast<long long>(l) * b_stride]; };
     if (PERSIST && kk > 0) {  // x of "line -1" is zero for every task
       for (int j = tid; j < 2 * kd_max; j += kCT) xbuf[j] = 0.0;
       compute_bar();
@@ -1841,20 +1915,20 @@ __global__ void __launch_bounds__(kST, 1)
       if (t >= nl || j >= kd) return;
       const int l = chain_line(phase, chain, s, t);
       if (phase == 0) {
-        pf_r = rl ? rl[static_cast<long long>(l) * kd + j] : r[gidx(s, l, j, W, nc)];
-        if (t > 0) pf_b = bcoef(s, coef, N, W, nc, chain == 0 ? l : l + 1, j);
+        pf_r = rl ? rl[static_cast<long long>(l) * kd + j] : r[gix(l)];
+        if (t > 0) pf_b = bco(chain == 0 ? l : l + 1);
       } else if (t == 0) {
-        double w = rl ? rl[static_cast<long long>(l) * kd + j] : r[gidx(s, l, j, W, nc)];
-        if (m > 0) w -= bcoef(s, coef, N, W, nc, m, j) * __ldcg(yl + static_cast<long long>(m - 1) * kd + j);
-        if (m < L - 1)
-          w -= bcoef(s, coef, N, W, nc, m + 1, j) * __ldcg(yl + static_cast<long long>(m + 1) * kd + j);
+        double w = rl ? rl[static_cast<long long>(l) * kd + j] : r[gix(l)];
+        if (m > 0) w -= bco(m) * __ldcg(yl + static_cast<long long>(m - 1) * kd + j);
+        if (m < L - 1) w -= bco(m + 1) * __ldcg(yl + static_cast<long long>(m + 1) * kd + j);
         pf_r = w;
       } else {
-        pf_b = bcoef(s, coef, N, W, nc, chain == 0 ? l + 1 : l, j);
+        pf_b = bco(chain == 0 ? l + 1 : l);
         pf_y = __ldcg(yl + static_cast<long long>(l) * kd + j);
       }
     };
     prefetch(0);
+    double* ya = yacc + static_cast<size_t>(warp) * kd_max;
     for (int t = 0; t < nl; ++t) {
       const int l = chain_line(phase, chain, s, t);
       const int par = t & 1;
@@ -1865,27 +1939,27 @@ __global__ void __launch_bounds__(kST, 1)
       const double cur_y = pf_y;
       prefetch(t + 1);
       compute_bar();
-      for (int g0 = 0, g1; g0 < ng; g0 = g1, ++c_seq) {
-        g1 = rt_chunk_end(g0, ng, kd, cap);
-        const int st = c_seq % stages;
-        const int soff = prow_off32(16 * g0);
-        const uint32_t sb = smem_u32(stage0 + static_cast<size_t>(st) * cap);
-        const int T0 = rt_first_tile(g0), T1 = rt_first_tile(g1);
-        int tau = T0 + (warp - T0 % kCW + kCW) % kCW;
+      for (int c = 0; c < nchunk; ++c, ++c_seq) {
+        const int2 ce = chunk_tab[c];
+        const int soff = ce.x;
+        const int T0 = ce.y & 255, T1 = (ce.y >> 8) & 255, T0m = ce.y >> 16;
+        const int st = c_seq & 1;
+        const uint32_t sb = sb0 + static_cast<uint32_t>(st) * static_cast<uint32_t>(cap) * 8u;
+        int tau = T0 + warp - T0m + (warp < T0m ? kCW : 0);
         // every warp waits for the stage, tiles or not: a warp may not arrive on empty for the
         // stage's next use before the producer has refilled it
-        mbar_wait(&full[st], (c_seq / stages) & 1);
-        {
-          double* ya = yacc + static_cast<size_t>(warp) * kd_max;
-          int g = g0;
-          for (; tau < T1; tau += kCW) {
-            while (rt_first_tile(g + 1) <= tau) ++g;
-            const int J = tau - rt_first_tile(g), I = g >> 1;
-            if (J < I && 16 * (g + 1) <= kd)
-              rt_tile<false>(sb, soff, 16 * g, 32 * J, kd, wv, ya, lane);
-            else
-              rt_tile<true>(sb, soff, 16 * g, 32 * J, kd, wv, ya, lane);
-          }
+        mbar_wait(&full[st], (c_seq >> 1) & 1);
+        for (; tau < T1; tau += kCW) {
+          const int e = tile_tab[tau];
+          const int R0 = (e & 31) << 4, C0 = ((e >> 5) & 15) << 5, kind = e >> 9;
+          if (kind == 0)
+            rt_tile<0>(sb, soff, R0, C0, kd, wv, ya, lane);
+          else if (kind == 1)
+            rt_tile<1>(sb, soff, R0, C0, kd, wv, ya, lane);
+          else if (kind == 2)
+            rt_tile<2>(sb, soff, R0, C0, kd, wv, ya, lane);
+          else
+            rt_tile<3>(sb, soff, R0, C0, kd, wv, ya, lane);
         }
         if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
       }
