@@ -1626,6 +1626,17 @@ __device__ __forceinline__ int rt_chunk_end(int g0, int ng, int kd, int cap) {
   return g1;
 }
 
+// first row group of CTA q of a C-CTA cluster: the line's ng groups cut into C runs of about
+// equal tile counts (= equal bytes: a tile is 512 entries)
+__device__ __forceinline__ int rt_group_lo(int q, int C, int ng) {
+  if (q <= 0) return 0;
+  if (q >= C) return ng;
+  const int target = (rt_first_tile(ng) * q + C / 2) / C;
+  int g = 0;
+  while (g < ng && rt_first_tile(g) < target) ++g;
+  return g;
+}
+
 // The chunk and tile schedule of a line depends only on (kd, cap): the compute warps keep it
 // in two small tables in the shared-memory header, rebuilt when a task's kd differs from the
 // previous one's (per chunk and per tile the schedule arithmetic cost ~100 and ~25
@@ -1636,6 +1647,7 @@ __device__ __forceinline__ int rt_chunk_end(int g0, int ng, int kd, int cap) {
 constexpr int kRtTabChunks = 256;  // byte offset of the chunk table in the header (28 x 8 B)
 constexpr int kRtTabTiles = 480;   // byte offset of the tile table (<= 210 x 2 B)
 constexpr int kRtTabCount = 232;   // byte offset of the chunk count
+constexpr int kRtXbar = 192;       // byte offset of the two line-exchange mbarriers (clusters)
 static_assert(kRtTabChunks + 8 * ((kRtMaxKd + 15) / 16) <= kRtTabTiles, "chunk table");
 static_assert(kRtTabTiles + 2 * (((kRtMaxKd + 15) / 16 + 1) / 2) * (((kRtMaxKd + 15) / 16) / 2 + 1) <=
                   kSolveHdr, "tile table");
@@ -1746,6 +1758,12 @@ __device__ __forceinline__ void rt_tile(uint32_t sb, int soff, int R0, int C0, i
   __syncwarp();
 }
 
+// Clusters (C = 2 or 4 CTAs per chain, when a rank has fewer chains than SMs — multi-GPU
+// shards): CTA q streams and multiplies only its run of row groups (rt_group_lo: equal bytes),
+// so each SM ingests 1/C of the line; at the end of a line every CTA sends its kd partial sums
+// to the others (st.async into their shared memory, one transaction barrier per line parity)
+// and all of them add the C partials in CTA order, so every CTA holds the same x for the next
+// line's operand; CTA 0 writes the results. One launch per sweep (no task queue).
 template <bool PERSIST>
 __global__ void __launch_bounds__(kST, 1)
     k_line_solve_rt(const SubInfo* __restrict__ subs, const double* __restrict__ fac,
@@ -1755,11 +1773,14 @@ __global__ void __launch_bounds__(kST, 1)
                     const double* __restrict__ rlocal, int* __restrict__ qsync, int nsub_all) {
   if (flags && (flags[0] | flags[1])) return;  // PCG converged or failed (grid-uniform)
   constexpr int stages = 2;
-  // tasks as in k_line_solve: one chain per CTA, or (PERSIST) the dynamic queue of both sweeps
+  const int C = PERSIST ? 1 : static_cast<int>(cl_size());
+  const int crank = PERSIST ? 0 : static_cast<int>(cl_rank());
+  // tasks as in k_line_solve: one chain per cluster, or (PERSIST) the dynamic queue of both sweeps
   const int ntask = PERSIST ? 4 * nsub_all : 1;
   auto decode = [&](int tk, int& ph, int& sub, int& chain) {
     if (!PERSIST) {
-      ph = phase_arg, sub = static_cast<int>(blockIdx.x) >> 1, chain = blockIdx.x & 1;
+      const int cid = static_cast<int>(blockIdx.x) / C;
+      ph = phase_arg, sub = cid >> 1, chain = cid & 1;
       return;
     }
     ph = tk >= 2 * nsub_all ? 1 : 0;
@@ -1777,6 +1798,8 @@ __global__ void __launch_bounds__(kST, 1)
   double* yacc = stage0 + static_cast<size_t>(stages) * cap;  // kCW x kd_max
   double* wv = yacc + static_cast<size_t>(kCW) * kd_max;       // kd_max
   double* xbuf = wv + kd_max;                                  // 2 x kd_max (line parity)
+  double* xch = xbuf + 2 * kd_max;  // C > 1: 2 x C x kd_max partial sums (line parity, sender)
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(smem_raw + kRtXbar);  // [2] (line parity)
   int2* chunk_tab = reinterpret_cast<int2*>(smem_raw + kRtTabChunks);
   unsigned short* tile_tab = reinterpret_cast<unsigned short*>(smem_raw + kRtTabTiles);
   int* chunk_cnt = reinterpret_cast<int*>(smem_raw + kRtTabCount);
@@ -1789,12 +1812,14 @@ __global__ void __launch_bounds__(kST, 1)
       mbar_init(&tbar[q], 1);
       mbar_init(&tfree[q], 1);
     }
+    mbar_init(&xbar[0], 1);  // armed with the expected bytes by this CTA at every line
+    mbar_init(&xbar[1], 1);
     fence_barrier_init();
   }
   // yacc, wv, xbuf start at zero — and so do the ring stages: a masked tile row reads a finite
   // stand-in from its stage (rt_tile), which must not be a NaN pattern of never-written memory
   for (int j = tid; j < stages * cap + (kCW + 3) * kd_max; j += kST) stage0[j] = 0.0;
-  __syncthreads();
+  if (C > 1) cl_sync(); else __syncthreads();  // barriers initialised cluster-wide
 
   // ------------------------------------------------------------------ producer warp
   if (warp == kCW) {
@@ -1815,11 +1840,12 @@ __global__ void __launch_bounds__(kST, 1)
       decode(tk, phase, sub, chain);
       const SubInfo s = subs[sub];
       const int kd = s.kd, nl = chain_len(phase, chain, s), ng = (kd + 15) >> 4;
+      const int glo = rt_group_lo(crank, C, ng), ghi = rt_group_lo(crank + 1, C, ng);
       const double* F = fac + s.fac_off;
       for (int t = 0; t < nl; ++t) {
         const int l = chain_line(phase, chain, s, t);
-        for (int g0 = 0, g1; g0 < ng; g0 = g1, ++q) {
-          g1 = rt_chunk_end(g0, ng, kd, cap);
+        for (int g0 = glo, g1; g0 < ghi; g0 = g1, ++q) {
+          g1 = rt_chunk_end(g0, ghi, kd, cap);
           const int st = q % stages;
           if (q >= stages) mbar_wait(&empty[st], ((q / stages) - 1) & 1);
           const int o0 = prow_off32(16 * g0), o1 = prow_off32(min(16 * g1, kd));
@@ -1861,9 +1887,10 @@ __global__ void __launch_bounds__(kST, 1)
     const double* rl = rlocal ? rlocal + s.vec_off : nullptr;  // per-subdomain rhs (RAS mode)
     if (kd != tab_kd) {  // (re)build the schedule tables; every compute warp is past the last line
       tab_kd = kd;
-      const int ntile = rt_first_tile(ng);
-      for (int tau = tid; tau < ntile; tau += kCT) {
-        int g = 0;
+      const int glo = rt_group_lo(crank, C, ng), ghi = rt_group_lo(crank + 1, C, ng);
+      const int T_lo = rt_first_tile(glo), T_hi = rt_first_tile(ghi);
+      for (int tau = T_lo + tid; tau < T_hi; tau += kCT) {
+        int g = glo;
         while (rt_first_tile(g + 1) <= tau) ++g;
         const int J = tau - rt_first_tile(g), I = g >> 1;
         const int kind = J == I ? 2 + (g & 1) : (16 * (g + 1) > kd ? 1 : 0);
@@ -1871,10 +1898,10 @@ __global__ void __launch_bounds__(kST, 1)
       }
       if (tid == 0) {
         int c = 0;
-        for (int g0 = 0, g1; g0 < ng; g0 = g1, ++c) {
-          g1 = rt_chunk_end(g0, ng, kd, cap);
+        for (int g0 = glo, g1; g0 < ghi; g0 = g1, ++c) {
+          g1 = rt_chunk_end(g0, ghi, kd, cap);
           const int T0 = rt_first_tile(g0), T1 = rt_first_tile(g1);
-          chunk_tab[c] = make_int2(prow_off32(16 * g0), T0 | (T1 << 8) | ((T0 % kCW) << 16));
+          chunk_tab[c] = make_int2(prow_off32(16 * g0), T0 | (T1 << 8) | (((T0 - T_lo) % kCW) << 16));
         }
         *chunk_cnt = c;
       }
@@ -1938,6 +1965,8 @@ __global__ void __launch_bounds__(kST, 1)
         wv[tid] = (phase == 0) ? pf_r - pf_b * xprev[tid] : (t == 0 ? pf_r : pf_b * xprev[tid]);
       const double cur_y = pf_y;
       prefetch(t + 1);
+      // this line's incoming partial sums: kd doubles from each of the other CTAs
+      if (C > 1 && tid == 0) mbar_arrive_expect(&xbar[par], 8u * static_cast<uint32_t>(kd) * (C - 1));
       compute_bar();
       for (int c = 0; c < nchunk; ++c, ++c_seq) {
         const int2 ce = chunk_tab[c];
@@ -1972,19 +2001,32 @@ __global__ void __launch_bounds__(kST, 1)
           tv += yacc[w * kd_max + j];
           yacc[w * kd_max + j] = 0.0;
         }
+        if (C > 1) {
+          // all-to-all of the CTAs' partial sums; the line's product is their sum in CTA order
+          // on every CTA. A sender is at most one line ahead of a receiver (it needs the
+          // receiver's partials of the line before), so the two parities never collide.
+          double* mine = xch + static_cast<size_t>(par * C + crank) * kd_max + j;
+          *mine = tv;
+          for (int c = 0; c < C; ++c)
+            if (c != crank) st_async_remote(mine, tv, &xbar[par], static_cast<unsigned>(c));
+          mbar_wait_cluster(&xbar[par], (t >> 1) & 1);
+          tv = 0.0;
+          for (int c = 0; c < C; ++c) tv += xch[static_cast<size_t>(par * C + c) * kd_max + j];
+        }
         const long long k = static_cast<long long>(l) * kd + j;
+        const bool wr = crank == 0;
         double v;
         if (!subtract) {
           v = tv;
           if (phase == 0) {
-            yl[k] = v;
-            if (L == 1) zl[k] = v;
-          } else if (chain == mid_writer(s)) {
+            if (wr) yl[k] = v;
+            if (wr && L == 1) zl[k] = v;
+          } else if (wr && chain == mid_writer(s)) {
             zl[k] = v;  // middle line, written once
           }
         } else {
           v = cur_y - tv;
-          zl[k] = v;
+          if (wr) zl[k] = v;
         }
         xbuf[par * kd_max + j] = v;
       }
@@ -2713,7 +2755,7 @@ SolvePlan solve_plan(int kd_max, int C) {
   pl.tile = 0;
   const char* force = std::getenv("FFB_SOLVE");
   const bool ring_forced = force && std::string(force) == "ring";
-  const bool rt_forced = force && std::string(force) == "rt" && C == 1 && kd_max <= kRtMaxKd;
+  const bool rt_forced = force && std::string(force) == "rt" && C <= 4 && kd_max <= kRtMaxKd;
   if (!ring_forced && !rt_forced && nt <= kTileMaxNt && nt * (nt + 1) / 2 <= kTileWarps * C) {
     ensure_tile_tables_host();
     const int ci = C == 1 ? 0 : (C == 2 ? 1 : (C == 4 ? 2 : 3));
@@ -2742,12 +2784,13 @@ SolvePlan solve_plan(int kd_max, int C) {
     for (int n = 1; n <= nt; ++n) tables_ok = tables_ok && h_stage[ci][n] > 0;
     if (tables_ok && smem <= 227 * 1024) pl.tile = 1, pl.smem = smem;
   }
-  // row-group tiles (k_line_solve_rt) for one CTA per chain: two ring stages, each holding at
+  // row-group tiles (k_line_solve_rt) for one CTA per chain or clusters of 2 / 4 (each CTA a
+  // run of row groups, partial sums exchanged per line): two ring stages, each holding at
   // least one 16-row group of the widest line; FFB_SOLVE=ring keeps the row-batch ring,
   // FFB_SOLVE=rt takes the row-group tiles also where the register-tiled kernel fits
   pl.rt = 0;
-  if (!pl.tile && !ring_forced && C == 1 && kd_max <= kRtMaxKd) {
-    const size_t fx = kSolveHdr + static_cast<size_t>(kCW + 3) * kd_max * sizeof(double);
+  if (!pl.tile && !ring_forced && C <= 4 && kd_max <= kRtMaxKd) {
+    const size_t fx = kSolveHdr + (static_cast<size_t>(kCW + 3) + (C > 1 ? 2 * C : 0)) * kd_max * sizeof(double);
     const long long cap_rt = static_cast<long long>((budget - fx) / (2 * sizeof(double))) & ~1LL;
     if (cap_rt >= 16LL * (kd_max + 2)) {
       pl.rt = 1;
@@ -2781,8 +2824,8 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
                          r, ylocal, zlocal, W, nc, pl.cap, pl.kd_max, 0, flags, rlocal, qsync,
                          nsub);
         } else {
-          launch_cluster(k_line_solve_rt<false>, 2 * nsub, kST, pl.smem, 1, st, d_subs, fac,
-                         coef, N, r, ylocal, zlocal, W, nc, pl.cap, pl.kd_max, phase, flags,
+          launch_cluster(k_line_solve_rt<false>, 2 * nsub * pl.C, kST, pl.smem, pl.C, st, d_subs,
+                         fac, coef, N, r, ylocal, zlocal, W, nc, pl.cap, pl.kd_max, phase, flags,
                          rlocal, nullptr, nsub);
         }
       } else if (qsync) {  // one launch for both sweeps (the dynamic queue holds them in order)

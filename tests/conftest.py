@@ -19,6 +19,17 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: larger configurations")
 
 
+def pytest_collection_modifyitems(config, items):
+    """A device-side wait that never completes would block the whole run inside a C call, where a
+    signal cannot reach it: give every GPU test a watchdog thread (pytest-timeout, when present)
+    that dumps the stacks and ends the process instead."""
+    if not config.pluginmanager.hasplugin("timeout"):
+        return
+    for item in items:
+        if item.get_closest_marker("gpu") and not item.get_closest_marker("timeout"):
+            item.add_marker(pytest.mark.timeout(300, method="thread"))
+
+
 @pytest.fixture(scope="session")
 def port():
     """The plain-C restatement (always buildable; travels to the GPU box)."""

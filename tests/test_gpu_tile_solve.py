@@ -75,25 +75,33 @@ def test_tile_solve_matches_ring_and_oracle(monkeypatch, port, H, W, px, py, ov,
         assert rel_l2(u_t[c], ref_u[c]) < 1e-9, c
 
 
-# k_line_solve_rt (row-group tiles, one CTA per chain): (H, W, px, py, ov, nc, FFB_SOLVE)
+# k_line_solve_rt (row-group tiles; one CTA per chain or a cluster of 2 / 4 CTAs, each with its
+# run of row groups): (H, W, px, py, ov, nc, FFB_SOLVE, FFB_CLUSTER)
 RT_CASES = [
-    (40, 32, 1, 1, 0, 3, "rt"),    # kd 96: six 16-row groups, three diagonal tiles
-    (12, 9, 1, 1, 0, 3, "rt"),     # kd 27: one partial group, rows past the line
-    (50, 44, 3, 2, 4, 2, "rt"),    # two components, six subdomains
-    (130, 160, 2, 2, 3, 3, None),  # kd ~200: the default choice at one CTA per chain
-    (149, 160, 1, 1, 0, 3, None),  # kd 447: the widest line, odd, one group split over stages
+    (40, 32, 1, 1, 0, 3, "rt", "1"),    # kd 96: six 16-row groups, three diagonal tiles
+    (12, 9, 1, 1, 0, 3, "rt", "1"),     # kd 27: one partial group, rows past the line
+    (50, 44, 3, 2, 4, 2, "rt", "1"),    # two components, six subdomains
+    (130, 160, 2, 2, 3, 3, None, "1"),  # kd ~200: the default choice at one CTA per chain
+    (149, 160, 1, 1, 0, 3, None, "1"),  # kd 447: the widest line, odd, one group split over stages
+    (40, 32, 1, 1, 0, 3, "rt", "2"),    # 2-CTA clusters: groups 0-3 / 4-5
+    (12, 9, 1, 1, 0, 3, "rt", "4"),     # two groups on four CTAs: two CTAs only exchange zeros
+    (50, 44, 3, 2, 4, 2, "rt", "4"),    # two components, 4-CTA clusters
+    (130, 160, 2, 2, 3, 3, "rt", "2"),  # kd ~200 on 2-CTA clusters
+    (149, 160, 1, 1, 0, 3, None, "2"),  # kd 447 on 2-CTA clusters: the default choice there
+    (149, 160, 1, 1, 0, 3, None, "4"),  # and on 4
 ]
 
 
-@pytest.mark.parametrize("H,W,px,py,ov,nc,force", RT_CASES)
-def test_row_group_tiles_match_ring_and_oracle(monkeypatch, port, H, W, px, py, ov, nc, force):
+@pytest.mark.parametrize("H,W,px,py,ov,nc,force,cluster", RT_CASES)
+def test_row_group_tiles_match_ring_and_oracle(monkeypatch, port, H, W, px, py, ov, nc, force,
+                                               cluster):
     f0, f1 = rand_pair(H, W, 5 * H + W)
     t = port.frames_to_terms(f0, f1, 1.0, 2.5)
     rng = np.random.default_rng(H * W)
     ntri = 2 * (W - 1) * (H - 1)
     a = rng.uniform(20, 1000, ntri)
     l = np.full(ntri, 1000.0)
-    monkeypatch.setenv("FFB_CLUSTER", "1")
+    monkeypatch.setenv("FFB_CLUSTER", cluster)
     if force:
         monkeypatch.setenv("FFB_SOLVE", force)
     else:

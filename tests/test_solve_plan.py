@@ -21,9 +21,9 @@ def plan(kd_max, clusters):
 
 # (kd_max, cluster CTAs per chain, kernel: 1 register-tiled, 2 row-group tile ring, 0 row-batch
 # ring) for the configurations' line widths: c1 198 on 8-CTA clusters, c2 297 on 4, c3/c4 423
-# on 1, c5 810 on 4
+# on 1 (and on 2- or 4-CTA clusters for a multi-GPU shard), c5 810 on 4
 @pytest.mark.parametrize("kd,clusters,tiled", [(198, 8, 1), (297, 4, 1), (423, 1, 2), (810, 4, 0),
-                                               (96, 8, 1), (96, 1, 1), (27, 1, 1), (320, 4, 0),
+                                               (96, 8, 1), (96, 1, 1), (27, 1, 1), (320, 4, 2), (423, 2, 2),
                                                (480, 8, 0), (448, 1, 2), (449, 1, 0),
                                                (161, 1, 2)])
 def test_plan_kernel_choice(kd, clusters, tiled):
@@ -48,7 +48,8 @@ def test_plan_every_width_fits():
 @pytest.mark.parametrize("clusters,widest", [(1, 160), (2, 224), (4, 318), (8, 416)])
 def test_plan_switch_point(clusters, widest):
     assert plan(widest, clusters)[0] == 1
-    assert plan(widest + 1, clusters)[0] == (2 if clusters == 1 else 0)
+    # above it: the row-group tiles for one CTA per chain and clusters of 2 / 4, else the ring
+    assert plan(widest + 1, clusters)[0] == (2 if clusters <= 4 else 0)
 
 
 def test_plan_ring_override(monkeypatch):

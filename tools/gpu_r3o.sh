@@ -1,0 +1,4 @@
+# stress: the whole GPU suite three times (watchdog 300 s per test)
+for i in 1 2 3; do
+  ( time timeout 900 python -m pytest tests -x -q -m gpu ) 2>&1 | tail -6 | tr '\n' ' '; echo " [suite run $i]"
+done
