@@ -40,6 +40,13 @@ def parse():
     ap.add_argument("--config", default=os.environ.get("FFB_BENCH_CONFIG", "c4"))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # f64 (default, the headline): the preconditioner streams the subdomain factors in double.
+    # f32: the opt-in single-precision COPY of the factors (ffb_set_factor_storage; the
+    # factorisation, products, CG vectors and the stopping test stay in double, same 1e-8
+    # parity) as the measured arm. The default run also reports it, separately, under
+    # "variant_f32_factor_copy" unless --no-variants.
+    ap.add_argument("--factor-storage", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--no-variants", action="store_true")
     return ap.parse_args()
 
 
@@ -286,6 +293,8 @@ def main():
     stream = torch.cuda.Stream(dev)  # the launching stream: library kernels + timing events
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
+    if args.factor_storage == "f32":
+        ctx.set_factor_storage(32)
     rc = run_config_for(cfg, ff)
     H, W = cfg.H, cfg.W
     npx = H * W
@@ -367,7 +376,9 @@ def main():
         return
     s = stats[-1]
     peak, peak_kind = measured_peak()
-    asm_bytes = 8.0 * s.factor_doubles  # packed line inverses, forward + backward sweep
+    f32_in_use = ctx.factor_storage()[1] == 32
+    # packed line inverses, forward + backward sweep (4 bytes each from the opt-in f32 copy)
+    asm_bytes = (4.0 if f32_in_use else 8.0) * s.factor_doubles
     try:
         from paper_1508_02977_b200 import _lib
         fn = _lib.load().ffb_debug_solve_kernel
@@ -383,7 +394,8 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": workload_config(cfg),
+        "config": dict(workload_config(cfg), factor_storage="f32 copy streamed by the solve "
+                       "(factorisation, products, CG in f64)") if f32_in_use else workload_config(cfg),
         "parallelism": (f"row bands of subdomains over {world} GPUs, NCCL P2P halos + "
                         f"all-reduced CG units (bitwise equal to 1 GPU)") if world > 1 else "1gpu",
         "gpu_launches": int(launches),
@@ -405,6 +417,38 @@ def main():
                    if s.ms_pcg > 0 else None},
         "clocks": clk.summary(),
     }
+    if world == 1 and not args.no_variants and not f32_in_use:
+        # Reported beside the headline, never as it: the same step with the solve kernel streaming
+        # a single-precision copy of the subdomain factors (half the bytes per application;
+        # everything else in double, same parity bar — tests/test_gpu_fullsize.py)
+        ctx.set_stream(stream.cuda_stream)
+        ctx.set_factor_storage(32)
+        if ctx.factor_storage()[1] == 32:
+            step()
+            torch.cuda.synchronize()
+            va, vb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            nv = max(1, min(args.steps, 2))
+            vstats = None
+            flush.fill_(0.5)
+            va.record(stream)
+            for _ in range(nv):
+                vstats = step()
+            vb.record(stream)
+            torch.cuda.synchronize()
+            vms = va.elapsed_time(vb) / nv
+            line["variant_f32_factor_copy"] = {
+                "what": "opt-in ffb_set_factor_storage(32): the subdomain solve streams a "
+                        "single-precision copy of the line inverses; factorisation, products, CG "
+                        "vectors and the true-residual stopping test in f64; u within 1e-8 of the "
+                        "reference like the default (not the headline, which stores doubles)",
+                "value": npx / (vms * 1e-3) / 1e6, "unit": "Mpixel/s", "ms_per_step": vms,
+                "steps": nv, "pcg_iterations_per_step": vstats.pcg_iterations,
+                "ms_pcg": vstats.ms_pcg, "ms_factor": vstats.ms_factor,
+                "solve_ms_per_application": vstats.ms_asm_per_iter,
+                "solve_gbs": (4.0 * vstats.factor_doubles / (vstats.ms_asm_per_iter * 1e-3) / 1e9)
+                if vstats.ms_asm_per_iter > 0 else None}
+        ctx.set_factor_storage(64)
+        ctx.set_stream(None)
     if world == 1 and not args.no_cpu_baseline:
         dt, kind, cores, sample = cpu_reference_step(f0, f1, cfg)
         line["cpu_baseline"] = {"value": npx / dt / 1e6, "unit": "Mpixel/s", "cores": cores,

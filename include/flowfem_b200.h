@@ -89,6 +89,17 @@ int ffb_destroy(ffb_ctx* ctx);
  * default stream) when own == 0, or on the context's own stream when own != 0. Lets a host
  * framework order the solve with its own work and bracket it with its own events. */
 int ffb_set_stream(ffb_ctx* ctx, void* stream, int own);
+/* Storage of the subdomain factors the preconditioner streams (no reference counterpart: the
+ * reference's SparseCholesky, linsolve.hpp:32-48, keeps doubles). 64 (default): the packed
+ * line inverses in double. 32: opt-in — the solve kernel of the wide-line regime
+ * (k_line_solve_rt: c3, c4) streams a single-precision COPY of them, half the bytes per
+ * application; the factorisation, the products, the CG vectors and the stopping test on the
+ * true residual stay in double, so the converged fields meet the same 1e-8 bar
+ * (tests/test_gpu_fullsize.py). Environment FFB_FACTOR_F32=1 selects 32 at ffb_create.
+ * ffb_get_factor_storage: the requested width and the one in use with the resident partition
+ * (64 where another solve kernel runs). */
+int ffb_set_factor_storage(ffb_ctx* ctx, int bits);
+int ffb_get_factor_storage(ffb_ctx* ctx, int* bits, int* in_use);
 
 /* ---- imaging: include/flowfem/imaging.hpp ----------------------------------------- */
 /* gaussian_smooth (imaging.hpp:42-44, imaging.cpp:33-63) */

@@ -59,6 +59,8 @@ SIGNATURES = {
     "ffb_create": (_i, [C.POINTER(_vp), _i]),
     "ffb_destroy": (_i, [_vp]),
     "ffb_set_stream": (_i, [_vp, _vp, _i]),
+    "ffb_set_factor_storage": (_i, [_vp, _i]),
+    "ffb_get_factor_storage": (_i, [_vp, C.POINTER(_i), C.POINTER(_i)]),
     "ffb_gaussian_smooth": (_i, [_vp, _i, _i, _vp, _d, _vp]),
     "ffb_compute_derivatives": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ffb_build_data_terms": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _d, _vp]),

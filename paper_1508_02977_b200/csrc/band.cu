@@ -1037,6 +1037,21 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t addr) {
   return v;
 }
 
+// two consecutive entries of a staged factor row as doubles (FT = double: one 16-byte load;
+// float, the opt-in single-precision factor copy: one 8-byte load, widened)
+template <class FT>
+__device__ __forceinline__ double2 lds_pair(uint32_t addr);
+template <>
+__device__ __forceinline__ double2 lds_pair<double>(uint32_t addr) {
+  return lds_f64x2(addr);
+}
+template <>
+__device__ __forceinline__ double2 lds_pair<float>(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return make_double2(static_cast<double>(v.x), static_cast<double>(v.y));
+}
+
 // R per-lane partial sums (R = 4 or 8 rows) -> lane ends with the warp total of row
 // lane / (32 / R): halving exchanges (16, 8[, 4]) then a butterfly over the rest
 template <int R>
@@ -1666,7 +1681,7 @@ static_assert(kRtTabTiles + 2 * (((kRtMaxKd + 15) / 16 + 1) / 2) * (((kRtMaxKd +
 // dropped. The triangular half's masks depend on the lane only through d = 4 rg - 2 cg:
 // entry (a, c) is on or below the diagonal iff d + a - c >= 0. Operand slots past the line
 // hold finite values (zero, or an earlier task's), which the zeroed entries cancel.
-template <int KIND>
+template <int KIND, class FT>
 __device__ __forceinline__ void rt_tile(uint32_t sb, int soff, int R0, int C0, int kd,
                                         const double* __restrict__ wv, double* __restrict__ yacc,
                                         int lane) {
@@ -1685,9 +1700,9 @@ __device__ __forceinline__ void rt_tile(uint32_t sb, int soff, int R0, int C0, i
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     const int oa = (KIND != 0 && i0 + a >= kd) ? j0 : o[a];
-    const uint32_t ad = sb + 8u * static_cast<uint32_t>(oa);
-    t[a][0] = lds_f64x2(ad);
-    t[a][1] = HALF1 ? lds_f64x2(ad + 128u) : make_double2(0.0, 0.0);
+    const uint32_t ad = sb + static_cast<uint32_t>(sizeof(FT)) * static_cast<uint32_t>(oa);
+    t[a][0] = lds_pair<FT>(ad);
+    t[a][1] = HALF1 ? lds_pair<FT>(ad + 16u * static_cast<uint32_t>(sizeof(FT))) : make_double2(0.0, 0.0);
   }
   const double2 wc0 = *reinterpret_cast<const double2*>(wv + j0);
   const double2 wc1 = HALF1 ? *reinterpret_cast<const double2*>(wv + j0 + 16) : make_double2(0.0, 0.0);
@@ -1764,9 +1779,13 @@ __device__ __forceinline__ void rt_tile(uint32_t sb, int soff, int R0, int C0, i
 // to the others (st.async into their shared memory, one transaction barrier per line parity)
 // and all of them add the C partials in CTA order, so every CTA holds the same x for the next
 // line's operand; CTA 0 writes the results. One launch per sweep (no task queue).
-template <bool PERSIST>
+// FT = float streams the single-precision copy of the line inverses (factor_to_f32: opt-in,
+// half the bytes per application; the products and sums stay in double): fac then points at
+// that copy, a line of it starts at fac32_off + l * ((line_sz + 3) & ~3) floats, and `cap`
+// counts floats (twice the doubles the same stage holds).
+template <bool PERSIST, class FT>
 __global__ void __launch_bounds__(kST, 1)
-    k_line_solve_rt(const SubInfo* __restrict__ subs, const double* __restrict__ fac,
+    k_line_solve_rt(const SubInfo* __restrict__ subs, const FT* __restrict__ fac,
                     const double* __restrict__ coef, size_t N, const double* __restrict__ r,
                     double* __restrict__ ylocal, double* __restrict__ zlocal, int W, int nc,
                     int cap, int kd_max, int phase_arg, const int* __restrict__ flags,
@@ -1794,10 +1813,12 @@ __global__ void __launch_bounds__(kST, 1)
   uint64_t* tbar = empty + 8;  // [4] PERSIST: task id k published by the producer
   uint64_t* tfree = tbar + 4;  // [4] PERSIST: the consumers have read task slot k
   int* task_ids = reinterpret_cast<int*>(smem_raw + 240);  // [4]
+  constexpr int kEls = 8 / static_cast<int>(sizeof(FT));  // factor entries per double of stage
+  const int cap_d = cap / kEls;                           // a stage in doubles
   double* stage0 = reinterpret_cast<double*>(smem_raw + kSolveHdr);
-  double* yacc = stage0 + static_cast<size_t>(stages) * cap;  // kCW x kd_max
-  double* wv = yacc + static_cast<size_t>(kCW) * kd_max;       // kd_max
-  double* xbuf = wv + kd_max;                                  // 2 x kd_max (line parity)
+  double* yacc = stage0 + static_cast<size_t>(stages) * cap_d;  // kCW x kd_max
+  double* wv = yacc + static_cast<size_t>(kCW) * kd_max;         // kd_max
+  double* xbuf = wv + kd_max;                                    // 2 x kd_max (line parity)
   double* xch = xbuf + 2 * kd_max;  // C > 1: 2 x C x kd_max partial sums (line parity, sender)
   uint64_t* xbar = reinterpret_cast<uint64_t*>(smem_raw + kRtXbar);  // [2] (line parity)
   int2* chunk_tab = reinterpret_cast<int2*>(smem_raw + kRtTabChunks);
@@ -1818,7 +1839,7 @@ __global__ void __launch_bounds__(kST, 1)
   }
   // yacc, wv, xbuf start at zero — and so do the ring stages: a masked tile row reads a finite
   // stand-in from its stage (rt_tile), which must not be a NaN pattern of never-written memory
-  for (int j = tid; j < stages * cap + (kCW + 3) * kd_max; j += kST) stage0[j] = 0.0;
+  for (int j = tid; j < stages * cap_d + (kCW + 3) * kd_max; j += kST) stage0[j] = 0.0;
   if (C > 1) cl_sync(); else __syncthreads();  // barriers initialised cluster-wide
 
   // ------------------------------------------------------------------ producer warp
@@ -1841,7 +1862,9 @@ __global__ void __launch_bounds__(kST, 1)
       const SubInfo s = subs[sub];
       const int kd = s.kd, nl = chain_len(phase, chain, s), ng = (kd + 15) >> 4;
       const int glo = rt_group_lo(crank, C, ng), ghi = rt_group_lo(crank + 1, C, ng);
-      const double* F = fac + s.fac_off;
+      const bool f32 = sizeof(FT) == 4;
+      const FT* F = fac + (f32 ? s.fac32_off : s.fac_off);
+      const long long lstride = f32 ? ((s.line_sz + 3) & ~3LL) : s.line_sz;
       for (int t = 0; t < nl; ++t) {
         const int l = chain_line(phase, chain, s, t);
         for (int g0 = glo, g1; g0 < ghi; g0 = g1, ++q) {
@@ -1849,12 +1872,14 @@ __global__ void __launch_bounds__(kST, 1)
           const int st = q % stages;
           if (q >= stages) mbar_wait(&empty[st], ((q / stages) - 1) & 1);
           const int o0 = prow_off32(16 * g0), o1 = prow_off32(min(16 * g1, kd));
+          // bulk copies move multiples of 16 bytes: a float chunk's tail rounds up into the
+          // line's padding
+          const uint32_t bytes = (static_cast<uint32_t>(o1 - o0) * static_cast<uint32_t>(sizeof(FT)) + 15u) & ~15u;
           if (lane == 0) {
             fence_proxy_async();
-            mbar_expect_tx(&full[st], static_cast<uint32_t>((o1 - o0) * sizeof(double)));
-            bulk_g2s(stage0 + static_cast<size_t>(st) * cap,
-                     F + static_cast<long long>(l) * s.line_sz + o0,
-                     static_cast<uint32_t>((o1 - o0) * sizeof(double)), &full[st]);
+            mbar_expect_tx(&full[st], bytes);
+            bulk_g2s(stage0 + static_cast<size_t>(st) * cap_d, F + static_cast<long long>(l) * lstride + o0,
+                     bytes, &full[st]);
           }
           __syncwarp();
         }
@@ -1973,7 +1998,7 @@ __global__ void __launch_bounds__(kST, 1)
         const int soff = ce.x;
         const int T0 = ce.y & 255, T1 = (ce.y >> 8) & 255, T0m = ce.y >> 16;
         const int st = c_seq & 1;
-        const uint32_t sb = sb0 + static_cast<uint32_t>(st) * static_cast<uint32_t>(cap) * 8u;
+        const uint32_t sb = sb0 + static_cast<uint32_t>(st) * static_cast<uint32_t>(cap_d) * 8u;
         int tau = T0 + warp - T0m + (warp < T0m ? kCW : 0);
         // every warp waits for the stage, tiles or not: a warp may not arrive on empty for the
         // stage's next use before the producer has refilled it
@@ -1982,13 +2007,13 @@ __global__ void __launch_bounds__(kST, 1)
           const int e = tile_tab[tau];
           const int R0 = (e & 31) << 4, C0 = ((e >> 5) & 15) << 5, kind = e >> 9;
           if (kind == 0)
-            rt_tile<0>(sb, soff, R0, C0, kd, wv, ya, lane);
+            rt_tile<0, FT>(sb, soff, R0, C0, kd, wv, ya, lane);
           else if (kind == 1)
-            rt_tile<1>(sb, soff, R0, C0, kd, wv, ya, lane);
+            rt_tile<1, FT>(sb, soff, R0, C0, kd, wv, ya, lane);
           else if (kind == 2)
-            rt_tile<2>(sb, soff, R0, C0, kd, wv, ya, lane);
+            rt_tile<2, FT>(sb, soff, R0, C0, kd, wv, ya, lane);
           else
-            rt_tile<3>(sb, soff, R0, C0, kd, wv, ya, lane);
+            rt_tile<3, FT>(sb, soff, R0, C0, kd, wv, ya, lane);
         }
         if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
       }
@@ -2559,6 +2584,39 @@ void changed_lines(const SubInfo* d_subs, int nsub, const double* alpha, const d
   FFB_LAUNCHED();
 }
 
+// Single-precision copy of the packed line inverses for the opt-in f32 solve stream: lines
+// [lo, hi] of every subdomain (the ones the last factorisation rewrote; all without `changed`),
+// a line of the copy at fac32_off + l * ((line_sz + 3) & ~3). blockIdx.y strides the lines.
+__global__ void __launch_bounds__(256)
+    k_fac_to_f32(const SubInfo* __restrict__ subs, const double* __restrict__ fac,
+                 float* __restrict__ fac32, const int2* __restrict__ changed) {
+  const SubInfo s = subs[blockIdx.x];
+  int2 chg = changed ? changed[blockIdx.x] : make_int2(0, s.L - 1);
+  if (chg.x > chg.y) return;  // nothing changed in this subdomain
+  // chain 0 restarts at the first changed line and runs to the middle, chain 1 at the last
+  // one, and the middle line is redone (k_line_factor)
+  chg.x = min(chg.x, s.m), chg.y = max(chg.y, s.m);
+  const long long lstride = (s.line_sz + 3) & ~3LL;
+  for (int l = chg.x + static_cast<int>(blockIdx.y); l <= chg.y; l += gridDim.y) {
+    const double2* src = reinterpret_cast<const double2*>(fac + s.fac_off + static_cast<long long>(l) * s.line_sz);
+    float2* dst = reinterpret_cast<float2*>(fac32 + s.fac32_off + static_cast<long long>(l) * lstride);
+    const long long n2 = s.line_sz >> 1;  // line_sz is even
+    for (long long i = threadIdx.x; i < n2; i += blockDim.x) {
+      const double2 v = src[i];
+      dst[i] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
+    }
+    if (threadIdx.x < 2 && (s.line_sz & 3))  // the stride's padding: read by the chunk tails
+      fac32[s.fac32_off + static_cast<long long>(l) * lstride + s.line_sz + threadIdx.x] = 0.0f;
+  }
+}
+
+void factor_to_f32(const SubInfo* d_subs, int nsub, const double* fac, float* fac32,
+                   const int2* changed, cudaStream_t st) {
+  if (nsub <= 0) return;
+  k_fac_to_f32<<<dim3(nsub, 64), 256, 0, st>>>(d_subs, fac, fac32, changed);
+  FFB_LAUNCHED();
+}
+
 void line_factor(const SubInfo* d_subs, int nsub, int C, int nb, int kd_max,
                  const double* coef, size_t N, int W, int nc, double* fac, double* scratch,
                  long long scratch_stride, int* d_bad, cudaStream_t st, const int2* changed,
@@ -2806,7 +2864,8 @@ template <int M>
 static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
                            const double* fac, const double* coef, size_t N, const double* r,
                            double* ylocal, double* zlocal, int W, int nc, const int* flags,
-                           const double* rlocal, cudaStream_t st, int* qsync, int n_cta) {
+                           const double* rlocal, cudaStream_t st, int* qsync, int n_cta,
+                           const float* fac32) {
   for (int phase = 0; phase <= 1; ++phase) {
     if (pl.tile) {
       set_tile_tables();
@@ -2816,17 +2875,29 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
     } else {
       // one CTA per chain: n_cta persistent CTAs pull the chains of both sweeps from a queue;
       // else one cluster per (subdomain, chain), one launch per sweep
-      if (pl.rt) {
+      if (pl.rt && fac32) {  // the single-precision factor copy: a stage holds 2 cap floats
         if (qsync) {
           if (phase == 1) break;
           FFB_CUDA(cudaMemsetAsync(qsync, 0, (nsub + 1) * sizeof(int), st));
-          launch_cluster(k_line_solve_rt<true>, n_cta, kST, pl.smem, 1, st, d_subs, fac, coef, N,
-                         r, ylocal, zlocal, W, nc, pl.cap, pl.kd_max, 0, flags, rlocal, qsync,
-                         nsub);
+          launch_cluster(k_line_solve_rt<true, float>, n_cta, kST, pl.smem, 1, st, d_subs, fac32,
+                         coef, N, r, ylocal, zlocal, W, nc, 2 * pl.cap, pl.kd_max, 0, flags, rlocal,
+                         qsync, nsub);
         } else {
-          launch_cluster(k_line_solve_rt<false>, 2 * nsub * pl.C, kST, pl.smem, pl.C, st, d_subs,
-                         fac, coef, N, r, ylocal, zlocal, W, nc, pl.cap, pl.kd_max, phase, flags,
-                         rlocal, nullptr, nsub);
+          launch_cluster(k_line_solve_rt<false, float>, 2 * nsub * pl.C, kST, pl.smem, pl.C, st,
+                         d_subs, fac32, coef, N, r, ylocal, zlocal, W, nc, 2 * pl.cap, pl.kd_max,
+                         phase, flags, rlocal, nullptr, nsub);
+        }
+      } else if (pl.rt) {
+        if (qsync) {
+          if (phase == 1) break;
+          FFB_CUDA(cudaMemsetAsync(qsync, 0, (nsub + 1) * sizeof(int), st));
+          launch_cluster(k_line_solve_rt<true, double>, n_cta, kST, pl.smem, 1, st, d_subs, fac,
+                         coef, N, r, ylocal, zlocal, W, nc, pl.cap, pl.kd_max, 0, flags, rlocal,
+                         qsync, nsub);
+        } else {
+          launch_cluster(k_line_solve_rt<false, double>, 2 * nsub * pl.C, kST, pl.smem, pl.C, st,
+                         d_subs, fac, coef, N, r, ylocal, zlocal, W, nc, pl.cap, pl.kd_max, phase,
+                         flags, rlocal, nullptr, nsub);
         }
       } else if (qsync) {  // one launch for both sweeps (the dynamic queue holds them in order)
         if (phase == 1) break;
@@ -2847,24 +2918,24 @@ static void launch_solve_m(const SubInfo* d_subs, int nsub, const SolvePlan& pl,
 void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,
                 const double* coef, size_t N, const double* r, double* ylocal, double* zlocal,
                 int W, int nc, const int* flags, cudaStream_t st, const double* rlocal,
-                int* qsync, int n_cta) {
+                int* qsync, int n_cta, const float* fac32) {
   if (pl.tile || pl.C != 1) qsync = nullptr;  // the task queue: ring kernel, one CTA per chain
   if (nsub <= 0) return;  // a rank without subdomains (world > parts)
   if (pl.maxm <= 4)
     launch_solve_m<4>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
-                      qsync, n_cta);
+                      qsync, n_cta, fac32);
   else if (pl.maxm <= 8)
     launch_solve_m<8>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
-                      qsync, n_cta);
+                      qsync, n_cta, fac32);
   else if (pl.maxm <= 14)
     launch_solve_m<14>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
-                      qsync, n_cta);
+                      qsync, n_cta, fac32);
   else if (pl.maxm <= 20)
     launch_solve_m<20>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
-                      qsync, n_cta);
+                      qsync, n_cta, fac32);
   else if (pl.maxm <= 26)
     launch_solve_m<26>(d_subs, nsub, pl, fac, coef, N, r, ylocal, zlocal, W, nc, flags, rlocal, st,
-                      qsync, n_cta);
+                      qsync, n_cta, fac32);
   else
     fail("linsolve.cholesky: subdomain line too wide (kd > 832)");
 }

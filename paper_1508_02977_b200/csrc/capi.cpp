@@ -125,6 +125,11 @@ struct ffb_ctx {
   DBuf<SubInfo> d_subs;
   DBuf<AxisMap> d_col, d_row;
   DBuf<double> fac, fac_t, dscratch, ylocal, zlocal, rlocal, xlocal, G0, G1, incs;
+  // opt-in (ffb_set_factor_storage 32 / FFB_FACTOR_F32=1): the row-group tile solve streams a
+  // single-precision copy of the line inverses (half the bytes per application); the
+  // factorisation, the products and every CG vector stay in double
+  int factor_bits = 64;
+  DBuf<float> fac32;
   DBuf<int> own_col, own_row;
   // two-level coarse space (coarse.cu): core cuts, coarse node maps, A0 band + inverse
   bool coarse = true;
@@ -356,7 +361,7 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
     }
     c->plan = solve_plan(kd_max, c->ccl);
   }
-  long long fac_off = 0, vec_off = 0;
+  long long fac_off = 0, vec_off = 0, fac32_off = 0;
   double fd = 0, ad = 0, sn = 0, ff = 0;
   for (int p = 0; p < np; ++p) {
     SubInfo& s = c->subs[p];
@@ -373,7 +378,9 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
     s.m = (s.L - 1) / 2;  // the middle line of the twisted factorisation
     s.fac_off = fac_off;
     s.vec_off = vec_off;
+    s.fac32_off = fac32_off;
     if (p < c->s_lo || p >= c->s_hi) continue;  // another rank's subdomain: no storage here
+    fac32_off += (((s.line_sz + 3) & ~3LL) * s.L + 31) / 32 * 32;
     fac_off += (s.line_sz * s.L + 31) / 32 * 32;
     vec_off += (n + 31) / 32 * 32;
     fd += static_cast<double>(s.line_sz) * s.L;
@@ -421,6 +428,8 @@ void ensure_partition(ffb_ctx* c, int px, int py, int ov, int nc) {
                            c->st));
   c->fac.ensure(fac_off);
   if (c->plan.tile) c->fac_t.ensure(fac_off);  // tile-major copy for the register-tiled solve
+  if (c->factor_bits == 32 && c->plan.rt) c->fac32.ensure(fac32_off + 32);
+  else c->fac32.release();
   c->dscratch.ensure(factor_scratch_doubles(c->s_hi - c->s_lo, kd_max));
   c->ylocal.ensure(vec_off);
   c->zlocal.ensure(vec_off);
@@ -481,6 +490,8 @@ void ensure_factor(ffb_ctx* c, int nc) {
   line_factor(c->d_subs.p + c->s_lo, np, c->ccl, c->nbf, c->kd_max, c->coef.p, c->N, c->W, nc,
               c->fac.p, c->dscratch.p, static_cast<long long>(c->kd_max) * c->kd_max, c->d_bad.p,
               c->st, changed, c->plan.tile ? c->fac_t.p : nullptr);
+  if (c->fac32.p)
+    factor_to_f32(c->d_subs.p + c->s_lo, np, c->fac.p, c->fac32.p, changed, c->st);
   FFB_CUDA(cudaMemcpyAsync(c->alpha_fact.ensure(c->ntri), c->alpha.p, c->ntri * sizeof(double),
                            cudaMemcpyDeviceToDevice, c->st));
   std::vector<int> bad(np);
@@ -550,7 +561,7 @@ void launch_asm(ffb_ctx* c, int nc, const double* rvec, const int* flags) {
   }
   line_solve(c->d_subs.p + c->s_lo, c->s_hi - c->s_lo, c->plan, solve_factor(c), c->coef.p, c->N, rvec,
              c->ylocal.p, c->zlocal.p, c->W, nc, flags, c->st, nullptr,
-             c->n_cta ? c->qsync.p : nullptr, c->n_cta);
+             c->n_cta ? c->qsync.p : nullptr, c->n_cta, c->fac32.p);
   if (ev) FFB_CUDA(cudaEventRecord(ev->b, c->st));
 }
 
@@ -862,6 +873,7 @@ int ffb_create(ffb_ctx** out, int device) {
            std::to_string(prop.major) + "." + std::to_string(prop.minor));
     auto c = std::make_unique<ffb_ctx>();
     c->device = device;
+    if (const char* e = std::getenv("FFB_FACTOR_F32")) c->factor_bits = std::atoi(e) ? 32 : 64;
     FFB_CUDA(cudaSetDevice(device));
     FFB_CUDA(cudaStreamCreateWithFlags(&c->own_st, cudaStreamNonBlocking));
     c->st = c->own_st;
@@ -926,6 +938,28 @@ int ffb_debug_time_asm(ffb_ctx* c, int nc, int n, int dbg, double* ms) {
     set_solve_dbg(0);
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+  });
+}
+
+int ffb_set_factor_storage(ffb_ctx* c, int bits) {
+  return guard([&] {
+    check_ctx(c);
+    if (bits != 64 && bits != 32) fail("ffb_set_factor_storage: bits must be 64 or 32");
+    if (bits == c->factor_bits) return;
+    sync(c);
+    c->factor_bits = bits;
+    if (c->have_part) {  // rebuild the resident partition's storage; the next solve refactors
+      c->have_part = false;
+      ensure_partition(c, c->part_px, c->part_py, c->part_ov, c->part_nc);
+    }
+  });
+}
+
+int ffb_get_factor_storage(ffb_ctx* c, int* bits, int* in_use) {
+  return guard([&] {
+    check_ctx(c);
+    if (bits) *bits = c->factor_bits;
+    if (in_use) *in_use = c->fac32.p ? 32 : 64;  // 32 only where the row-group tile solve runs
   });
 }
 

@@ -85,6 +85,7 @@ struct SubInfo {
   long long line_sz;     // doubles per line of the packed factor (packed_line_size(kd))
   long long fac_off;     // offset (doubles) of the subdomain's factor
   long long vec_off;     // offset (doubles) into the per-subdomain vectors
+  long long fac32_off;   // offset (floats) of the subdomain in the single-precision factor copy
 };
 
 struct AxisMap {  // free-rectangle membership along one axis (<= 2 parts)
@@ -108,7 +109,11 @@ SolvePlan solve_plan(int kd_max, int C);
 void line_solve(const SubInfo* d_subs, int nsub, const SolvePlan& pl, const double* fac,
                 const double* coef, size_t N, const double* r, double* ylocal, double* zlocal,
                 int W, int nc, const int* flags, cudaStream_t st,
-                const double* rlocal = nullptr, int* qsync = nullptr, int n_cta = 0);
+                const double* rlocal = nullptr, int* qsync = nullptr, int n_cta = 0,
+                const float* fac32 = nullptr);
+// opt-in single-precision copy of the line inverses streamed by k_line_solve_rt<., float>
+void factor_to_f32(const SubInfo* d_subs, int nsub, const double* fac, float* fac32,
+                   const int2* changed, cudaStream_t st);
 
 // ---- literal Schwarz iteration (ras.cu) ---------------------------------------------------
 void ras_rhs(const SubInfo* d_subs, int nsub, const double* coef, const double* b,

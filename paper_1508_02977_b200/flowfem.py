@@ -63,6 +63,18 @@ class Context:
         _check(self.lib.ffb_set_stream(self._h, C.c_void_p(0 if own else stream_handle),
                                        int(own)))
 
+    def set_factor_storage(self, bits: int):
+        """64 (default): the preconditioner streams the subdomain factors in double. 32: opt-in —
+        the wide-line solve kernel (c3, c4) streams a single-precision copy, half the bytes per
+        application; factorisation, products and the CG stay in double (same 1e-8 parity)."""
+        _check(self.lib.ffb_set_factor_storage(self._h, int(bits)))
+
+    def factor_storage(self):
+        """(requested bits, bits in use with the resident partition)."""
+        b, u = C.c_int(), C.c_int()
+        _check(self.lib.ffb_get_factor_storage(self._h, C.byref(b), C.byref(u)))
+        return b.value, u.value
+
     def close(self):
         if getattr(self, "_h", None):
             self.lib.ffb_destroy(self._h)

@@ -67,6 +67,22 @@ def test_c3_chain_matches_oracle(ctx):
     check(r, g, cfg, ctx)
 
 
+def test_c3_chain_matches_oracle_f32_factor_copy(ctx):
+    """The opt-in single-precision copy of the subdomain factors (ffb_set_factor_storage 32: the
+    solve kernel streams half the bytes; factorisation, products and the CG stay in double) is a
+    different preconditioner, not a different problem: the converged chain meets the same bar."""
+    ctx.set_factor_storage(32)
+    try:
+        r, g, cfg = run_chain("c3", ctx)
+        assert ctx.factor_storage() == (32, 32)
+        check(r, g, cfg, ctx)
+        # the same operator up to 6e-8 per entry: the iteration counts do not move
+        ref_iters = [36, 24, 24, 23, 21, 21, 20, 19, 18, 18, 17]
+        assert all(abs(a - b) <= 2 for a, b in zip(r.stats.iters, ref_iters)), r.stats.iters
+    finally:
+        ctx.set_factor_storage(64)
+
+
 def test_c4_chain_matches_oracle(ctx):
     """c4 (the headline config): 2160x3840, 16x16 subdomains, overlap 4, 10 adaptive passes."""
     r, g, cfg = run_chain("c4", ctx)

@@ -23,9 +23,10 @@ def rand_pair(H, W, seed):
     return f0, f1
 
 
-def solve(t, a, l, px, py, ov, nc):
+def solve(t, a, l, px, py, ov, nc, factor_bits=64):
     ctx = ff.Context(0)
     try:
+        ctx.set_factor_storage(factor_bits)
         s = ff.SchwarzSolver(ctx)
         s.set_terms(ff.DataTerms(t))
         s.set_reg(ff.RegField(a, l))
@@ -117,6 +118,36 @@ def test_row_group_tiles_match_ring_and_oracle(monkeypatch, port, H, W, px, py, 
     for c in range(nc):
         assert rel_l2(u_t[c], u_r[c]) < 1e-9, c
         assert rel_l2(u_t[c], ref_u[c]) < 1e-9, c
+
+
+@pytest.mark.parametrize("H,W,px,py,ov,nc,cluster", [
+    (149, 160, 1, 1, 0, 3, "1"),  # kd 447 (odd, line size 2 mod 4: the copy's padded stride)
+    (139, 150, 1, 1, 0, 3, "1"),  # kd 417
+    (130, 160, 2, 2, 3, 3, "1"),
+    (149, 160, 1, 1, 0, 3, "2"),  # clusters
+    (50, 44, 3, 2, 4, 2, "4"),
+])
+def test_row_group_tiles_f32_factor_copy(monkeypatch, port, H, W, px, py, ov, nc, cluster):
+    """The opt-in single-precision factor copy (ffb_set_factor_storage 32) streamed by the
+    row-group tile kernel: same converged solution as the double factors and the oracle."""
+    f0, f1 = rand_pair(H, W, 11 * H + W)
+    t = port.frames_to_terms(f0, f1, 1.0, 2.5)
+    rng = np.random.default_rng(H * W + 1)
+    ntri = 2 * (W - 1) * (H - 1)
+    a = rng.uniform(20, 1000, ntri)
+    l = np.full(ntri, 1000.0)
+    monkeypatch.setenv("FFB_CLUSTER", cluster)
+    monkeypatch.setenv("FFB_SOLVE", "rt")
+    u_d, it_d, res_d, kind_d = solve(t, a, l, px, py, ov, nc)
+    u_f, it_f, res_f, kind_f = solve(t, a, l, px, py, ov, nc, factor_bits=32)
+    assert kind_d == 2 and kind_f == 2
+    assert res_d <= 1e-12 and res_f <= 1e-12
+    assert abs(it_d - it_f) <= 2
+    ref_u, _, _ = port.cg_solve(t, a, l, nc, 1e-13)
+    for c in range(nc):
+        assert rel_l2(u_f[c], u_d[c]) < 1e-9, c
+        assert rel_l2(u_f[c], ref_u[c]) < 1e-9, c
+    assert not np.array_equal(u_f, u_d)  # the copy really was used
 
 
 def test_tile_solve_deterministic(port):
