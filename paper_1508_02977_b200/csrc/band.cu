@@ -461,12 +461,37 @@ __device__ __forceinline__ void rupd_tile_mma(double* __restrict__ D, int kd, in
                                               int k1, int TU, int TV, int lane) {
   const int g = lane >> 2, t = lane & 3;  // fragment row/col group, thread in group
   const int u0 = 32 * TU, v0 = 32 * TV;
-  double acc[4][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   const bool diag = TU == TV;
+#ifndef FFB_ACCX
+#define FFB_ACCX 1
+#endif
+  // The tile's entries are the accumulators' initial values (FFB_ACCX): D - Z Z^T is formed as
+  // D + (-Z) Z^T in the DMMA chain itself, so all 16 pair loads of the tile are in flight at
+  // once before the first product — one exposed L2 round trip per tile instead of one per
+  // RG row blocks after the products (the RG = 1 / 2 / 4 sweep, profiles/r2_factor_knobs.txt,
+  // shows how much of a tile is that latency) — and no second register set for them.
+  // 16-byte pairs (v even; K is 32-aligned, so a pair is wholly inside or outside it). The
+  // pair at v = u of an even row u also rewrites the row's pad, which nothing reads during the
+  // sweep and pack_line zeroes at its end.
+  double acc[4][4][2];
+  unsigned onmask = 0;
+  auto pair_ptr = [&](int i, int j) {
+    return reinterpret_cast<double2*>(D + prow_off32(u0 + 8 * i + g) + v0 + 8 * j + 2 * t);
+  };
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int u = u0 + 8 * i + g;
+    const bool row_on = u < kd && !(u >= k0 && u < k1);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int v = v0 + 8 * j + 2 * t;
+      const bool on = row_on && !(diag && j > i) && v <= u && (v < k0 || v >= k1);
+      onmask |= on ? 1u << (4 * i + j) : 0u;
+      double2 x = make_double2(0.0, 0.0);
+      if (FFB_ACCX && on) x = *pair_ptr(i, j);
+      acc[i][j][0] = x.x, acc[i][j][1] = x.y;
+    }
+  }
 #pragma unroll 2
   for (int c0 = 0; c0 < nbk; c0 += 4) {
     const double* zc = Z + (c0 + t) * kdp;  // A[m][k] = Z[c0+k][u0+m], B[k][n] = Z[c0+k][v0+n]
@@ -475,17 +500,27 @@ __device__ __forceinline__ void rupd_tile_mma(double* __restrict__ D, int kd, in
     for (int i = 0; i < 4; ++i) a[i] = zc[u0 + 8 * i + g];
 #pragma unroll
     for (int j = 0; j < 4; ++j) b[j] = diag ? a[j] : zc[v0 + 8 * j + g];
+    if (FFB_ACCX) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = -a[i];
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (!diag || j <= i) dmma_8x8x4(acc[i][j], a[i], b[j]);
   }
-  // read-modify-write in 16-byte pairs (v even; K is 32-aligned, so a pair is wholly inside
-  // or outside it). The pair at v = u of an even row u also rewrites the row's pad, which
-  // nothing reads during the sweep and pack_line zeroes at its end. The loads of RG row blocks
-  // are all issued before their stores: written load-store per pair, the compiler keeps the
-  // order (the stores may alias the next loads) and the tile pays one L2 round trip per pair.
+  if (FFB_ACCX) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (onmask >> (4 * i + j) & 1u) *pair_ptr(i, j) = make_double2(acc[i][j][0], acc[i][j][1]);
+    return;
+  }
+  // FFB_ACCX = 0: read-modify-write after the products, RG row blocks of loads before their
+  // stores (written load-store per pair, the compiler keeps the order — the stores may alias
+  // the next loads — and the tile pays one L2 round trip per pair).
 #ifndef FFB_RG
 #define FFB_RG 2
 #endif
@@ -493,28 +528,17 @@ __device__ __forceinline__ void rupd_tile_mma(double* __restrict__ D, int kd, in
 #pragma unroll
   for (int i0 = 0; i0 < 4; i0 += RG) {
     double2 x[RG][4];
-    double2* pp[RG][4];
-    bool on[RG][4];
-#pragma unroll
-    for (int ii = 0; ii < RG; ++ii) {
-      const int i = i0 + ii;
-      const int u = u0 + 8 * i + g;
-      const bool row_on = u < kd && !(u >= k0 && u < k1);
-      double* rowp = D + prow_off32(u);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int v = v0 + 8 * j + 2 * t;
-        on[ii][j] = row_on && !(diag && j > i) && v <= u && (v < k0 || v >= k1);
-        pp[ii][j] = reinterpret_cast<double2*>(rowp + v);
-        x[ii][j] = on[ii][j] ? *pp[ii][j] : make_double2(0.0, 0.0);
-      }
-    }
 #pragma unroll
     for (int ii = 0; ii < RG; ++ii)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (on[ii][j])
-          *pp[ii][j] = make_double2(x[ii][j].x - acc[i0 + ii][j][0], x[ii][j].y - acc[i0 + ii][j][1]);
+        x[ii][j] = (onmask >> (4 * (i0 + ii) + j) & 1u) ? *pair_ptr(i0 + ii, j) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int ii = 0; ii < RG; ++ii)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (onmask >> (4 * (i0 + ii) + j) & 1u)
+          *pair_ptr(i0 + ii, j) = make_double2(x[ii][j].x - acc[i0 + ii][j][0], x[ii][j].y - acc[i0 + ii][j][1]);
   }
 }
 
