@@ -83,6 +83,17 @@ def test_c3_chain_matches_oracle_f32_factor_copy(ctx):
         ctx.set_factor_storage(64)
 
 
+def test_c4_chain_matches_oracle_f32_factor_copy(ctx):
+    """The headline config with the opt-in single-precision factor copy: same parity bar."""
+    ctx.set_factor_storage(32)
+    try:
+        r, g, cfg = run_chain("c4", ctx)
+        assert ctx.factor_storage() == (32, 32)
+        check(r, g, cfg, ctx)
+    finally:
+        ctx.set_factor_storage(64)
+
+
 def test_c4_chain_matches_oracle(ctx):
     """c4 (the headline config): 2160x3840, 16x16 subdomains, overlap 4, 10 adaptive passes."""
     r, g, cfg = run_chain("c4", ctx)
