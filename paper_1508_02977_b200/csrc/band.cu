@@ -1043,13 +1043,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Waits are bounded: a wait that has not completed after ~2e11 cycles (about 100 s — four
+// orders of magnitude beyond the longest legitimate one) traps, so a protocol error ends the
+// process with a CUDA error instead of hanging it (the fast path, a completed phase on the
+// first try, does not read the clock).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
+      ".reg .s64 t0, t1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra DONE_%=;\n"
+      "mov.u64 t0, %%clock64;\n"
       "WAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
-      "@!P1 bra WAIT_%=;\n"
+      "@P1 bra DONE_%=;\n"
+      "mov.u64 t1, %%clock64;\n"
+      "sub.s64 t1, t1, t0;\n"
+      "setp.lt.s64 P1, t1, 200000000000;\n"
+      "@P1 bra WAIT_%=;\n"
+      "trap;\n"
+      "DONE_%=:\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(0x989680u)  // suspend-time hint: sleep in the wait instead of polling
       : "memory");
@@ -1181,14 +1195,34 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   return v;
 }
 
+// persistent queue: a backward task waits for its subdomain's forward chains (bounded, as above)
+__device__ __forceinline__ void wait_forward_done(const int* p, int need) {
+  if (ld_acquire_gpu(p) >= need) return;
+  const long long t0 = clock64();
+  while (ld_acquire_gpu(p) < need) {
+    __nanosleep(100);
+    if (clock64() - t0 > 200000000000LL) __trap();
+  }
+}
+
 // wait with cluster-scope acquire: pairs with remote release-arrivals from the other CTAs
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
+      ".reg .s64 t0, t1;\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONEC_%=;\n"
+      "mov.u64 t0, %%clock64;\n"
       "WAITC_%=:\n"
       "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAITC_%=;\n"
+      "@P1 bra DONEC_%=;\n"
+      "mov.u64 t1, %%clock64;\n"
+      "sub.s64 t1, t1, t0;\n"
+      "setp.lt.s64 P1, t1, 200000000000;\n"
+      "@P1 bra WAITC_%=;\n"
+      "trap;\n"
+      "DONEC_%=:\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
@@ -1392,7 +1426,7 @@ __global__ void __launch_bounds__(kST, 1)
   if (PERSIST && phase == 1) {  // both forward chains of this subdomain are done
     if (tid == 0) {
       const int need = (s.m > 0 ? 1 : 0) + (s.L - 1 - s.m > 0 ? 1 : 0);
-      while (ld_acquire_gpu(qsync + 1 + sub) < need) __nanosleep(100);
+      wait_forward_done(qsync + 1 + sub, need);
     }
     compute_bar();
   }
@@ -1979,7 +2013,7 @@ __global__ void __launch_bounds__(kST, 1)
     if (PERSIST && phase == 1) {  // both forward chains of this subdomain are done
       if (tid == 0) {
         const int need = (s.m > 0 ? 1 : 0) + (s.L - 1 - s.m > 0 ? 1 : 0);
-        while (ld_acquire_gpu(qsync + 1 + sub) < need) __nanosleep(100);
+        wait_forward_done(qsync + 1 + sub, need);
       }
       compute_bar();
     }
