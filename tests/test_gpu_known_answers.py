@@ -249,3 +249,103 @@ def test_dirichlet_rows_are_eliminated_into_the_rhs(ctx):
     r = ff.spmv(full, xf.ravel(), ctx) - full.rhs
     rfree = r.reshape(-1, nc)[free]
     assert np.max(np.abs(rfree)) <= 1e-8 * np.max(np.abs(full.rhs))
+
+
+# ------------------------------------------------------------------ test_pipeline.cpp
+def pattern_frame(H, W, sx=0.0, sy=0.0):
+    """fixtures.hpp:23-33: a two-sinusoid texture clamped to [0, 1], shifted by (sx, sy)."""
+    y, x = np.mgrid[0:H, 0:W].astype(float)
+    x, y = x - sx, y - sy
+    v = (0.45 + 0.25 * np.sin(2 * np.pi * x / 7.3 + 1.1) * np.cos(2 * np.pi * y / 9.7)
+         + 0.15 * np.sin(2 * np.pi * (x + y) / 13.1))
+    return np.clip(v, 0.0, 1.0)
+
+
+def smooth_frame(H, W, sx, sy):
+    """test_pipeline.cpp:24-35: long-wavelength texture bounded to [0.1, 0.7]."""
+    y, x = np.mgrid[0:H, 0:W].astype(float)
+    x, y = x - sx, y - sy
+    return (0.4 + 0.2 * np.sin(2 * np.pi * x / 11.3 + 0.7) * np.cos(2 * np.pi * y / 14.7)
+            + 0.1 * np.sin(2 * np.pi * (x + y) / 17.9))
+
+
+def const_truth(H, W, tu, tv):
+    return ff.FloField(np.full((H, W), tu, np.float32), np.full((H, W), tv, np.float32))
+
+
+def small_config(**kw):
+    # test_pipeline.cpp:37-47: [0, 1] frames, alpha0 = lambda0 = 0.05, 2x2 parts, overlap 5, no
+    # adaptation (here the converged solve the reference's 15 Schwarz iterations approach)
+    return ff.RunConfig(alpha0=0.05, lambda0=0.05, parts=4, overlap=5, adapt=False, adapt_iters=0,
+                        **kw)
+
+
+def test_plain_translation_is_recovered(ctx):
+    # test_pipeline.cpp:55-67
+    H = W = 48
+    r = ff.run_on_frames(pattern_frame(H, W), pattern_frame(H, W, 1.0, 0.0), small_config(), ctx)
+    m = ff.compute_metrics(r.flow, const_truth(H, W, 1.0, 0.0), ctx)
+    assert m.valid == H * W
+    assert m.ee < 0.3
+    assert m.aae_deg < 8.0
+
+
+def test_modelling_illumination_pays_off_under_a_gain(ctx):
+    # test_pipeline.cpp:69-83 (acceptance criterion 7): brightness x1.2, shift (0.25, 0.1)
+    H = W = 48
+    f0 = smooth_frame(H, W, 0.0, 0.0)
+    f1 = np.clip(1.2 * smooth_frame(H, W, 0.25, 0.1), 0.0, 1.0)
+    truth = const_truth(H, W, 0.25, 0.1)
+    on = ff.run_on_frames(f0, f1, ff.RunConfig(alpha0=0.05, lambda0=5.0, parts=4, overlap=5,
+                                               adapt=False, adapt_iters=0, illumination=True), ctx)
+    off = ff.run_on_frames(f0, f1, ff.RunConfig(alpha0=0.05, lambda0=5.0, parts=4, overlap=5,
+                                                adapt=False, adapt_iters=0, illumination=False), ctx)
+    ee_on = ff.compute_metrics(on.flow, truth, ctx).ee
+    ee_off = ff.compute_metrics(off.flow, truth, ctx).ee
+    assert ee_on < 0.6 * ee_off
+
+
+# ------------------------------------------------------------------ test_linsolve.cpp
+def dense_of(s):
+    A = np.zeros((s.n, s.n))
+    for r in range(s.n):
+        A[r, s.cols[s.row_ptr[r]:s.row_ptr[r + 1]]] = s.vals[s.row_ptr[r]:s.row_ptr[r + 1]]
+    return A
+
+
+def test_refactorization_reuses_the_symbolic_pattern(ctx):
+    # test_linsolve.cpp:135-158: analyze once, factorize twice with new values of one pattern
+    H = W = 9
+    terms = ff.frames_to_terms(255.0 * rand_image(H, W, 17), 255.0 * rand_image(H, W, 18), 1.0, 2.5, ctx)
+    reg = ff.uniform_reg(W, H, 80.0, 60.0)
+    s = ff.assemble(terms, reg, 3, ctx=ctx)
+    chol = ff.SparseCholesky(ctx)
+    chol.analyze(s)
+    chol.factorize(s, 2)
+    x0 = chol.solve(s.rhs)
+    reg.alpha *= 0.25  # same pattern, new values
+    s = ff.assemble(terms, reg, 3, ctx=ctx)
+    chol.factorize(s, 2)
+    x1 = chol.solve(s.rhs)
+    fresh = ff.SparseCholesky(ctx)
+    fresh.analyze(s)
+    fresh.factorize(s, 1)
+    assert np.array_equal(x1, fresh.solve(s.rhs))
+    xd = np.linalg.solve(dense_of(s), s.rhs)
+    assert np.linalg.norm(x1 - xd) / np.linalg.norm(xd) < 1e-10
+    assert np.linalg.norm(x0 - x1) / np.linalg.norm(x1) > 1e-6  # the values really changed
+
+
+def test_strongly_mixed_scales_stay_solvable(ctx):
+    # test_linsolve.cpp:224-237: lambda = 1e12 next to alpha = 1e3 (condition ~1e9): backward
+    # stability is the guarantee, forward agreement with the dense solve only to kappa * eps
+    H = W = 8
+    terms = ff.frames_to_terms(255.0 * rand_image(H, W, 33), 255.0 * rand_image(H, W, 34), 1.0, 2.5, ctx)
+    s = ff.assemble(terms, ff.uniform_reg(W, H, 1e3, 1e12), 3, ctx=ctx)
+    rep = ff.SolveReport()
+    x = ff.solve(s, ff.SolverConfig(), rep, ctx=ctx)
+    A = dense_of(s)
+    scale = np.linalg.norm(A, np.inf) * np.linalg.norm(x, np.inf) + np.linalg.norm(s.rhs, np.inf)
+    assert np.linalg.norm(A @ x - s.rhs, np.inf) < 1e-12 * scale
+    xd = np.linalg.solve(A, s.rhs)
+    assert np.linalg.norm(x - xd) / np.linalg.norm(xd) < 1e-3
