@@ -1324,7 +1324,14 @@ __global__ void __launch_bounds__(kST, 1)
   }
   int* rlos = reinterpret_cast<int*>(smem_raw + 256);  // row_lo(c) for c = 0..C (C > 1)
   if (C > 1 && tid <= C) rlos[tid] = row_lo(tid, C, subs[(blockIdx.x / C) >> 1].kd, rc);
-  for (int j = tid; j < 2 * kd_max; j += kST) xbuf[j] = 0.0;
+  // Everything after the header starts at zero: x of "line -1" (xbuf), and the slots the row
+  // loop reads without a mask — the operand pair past an odd line width (wv[kd], multiplied by
+  // a zeroed entry: a NaN pattern left in shared memory by an earlier kernel made 0 * NaN and
+  // stalled the CG on NaN residuals, seen with kd 447 on 4-CTA clusters), the ring stages.
+  {
+    const int nz = stages * cap + (ncs + 5 + 2 * C) * kd_max;  // colpart wv yrow xbuf red dcorr
+    for (int j = tid; j < nz; j += kST) stage0[j] = 0.0;
+  }
   if (C > 1) cl_sync(); else __syncthreads();  // barriers initialised cluster-wide
 
   // ------------------------------------------------------------------ producer warp
@@ -2305,6 +2312,10 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     return rl ? rl[static_cast<long long>(l) * kd + j] : r[op_r[j] + static_cast<long long>(l) * r_step];
   };
   auto b_at = [&](int l, int j) { return coef[op_b[j] + static_cast<long long>(l) * b_step]; };
+  // the line stages, operands and contribution slots start at zero (no NaN pattern of an earlier
+  // kernel's shared memory can meet a masked-out product)
+  for (int j = tid; j < 2 * stage_doubles + 2 * kdp_max; j += kTileThreads) stage[j] = 0.0;
+  for (int j = tid; j < n_own * (nt + 1) * 32; j += kTileThreads) slots[j] = 0.0;
   cl_sync();  // barriers and op_r / op_b initialised (cluster-wide: before any remote arrival)
 
   // my tile of line step t -> stage t & 1 (one bulk copy per warp: the warp rewrites only its

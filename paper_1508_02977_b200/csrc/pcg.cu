@@ -77,7 +77,9 @@ __device__ void apply_stage(PcgCtl* ctl, int stage, double s, double s2) {
         ctl->done = 1;
       } else {
         ctl->res = sqrt(s2) / ctl->normb;
-        ctl->done = ctl->res <= ctl->tol ? 1 : 0;
+        // a NaN residual can never pass the test: stop at once (the host reports
+        // "no convergence ... relative residual nan") instead of iterating to max_iters
+        ctl->done = (ctl->res <= ctl->tol || ctl->res != ctl->res) ? 1 : 0;
       }
       break;
     case kStPap:
@@ -87,7 +89,7 @@ __device__ void apply_stage(PcgCtl* ctl, int stage, double s, double s2) {
       ctl->rr = s;
       ctl->res = sqrt(s) / ctl->normb;
       ctl->iters = ctl->k;
-      if (ctl->res <= ctl->tol || ctl->k >= ctl->max_iters) ctl->done = 1;
+      if (ctl->res <= ctl->tol || ctl->k >= ctl->max_iters || ctl->res != ctl->res) ctl->done = 1;
       break;
     case kStRz:
       ctl->rz_old = ctl->rz;
