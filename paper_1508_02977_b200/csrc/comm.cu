@@ -179,8 +179,14 @@ struct LocalComm final : Comm {
     }
     hub->post[rank] = const_cast<double*>(send);
     hub->barrier();
+    // Copies go on the rank's own stream and are waited for before the second rendezvous: a
+    // device-to-device cudaMemcpy does not block the host and runs on the legacy stream, which
+    // the contexts' non-blocking streams are not ordered after — the peer could overwrite its
+    // buffer, or this rank's next kernel read the destination, before the copy had landed (a
+    // rare glitch of one CG scalar or halo: seen as a 1e-8 difference once in ~20 suite runs).
     for (int q = 0; q < world; ++q)
-      FFB_CUDA(cudaMemcpy(stage + q * n, hub->post[q], n * sizeof(double), cudaMemcpyDefault));
+      FFB_CUDA(cudaMemcpyAsync(stage + q * n, hub->post[q], n * sizeof(double), cudaMemcpyDefault, st));
+    FFB_CUDA(cudaStreamSynchronize(st));
     hub->barrier();  // every rank holds every buffer: now they may be overwritten
     k_sum_ranks<<<64, 256, 0, st>>>(stage, world, n, recv);
     FFB_LAUNCHED();
@@ -195,12 +201,13 @@ struct LocalComm final : Comm {
       bool found = false;
       for (const Xfer& t : hub->xf[x[k].peer])
         if (t.send && t.peer == rank && t.n == x[k].n) {
-          FFB_CUDA(cudaMemcpy(x[k].ptr, t.ptr, t.n * sizeof(double), cudaMemcpyDefault));
+          FFB_CUDA(cudaMemcpyAsync(x[k].ptr, t.ptr, t.n * sizeof(double), cudaMemcpyDefault, st));
           found = true;
           break;
         }
       if (!found) fail("schwarz.comm: unmatched halo receive");
     }
+    FFB_CUDA(cudaStreamSynchronize(st));  // received before the senders may reuse their buffers
     hub->barrier();
   }
   void allgather_rows(double* buf, const size_t* off, const size_t* cnt,
@@ -210,8 +217,9 @@ struct LocalComm final : Comm {
     hub->barrier();
     for (int q = 0; q < world; ++q)
       if (q != rank && cnt[q])
-        FFB_CUDA(cudaMemcpy(buf + off[q], hub->post[q] + off[q], cnt[q] * sizeof(double),
-                            cudaMemcpyDefault));
+        FFB_CUDA(cudaMemcpyAsync(buf + off[q], hub->post[q] + off[q], cnt[q] * sizeof(double),
+                                 cudaMemcpyDefault, st));
+    FFB_CUDA(cudaStreamSynchronize(st));
     hub->barrier();
   }
 };
