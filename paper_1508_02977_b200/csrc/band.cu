@@ -2312,9 +2312,9 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     return rl ? rl[static_cast<long long>(l) * kd + j] : r[op_r[j] + static_cast<long long>(l) * r_step];
   };
   auto b_at = [&](int l, int j) { return coef[op_b[j] + static_cast<long long>(l) * b_step]; };
-  // the line stages, operands and contribution slots start at zero (no NaN pattern of an earlier
-  // kernel's shared memory can meet a masked-out product)
-  for (int j = tid; j < 2 * stage_doubles + 2 * kdp_max; j += kTileThreads) stage[j] = 0.0;
+  // the operands and contribution slots start at zero (no NaN pattern of an earlier kernel's
+  // shared memory can meet a zero operand; the tile loads themselves are masked by selection)
+  for (int j = tid; j < 2 * kdp_max; j += kTileThreads) wv[j] = 0.0;
   for (int j = tid; j < n_own * (nt + 1) * 32; j += kTileThreads) slots[j] = 0.0;
   cl_sync();  // barriers and op_r / op_b initialised (cluster-wide: before any remote arrival)
 
