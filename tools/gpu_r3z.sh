@@ -1,5 +1,5 @@
 # repeat the whole GPU suite until the intermittent failure shows; keep the failing log
-for i in $(seq 1 14); do
+for i in $(seq 1 8); do
   timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/r3z_run.log 2>&1
   rc=$?
   echo "run $i rc $rc: $(tail -1 gpurun_out/r3z_run.log)"
