@@ -18,15 +18,22 @@
 // half the bytes per application of a banded Cholesky factor of the same matrix (which must
 // hold the filled-in B_l L^-T blocks), and the only sequential dependency is line to line.
 //
-// Factor (K5, one CTA per subdomain): per line, build D_l in an L2-resident kd x kd scratch
-// and invert it in place with a blocked symmetric sweep (Gauss-Jordan for SPD):
-//     pivot block K (one warp, in registers): Lc = chol(A_KK), Li = Lc^-1, Z = A_RK Li^T,
-//     A_RR -= Z Z^T (8x8 register tiles, FP64 FMA), A_RK <- Z Li, A_KK <- -Li^T Li,
+// Factor (K5, k_line_factor: a 4- or 8-CTA cluster per (subdomain, chain) of the twisted
+// factorisation): per line, build D_l in place in the packed factor storage (L2-resident while
+// it is swept) and invert it with a blocked symmetric sweep (Gauss-Jordan for SPD):
+//     pivot block K (two warps, in registers, one step ahead): Lc = chol(A_KK), Li = Lc^-1,
+//     Z = A_RK Li^T, A_RR -= Z Z^T (32x32 warp tiles on the FP64 tensor cores, DMMA m8n8k4),
+//     A_RK <- Z Li, A_KK <- -Li^T Li,
 // which leaves -D^{-1}; the flops equal a banded Cholesky's (n kd^2 / 2 FMAs).
-// Solve (K6, one CTA per subdomain): the packed rows of each line are streamed through a
-// shared-memory ring with cp.async.bulk + mbarrier (TMA bulk copies); each warp takes whole
-// rows, producing the row dot products and, for the symmetric half, per-lane column partial
-// sums in registers, combined in a fixed order (deterministic).
+// Solve (K6), three kernels by regime, every sum in a fixed order (deterministic):
+//   k_line_solve_tile — narrow lines (c1, c2), latency regime: one 32x32 register tile per warp
+//     across a cluster, operands and partial sums over distributed shared memory;
+//   k_line_solve_rt   — lines up to 448 unknowns (c3, c4), bandwidth regime: the packed rows
+//     stream through a shared-memory ring (cp.async.bulk + mbarrier) in whole 16-row groups and
+//     are multiplied as 16x32 register tiles; one CTA per chain (persistent task queue when
+//     chains > SMs) or a 2-/4-CTA cluster per chain; optional single-precision factor copy;
+//   k_line_solve      — wider lines (c5) and 8-CTA clusters: the same ring with row batches,
+//     each warp taking whole rows (row dots + per-lane column partials).
 #include "ffb_internal.cuh"
 
 #include <mutex>
